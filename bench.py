@@ -1,0 +1,435 @@
+"""Benchmark: particles resampled per second (BASELINE.json metric) on B200.
+
+Workload (BASELINE.json configs[1]): all five resamplers -- multinomial,
+stratified, systematic, Metropolis(B=32), rejection(sup_w = max w) -- at
+N = 2^20 on i.i.d. log-normal (sigma = 1) weights, float32 AND float64.  One
+step = the ten deliveries (resample + permute to an in-place-valid ancestry,
+the timed region of the reference's bench.py:155-161), i.e. 10 * 2^20
+particles.  Weights are resident in HBM before timing; L2 is flushed
+(256 MiB write) before every delivery and every delivery is timed with CUDA
+events on the launching stream; the flush is outside the timed region.
+
+Also reported (north-star targets): systematic delivery
+and Metropolis(B=32) at N = 2^24 float32 against the measured HBM roofline.
+
+`--impl reference` times the reference algorithm on the host: the oracle
+port (oracle/pfr_oracle.py, NumPy + the Python chain walk, like the reference),
+the ten deliveries spread over a process pool using every host core.
+
+Multi-GPU (torchrun): every rank runs the same per-GPU workload on its own
+independent filters (no communication, scaling "weak"); value = all ranks'
+particles / max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALGS = ("multinomial", "stratified", "systematic", "metropolis", "rejection")
+DTYPES = ("f32", "f64")
+METRIC = "particles resampled/sec vs N per resampler (1/2/4/8 B200); % HBM roofline"
+N_DEFAULT = 1 << 20
+B_STEPS = 32
+SIGMA = 1.0
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def log_normal_weights(n, seed, dtype=np.float64):
+    g = np.random.default_rng(seed)
+    lw = g.normal(0.0, SIGMA, n)
+    return np.exp(lw - lw.max()).astype(dtype)
+
+
+def algorithmic_bytes(alg, s, n, trips=None):
+    """bytes per particle x N for one delivery's dominant kernel."""
+    if alg in ("systematic", "stratified", "multinomial"):
+        return (s + 4) * n
+    if alg == "metropolis":
+        return (s + 4 + B_STEPS * s) * n
+    if alg == "rejection":
+        return (s + 4 + trips * s) * n
+    raise ValueError(alg)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler
+
+
+class Clocks:
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (host)
+
+
+def _ref_delivery(args):
+    alg, dt, n, seed = args
+    from oracle import pfr_oracle as orc
+
+    w = log_normal_weights(n, seed, np.float32 if dt == "f32" else np.float64)
+    t0 = time.perf_counter()
+    orc.deliver(w, alg, seed, (1,), b=B_STEPS, sup_w=float(w.max()))
+    return time.perf_counter() - t0
+
+
+def cpu_step(n, pool, seed=0):
+    """One step of the workload on the host; returns wall seconds."""
+    jobs = [(alg, dt, n, seed + i) for i, (alg, dt) in enumerate((a, d) for a in ALGS for d in DTYPES)]
+    t0 = time.perf_counter()
+    if pool is None:
+        for j in jobs:
+            _ref_delivery(j)
+    else:
+        list(pool.map(_ref_delivery, jobs))
+    return time.perf_counter() - t0
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = min(os.cpu_count() or 1, len(ALGS) * len(DTYPES))
+    n = args.n
+    with mp.get_context("spawn").Pool(cores) as pool:
+        for _ in range(args.warmup):
+            cpu_step(n, pool)
+        times = [cpu_step(n, pool) for _ in range(args.steps)]
+    per = sum(times) / len(times)
+    units = len(ALGS) * len(DTYPES) * n
+    value = units / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32,f64", "data": "synthetic log-normal weights",
+        "config": workload_config(n, world),
+        "cpu_baseline": {"value": value, "unit": "particles/s", "cores": cores, "kind": "port",
+                         "sample": f"the full step: 5 resamplers x (f32, f64) at N=2^{int(math.log2(n))}, "
+                                   f"oracle/pfr_oracle.py (NumPy + Python chain walk) over a {cores}-process pool"},
+        "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(n, world):
+    return {"workload": "configs[1]: multinomial/stratified/systematic/metropolis(B=32)/rejection(sup_w=max w), "
+                        f"N=2^{int(math.log2(n))}, f32 and f64, log-normal sigma={SIGMA}",
+            "n_particles": n, "deliveries_per_step": len(ALGS) * len(DTYPES), "metropolis_B": B_STEPS,
+            "rng": "own Philox4x32-10 (rng_mode='philox')", "l2": "flushed (256 MiB write) before every delivery",
+            "parallelism": f"replicas x{world} (independent filters per GPU)"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-targets", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1301_4019_b200 import _build
+
+    _build.build()
+    import paper_1301_4019_b200 as pf
+    from paper_1301_4019_b200 import _lib as L
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    pf.config.check = False  # validation kernels still run; statuses are read after timing
+    hbm, peak_src = peaks()
+    n = args.n
+
+    weights = {}
+    for i, dt in enumerate(DTYPES):
+        w = log_normal_weights(n, 1000 * rank + i, np.float32 if dt == "f32" else np.float64)
+        weights[dt] = torch.from_numpy(w).to(dev)
+    sup = {dt: float(weights[dt].max()) for dt in DTYPES}
+    trips = {dt: sup[dt] * n / float(weights[dt].double().sum()) for dt in DTYPES}
+    outs = {dt: torch.empty(n, dtype=torch.int32, device=dev) for dt in DTYPES}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    cfgs = {alg: pf.ResamplerConfig(alg, b=B_STEPS, sup_w=None) for alg in ALGS}
+
+    def delivery(alg, dt, rs, parts=None):
+        """One delivery; `parts` collects (name, start, end) event pairs per sub-call."""
+        w = weights[dt]
+        if alg in ("systematic", "stratified"):
+            return pf.deliver(w, cfgs[alg], rs, index_dtype=torch.int32, out=outs[dt])
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        if alg == "multinomial":
+            a = pf.multinomial_ancestors(w, rs, index_dtype=torch.int32)
+        elif alg == "metropolis":
+            a = pf.metropolis_ancestors(w, B_STEPS, rs, index_dtype=torch.int32)
+        else:
+            a = pf.rejection_ancestors(w, sup[dt], rs, index_dtype=torch.int32)
+        e1.record(stream)
+        if parts is not None:
+            parts.append((f"{alg}/{dt}", e0, e1))
+        return pf.permute_parallel(a, index_dtype=torch.int32)
+
+    def timed_step(step, parts):
+        evs = []
+        for i, alg in enumerate(ALGS):
+            for j, dt in enumerate(DTYPES):
+                flush.zero_()
+                s0 = torch.cuda.Event(enable_timing=True)
+                s1 = torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                delivery(alg, dt, pf.RngStream(step, (rank, i, j)), parts)
+                s1.record(stream)
+                evs.append((f"{alg}/{dt}", s0, s1))
+        return evs
+
+    for s in range(args.warmup):
+        timed_step(10_000 + s, None)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    L.lib().pfr_launch_count(1)
+    per_delivery = {}
+    kernel_parts = {}
+    with Clocks(local) as clk:
+        all_evs, all_parts = [], []
+        for s in range(args.steps):
+            parts = []
+            all_evs.append(timed_step(s, parts))
+            all_parts.append(parts)
+        torch.cuda.synchronize()
+    launches = int(L.lib().pfr_launch_count(1))
+    total_ms = 0.0
+    for evs in all_evs:
+        for name, a, b in evs:
+            t = a.elapsed_time(b)
+            per_delivery.setdefault(name, []).append(t)
+            total_ms += t
+    for parts in all_parts:
+        for name, a, b in parts:
+            kernel_parts.setdefault(name, []).append(a.elapsed_time(b))
+    status = int(L.status_word().item())
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    units_per_step = len(ALGS) * len(DTYPES) * n
+    value = world * units_per_step / (ms_per_step * 1e-3)
+
+    # dominant kernel of the step (largest share), roofline from live events
+    dom_name, dom_ms = None, 0.0
+    for name, ts in kernel_parts.items():
+        m = sum(ts) / len(ts)
+        if m > dom_ms:
+            dom_name, dom_ms = name, m
+    # deliveries that are a single fused library call count as one kernel group
+    for name, ts in per_delivery.items():
+        if name.split("/")[0] in ("systematic", "stratified"):
+            m = sum(ts) / len(ts)
+            if m > dom_ms:
+                dom_name, dom_ms = name, m
+    alg, dt = dom_name.split("/")
+    s_bytes = 4 if dt == "f32" else 8
+    alg_bytes = algorithmic_bytes(alg, s_bytes, n, trips[dt])
+    achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
+
+    # ---------------- e2e: host buffers through the public API ----------------
+    host_w = {dt: weights[dt].cpu().pin_memory() for dt in DTYPES}
+    host_c = {dt: torch.empty(n, dtype=torch.int32).pin_memory() for dt in DTYPES}
+    dev_w = {dt: torch.empty_like(weights[dt]) for dt in DTYPES}
+    h2d = d2h = 0
+    e2e_ms = 0.0
+    for s in range(args.warmup + args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        e0.record(stream)
+        for i, alg in enumerate(ALGS):
+            for j, dt in enumerate(DTYPES):
+                dev_w[dt].copy_(host_w[dt], non_blocking=True)
+                w_saved = weights[dt]
+                weights[dt] = dev_w[dt]
+                c = delivery(alg, dt, pf.RngStream(50_000 + s, (rank, i, j)))
+                weights[dt] = w_saved
+                host_c[dt].copy_(c, non_blocking=True)
+                if s == args.warmup:
+                    h2d += dev_w[dt].numel() * dev_w[dt].element_size()
+                    d2h += c.numel() * c.element_size()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if s >= args.warmup:
+            e2e_ms += e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * units_per_step / (e2e_ms / args.steps * 1e-3)
+
+    # ---------------- north-star targets: N = 2^24 float32 ----------------
+    targets = None
+    if not args.no_targets:
+        targets = north_star_targets(pf, torch, dev, stream, flush, hbm)
+
+    # ---------------- CPU baseline (rank 0, N=1 only) ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import multiprocessing as mp
+
+        cores = min(os.cpu_count() or 1, len(ALGS) * len(DTYPES))
+        with mp.get_context("spawn").Pool(cores) as pool:
+            cpu_s = cpu_step(n, pool)
+        cpu = {"value": units_per_step / cpu_s, "unit": "particles/s", "cores": cores, "kind": "port",
+               "sample": f"one step (5 resamplers x f32/f64 at N=2^{int(math.log2(n))}) of the oracle port "
+                         f"(NumPy + Python chain walk, like the reference), {cores} processes, {cpu_s:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32,f64 weights; f64 positions; int32 indices",
+            "data": "synthetic i.i.d. log-normal weights (sigma=1), resident in HBM",
+            "config": workload_config(n, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None, "kernel": dom_name,
+                         "algorithmic_bytes": alg_bytes, "kernel_ms": dom_ms, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "particles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "per_delivery_ms": {k: sum(v) / len(v) for k, v in per_delivery.items()},
+            "status_bits": status,
+            "targets": targets,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def north_star_targets(pf, torch, dev, stream, flush, hbm, reps=10):
+    n = 1 << 24
+    w = torch.from_numpy(log_normal_weights(n, 424242, np.float32)).to(dev)
+    c = torch.empty(n, dtype=torch.int32, device=dev)
+    a = torch.empty(n, dtype=torch.int32, device=dev)
+    cfg = pf.ResamplerConfig("systematic")
+    out = {}
+
+    def timeit(fn):
+        ts = []
+        for r in range(reps + 3):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn(r)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if r >= 3:
+                ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    t = timeit(lambda r: pf.deliver(w, cfg, pf.RngStream(r), index_dtype=torch.int32, out=c))
+    b = (4 + 4) * n
+    out["systematic_delivery_2^24_f32"] = {"us": t * 1e3, "particles_per_s": n / (t * 1e-3),
+                                           "algorithmic_bytes": b, "achieved_gbs": b / (t * 1e-3) / 1e9,
+                                           "frac": b / (t * 1e-3) / 1e9 / hbm, "target_frac": 0.70}
+    t = timeit(lambda r: pf.metropolis_ancestors(w, B_STEPS, pf.RngStream(r), index_dtype=torch.int32))
+    b = (4 + 4 + B_STEPS * 4) * n
+    out["metropolis_B32_2^24_f32_kernel"] = {"us": t * 1e3, "particles_per_s": n / (t * 1e-3),
+                                             "algorithmic_bytes": b, "achieved_gbs": b / (t * 1e-3) / 1e9,
+                                             "frac": b / (t * 1e-3) / 1e9 / hbm, "target_frac": 0.70}
+    cfgm = pf.ResamplerConfig("metropolis", b=B_STEPS)
+    t = timeit(lambda r: pf.deliver(w, cfgm, pf.RngStream(r), index_dtype=torch.int32))
+    out["metropolis_B32_2^24_f32_delivery"] = {"us": t * 1e3, "particles_per_s": n / (t * 1e-3)}
+    del w, c, a
+    return out
+
+
+if __name__ == "__main__":
+    main()

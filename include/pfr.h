@@ -1,0 +1,229 @@
+/*
+ * pfr.h -- C ABI of the B200 resampling library (libpfr.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `pfresample`
+ * (paths relative to /root/reference/pkg/src/pfresample).  Each entry point
+ * names the reference function it replaces.  Conventions:
+ *
+ *   - all array arguments are DEVICE pointers (CUDA global memory, 16-byte
+ *     aligned); scalars are passed by value;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream); every
+ *     call only ENQUEUES work on that stream and returns without synchronising;
+ *   - `ws`/`ws_bytes` is caller-owned scratch sized by pfr_workspace_bytes();
+ *     the library never allocates device memory on the hot path;
+ *   - inputs are never written (the reference never mutates inputs,
+ *     SPEC.md:371); outputs are caller-allocated;
+ *   - indices are int32 on output (N < 2^31); index inputs may be int32 or
+ *     int64 (`idx_dtype`);
+ *   - data-dependent validation (non-finite / negative / all-zero weights,
+ *     out-of-range ancestries, ...) is OR-ed into the device word `*status`
+ *     (PFR_ST_* bits; never cleared by the library).  The host reads it when
+ *     it synchronises and raises the reference's ValueError / RuntimeError;
+ *   - the return value is 0 (PFR_OK) or a PFR_E_* code for argument/launch
+ *     errors detectable on the host; pfr_last_error() returns a thread-local
+ *     message for the last failure.
+ */
+#ifndef PFR_H_
+#define PFR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFR_ABI_VERSION 1
+
+/* element types */
+enum pfr_dtype { PFR_F32 = 0, PFR_F64 = 1, PFR_I32 = 2, PFR_I64 = 3 };
+
+/* accumulation precision for weight scans/positions */
+enum pfr_accum {
+  PFR_ACC_F64 = 0,    /* positions and carries in float64 (default; fp32 is storage only) */
+  PFR_ACC_NATIVE = 1  /* accumulate in the weight dtype, like the reference's np.cumsum */
+};
+/* OR-ed into pfr_scan's `accum`: repair ulp-level non-monotonicity with an
+ * exact running max (only meaningful for non-negative inputs such as weights) */
+#define PFR_SCAN_MONOTONE 0x100
+
+/* where the random draws come from */
+enum pfr_rng_mode {
+  PFR_RNG_PHILOX = 0, /* own Philox4x32-10 keyed by derive_seed(seed, *ids) */
+  PFR_RNG_NUMPY = 1,  /* exact replay of numpy Philox4x64-10 as RngStream.generator() */
+  PFR_RNG_ARRAYS = 2  /* draws supplied by the caller in device arrays */
+};
+
+/* status bits OR-ed into *status by the kernels */
+enum pfr_status_bits {
+  PFR_ST_NONFINITE = 1u << 0,      /* weight/log-weight NaN or +-inf (+inf only for log-weights) */
+  PFR_ST_NEGATIVE = 1u << 1,       /* negative weight */
+  PFR_ST_POSITIVE = 1u << 2,       /* SET when at least one weight > 0 */
+  PFR_ST_RANGE = 1u << 3,          /* ancestry entry outside [0, N) */
+  PFR_ST_REPAIRED = 1u << 4,       /* monotone repair of O was needed (informational) */
+  PFR_ST_OVERFLOW = 1u << 5,       /* chain walk exceeded its bound: fallback kernel resolved it */
+  PFR_ST_NOPROGRESS = 1u << 6,     /* rejection exceeded max_rounds proposals for a slot */
+  PFR_ST_NOTMONOTONE = 1u << 7,    /* cumulative offspring input decreases */
+  PFR_ST_BADEND = 1u << 8,         /* cumulative offspring input does not end at N */
+  PFR_ST_NEGCOUNT = 1u << 9,       /* negative offspring count / cumulative start */
+  PFR_ST_BADSUM = 1u << 10,        /* offspring counts do not sum to N */
+  PFR_ST_RATIO = 1u << 11,         /* non-finite acceptance ratio w / bound */
+  PFR_ST_NONTERMINATION = 1u << 12,/* permute chain did not terminate (cannot happen for valid a) */
+  PFR_ST_NOTINT = 1u << 13,        /* non-integer value where an index was expected */
+  PFR_ST_NEEDS_REPAIR = 1u << 14   /* internal: O must be max-scanned before use */
+};
+
+enum pfr_error {
+  PFR_OK = 0,
+  PFR_E_ARG = 1,       /* invalid argument (size, dtype, null pointer) */
+  PFR_E_WORKSPACE = 2, /* workspace too small */
+  PFR_E_CUDA = 3,      /* CUDA launch error */
+  PFR_E_UNSUPPORTED = 4
+};
+
+/* operation ids for pfr_workspace_bytes */
+enum pfr_op {
+  PFR_OP_SCAN = 0,
+  PFR_OP_OFFSPRING = 1, /* systematic / stratified cumulative offspring */
+  PFR_OP_DELIVER = 2,   /* fused systematic/stratified -> in-place ancestry */
+  PFR_OP_PERMUTE = 3,
+  PFR_OP_MULTINOMIAL = 4,
+  PFR_OP_METROPOLIS = 5,
+  PFR_OP_REJECTION = 6,
+  PFR_OP_EXPAND = 7,
+  PFR_OP_LOGWEIGHTS = 8,
+  PFR_OP_PREDICATE = 9,
+  PFR_OP_ANY = 10 /* max over all ops */
+};
+
+/* the caller's RngStream(seed, ids) after key derivation (rng.py:39-74):
+ * key0 = derive_seed(seed, 0, *ids), key1 = derive_seed(seed, 1, *ids) */
+typedef struct pfr_rng {
+  uint64_t key0;
+  uint64_t key1;
+  int32_t mode; /* enum pfr_rng_mode */
+  int32_t reserved;
+} pfr_rng;
+
+/* ---- library --------------------------------------------------------- */
+int pfr_abi_version(void);
+const char* pfr_last_error(void);
+size_t pfr_workspace_bytes(int op, int64_t n, int dtype);
+/* number of kernels the library launched on this host thread since the last reset */
+uint64_t pfr_launch_count(int reset);
+
+/* one uniform in [0,1) of the stream, evaluated on the host with the same
+ * generator code the kernels use: NUMPY mode = the index-th
+ * Generator.random() draw (rng.py:69-74; resamplers.py:134 takes index 0);
+ * PHILOX mode = 53-bit double from Philox4x32-10 counter (index, 0, tag, 0). */
+double pfr_stream_uniform(const pfr_rng* rng, uint64_t index, uint32_t tag);
+
+/* ---- primitives (primitives.py) ---------------------------------------- */
+
+/* inclusive_prefix_sum (primitives.py:34-42), exclusive_prefix_sum (45-51),
+ * vector_sum (60-66), offspring_to_cumulative (ancestry.py:85-88).
+ * Single pass with a deterministic lookback tree.  `out_dtype` is the dtype of
+ * `out` (float: same as input; integer input: PFR_I64 or PFR_I32).  `total`
+ * (nullable, device) receives the sum (double for floats, int64 for ints).
+ * Validation bits: NONFINITE for floats, NEGCOUNT for negative ints. */
+int pfr_scan(const void* in, void* out, int64_t n, int dtype, int out_dtype, int accum, int exclusive,
+             void* total, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
+/* adjacent_difference (primitives.py:54-57) and cumulative_to_offspring
+ * (ancestry.py:91-94; validates non-decreasing/ends at N when dtype is int). */
+int pfr_adjacent_difference(const void* in, void* out, int64_t n, int dtype, int out_dtype, uint32_t* status,
+                            void* stream);
+
+/* lower_bound (primitives.py:91-106): out[i] = min(N-1, #{j : W[j] < u[i]}),
+ * float32 W compared in float64 as numpy promotes. */
+int pfr_lower_bound(const void* W, int64_t n, int dtype, const double* u, int64_t m, int32_t* out, void* stream);
+
+/* check_weights (diagnostics.py:38-51): NONFINITE / NEGATIVE / POSITIVE bits */
+int pfr_check_weights(const void* w, int64_t n, int dtype, uint32_t* status, void* stream);
+
+/* logweights_to_weights (diagnostics.py:138-155): w = exp(lw - max lw) */
+int pfr_logweights_to_weights(const void* lw, void* w, int64_t n, int dtype, uint32_t* status, void* ws,
+                              size_t ws_bytes, void* stream);
+
+/* ---- resamplers (resamplers.py) ------------------------------------------ */
+
+/* systematic_cumulative_offspring (resamplers.py:127-136) when uniforms == NULL
+ * (`offset` = the single u in [0,1)), stratified_cumulative_offspring
+ * (resamplers.py:105-124) otherwise or when rng != NULL && stratified.
+ * O[i] = min(N, floor(N*W[i]/W[N-1] + u[k-1])), k = min(N, floor(r)+1),
+ * then the monotone repair and O[N-1] = N (resamplers.py:139-153).
+ *   stratified == 0: systematic, u = offset cast to the weight dtype
+ *   stratified == 1: per-stratum u from `uniforms` (float64, length N) if not
+ *                    NULL, else from `rng` (PHILOX or NUMPY stream). */
+int pfr_cumulative_offspring(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
+                             const double* uniforms, const pfr_rng* rng, int32_t* O, uint32_t* status, void* ws,
+                             size_t ws_bytes, void* stream);
+
+/* Fused delivery: weights -> in-place-valid ancestry c, i.e.
+ * permute_parallel(cumulative_offspring_to_ancestors(<systematic|stratified O>))
+ * (bench.py:155-161 timed region for the offspring algorithms) without
+ * materialising the sorted ancestry.  O_out (nullable) also returns O. */
+int pfr_deliver_offspring(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
+                          const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,
+                          int32_t* max_steps, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
+/* multinomial_ancestors (resamplers.py:56-74).
+ *   rng mode ARRAYS: `uniforms` are the pre-scaled draws in [0, W[N-1]);
+ *   rng mode NUMPY : u = random(N) * W[N-1] replayed from the stream; out a is unsorted;
+ *   rng mode PHILOX: sorted order statistics (exponential spacings) merged
+ *                    against W: a is sorted (the O(N) Code-4 formulation).
+ * sorted_serial != 0 selects multinomial_ancestors_serial's log-spacing
+ * construction (resamplers.py:77-102) with NUMPY draws. */
+int pfr_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng, const double* uniforms,
+                    int sorted_serial, int32_t* a, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
+/* metropolis_ancestors (resamplers.py:204-234): N chains of B steps.
+ * rng mode ARRAYS uses u_draws[B*N] (float64) and j_draws[B*N] (idx_dtype). */
+int pfr_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng, const double* u_draws,
+                   const void* j_draws, int idx_dtype, int32_t* a, uint32_t* status, void* ws, size_t ws_bytes,
+                   void* stream);
+
+/* rejection_ancestors / _rejection_loop (resamplers.py:237-255, 282-310) and,
+ * with cap > 0, rejection_ancestors_capped (258-279): v = min(w, cap),
+ * bound = cap, out_w[i] = w[a[i]] / v[a[i]] (1 where v[a[i]] == 0).
+ * trips (nullable) gets per-slot proposal counts; max_rounds bounds them
+ * (the reference raises after 100000 rounds: NOPROGRESS). */
+int pfr_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
+                  int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status, void* ws,
+                  size_t ws_bytes, void* stream);
+
+/* ---- ancestry (ancestry.py) ---------------------------------------------- */
+
+/* cumulative_offspring_to_ancestors (ancestry.py:69-76): merge-path expand */
+int pfr_cumulative_to_ancestors(const void* O, int64_t n, int idx_dtype, int32_t* a, uint32_t* status, void* ws,
+                                size_t ws_bytes, void* stream);
+
+/* ancestors_to_offspring (ancestry.py:79-82): histogram */
+int pfr_ancestors_to_offspring(const void* a, int64_t n, int idx_dtype, int32_t* o, uint32_t* status, void* stream);
+
+/* prepermute (ancestry.py:125-136): d[v] = min{i : a[i] = v}, sentinel N */
+int pfr_prepermute(const void* a, int64_t n, int idx_dtype, int32_t* d, uint32_t* status, void* stream);
+
+/* permute_parallel (ancestry.py:139-174): c with o[i] > 0 => c[i] = i; same
+ * output as the reference for every input.  max_steps (nullable, device int32)
+ * gets the longest chain walk (return_max_steps=True). */
+int pfr_permute(const void* a, int64_t n, int idx_dtype, int32_t* c, int32_t* max_steps, uint32_t* status,
+                void* ws, size_t ws_bytes, void* stream);
+
+/* permute_parallel(cumulative_offspring_to_ancestors(O)) directly from O */
+int pfr_permute_cumulative(const int32_t* O, int64_t n, int32_t* c, int32_t* max_steps, uint32_t* status,
+                           void* ws, size_t ws_bytes, void* stream);
+
+/* satisfies_inplace_predicate (ancestry.py:97-101): *result = 1/0 (device int32) */
+int pfr_check_predicate(const void* c, int64_t n, int idx_dtype, int32_t* result, uint32_t* status, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* in-place copy step of the bootstrap filter (pf.py:86-97):
+ * x[i] = x[c[i]] wherever c[i] != i, for `width` float64 values per particle */
+int pfr_copy_particles(double* x, int64_t n, int64_t width, const int32_t* c, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PFR_H_ */

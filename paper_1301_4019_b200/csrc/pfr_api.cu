@@ -1,0 +1,361 @@
+// extern "C" boundary of libpfr (declared in include/pfr.h).
+//
+// Host-side responsibilities only: argument checks, workspace carving, kernel
+// launch sequencing on the caller's stream, error mapping.  No host compute on
+// the data path and no device allocation.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "pfr_internal.h"
+#include "pfr_tile.cuh"
+
+namespace pfr {
+
+namespace {
+thread_local std::string g_last_error;
+thread_local uint64_t g_launches = 0;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  size_t hdr, sum, max, O, d, a, scratch, end;
+};
+
+Layout layout(int64_t n) {
+  Layout L;
+  const int64_t tiles = num_tiles(n < 1 ? 1 : n);
+  const size_t cells = (size_t)Tree::cells_needed(tiles) * sizeof(uint64_t);
+  size_t off = 0;
+  L.hdr = off;
+  off = align_up(off + sizeof(WsHeader), 256);
+  L.sum = off;
+  off = align_up(off + cells, 256);
+  L.max = off;
+  off = align_up(off + cells, 256);
+  const size_t reset_end = off;
+  (void)reset_end;
+  L.O = off;
+  off = align_up(off + (size_t)n * 4, 256);
+  L.d = off;
+  off = align_up(off + (size_t)n * 4, 256);
+  L.a = off;
+  off = align_up(off + (size_t)n * 4, 256);
+  L.scratch = off;  // 4 x N int32 (fallback) or 2 x (N+1) float64 (multinomial)
+  off = align_up(off + (size_t)(n + 1) * 16, 256);
+  L.end = off;
+  return L;
+}
+
+size_t op_bytes(int op, int64_t n) {
+  const Layout L = layout(n);
+  switch (op) {
+    case PFR_OP_SCAN:
+    case PFR_OP_OFFSPRING:
+    case PFR_OP_METROPOLIS:
+    case PFR_OP_REJECTION:
+    case PFR_OP_EXPAND:
+    case PFR_OP_LOGWEIGHTS:
+      return L.O;
+    case PFR_OP_PREDICATE:
+      return L.a;
+    default:
+      return L.end;
+  }
+}
+
+int fail(int code, const char* msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorNotSupported ? PFR_E_UNSUPPORTED : PFR_E_CUDA;
+}
+
+bool valid_n(int64_t n) { return n >= 1 && n < 0x7F000000LL; }
+bool is_float(int dt) { return dt == PFR_F32 || dt == PFR_F64; }
+bool is_index(int dt) { return dt == PFR_I32 || dt == PFR_I64; }
+
+#define PFR_REQUIRE(cond, msg) \
+  do {                         \
+    if (!(cond)) return fail(PFR_E_ARG, msg); \
+  } while (0)
+
+#define PFR_WS(op)                                                                   \
+  Workspace ws;                                                                      \
+  if (!workspace_carve(ws_ptr, ws_bytes, n, ws) || ws_bytes < op_bytes(op, n))       \
+    return fail(PFR_E_WORKSPACE, "workspace too small (see pfr_workspace_bytes)");
+
+#define PFR_CHECK_LAUNCH(expr, where)          \
+  do {                                         \
+    cudaError_t _e = (expr);                   \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+}  // namespace
+
+void note_launch(int k) { g_launches += (uint64_t)k; }
+
+int num_sms() {
+  static thread_local int dev_cached = -1, sms = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != dev_cached) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 1;
+    dev_cached = dev;
+  }
+  return sms;
+}
+
+size_t workspace_bytes(int64_t n) { return layout(n).end; }
+
+bool workspace_carve(void* base, size_t bytes, int64_t n, Workspace& ws) {
+  std::memset(&ws, 0, sizeof(ws));
+  if (!base) return false;
+  const Layout L = layout(n);
+  char* b = static_cast<char*>(base);
+  if (reinterpret_cast<uintptr_t>(base) % 256) return false;
+  if (bytes < L.O) return false;
+  ws.hdr = reinterpret_cast<WsHeader*>(b + L.hdr);
+  ws.tiles = num_tiles(n);
+  ws.sum_cells = reinterpret_cast<uint64_t*>(b + L.sum);
+  ws.max_cells = reinterpret_cast<uint64_t*>(b + L.max);
+  ws.reset_bytes = L.O;
+  ws.bytes = bytes;
+  if (bytes >= L.d) ws.O = reinterpret_cast<int32_t*>(b + L.O);
+  if (bytes >= L.a) ws.d = reinterpret_cast<int32_t*>(b + L.d);
+  if (bytes >= L.scratch) ws.a = reinterpret_cast<int32_t*>(b + L.a);
+  if (bytes >= L.end) {
+    int32_t* sc = reinterpret_cast<int32_t*>(b + L.scratch);
+    const size_t q = align_up((size_t)(n + 1) * 4, 256) / 4;  // int32 elements per quarter
+    ws.j0 = sc;
+    ws.j1 = sc + q;
+    ws.r0 = sc + 2 * q;
+    ws.r1 = sc + 3 * q;
+    ws.f0 = reinterpret_cast<double*>(sc);
+    ws.f1 = reinterpret_cast<double*>(sc + 2 * q);
+  }
+  return true;
+}
+
+cudaError_t workspace_reset(const Workspace& ws, cudaStream_t s) {
+  return cudaMemsetAsync(ws.hdr, 0xFF, ws.reset_bytes, s);
+}
+
+}  // namespace pfr
+
+using namespace pfr;
+
+extern "C" {
+
+int pfr_abi_version(void) { return PFR_ABI_VERSION; }
+
+const char* pfr_last_error(void) { return g_last_error.c_str(); }
+
+size_t pfr_workspace_bytes(int op, int64_t n, int dtype) {
+  (void)dtype;
+  if (n < 1) n = 1;
+  if (op == PFR_OP_ANY) return workspace_bytes(n);
+  return op_bytes(op, n);
+}
+
+double pfr_stream_uniform(const pfr_rng* rng, uint64_t index, uint32_t tag) {
+  if (!rng) return 0.0;
+  if (rng->mode == PFR_RNG_NUMPY) return u64_to_unit(numpy_raw64(Key2x64{rng->key0, rng->key1}, index));
+  uint32_t o[4];
+  philox4x32_10((uint32_t)index, (uint32_t)(index >> 32), tag, 0, (uint32_t)rng->key0, (uint32_t)(rng->key0 >> 32), o);
+  return u64_to_unit(((uint64_t)o[0] << 32) | o[1]);
+}
+
+uint64_t pfr_launch_count(int reset) {
+  const uint64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+int pfr_scan(const void* in, void* out, int64_t n, int dtype, int out_dtype, int accum, int exclusive, void* total,
+             uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n), "n must be in [1, 2^31)");
+  PFR_REQUIRE(in && out, "null array");
+  PFR_REQUIRE(is_float(dtype) || is_index(dtype), "unsupported dtype");
+  if (is_float(dtype)) PFR_REQUIRE(out_dtype == dtype, "float scan keeps the input dtype");
+  if (is_index(dtype)) PFR_REQUIRE(is_index(out_dtype), "integer scan needs an integer output");
+  PFR_WS(PFR_OP_SCAN);
+  const int64_t expect = (accum & 0x200) ? n : -1;  // internal: offspring_to_cumulative sum check
+  PFR_CHECK_LAUNCH(launch_scan(in, out, n, dtype, out_dtype, accum & ~0x200, exclusive, total, expect, status, ws,
+                               (cudaStream_t)stream),
+                   "pfr_scan");
+  return PFR_OK;
+}
+
+int pfr_adjacent_difference(const void* in, void* out, int64_t n, int dtype, int out_dtype, uint32_t* status,
+                            void* stream) {
+  PFR_REQUIRE(valid_n(n), "n must be in [1, 2^31)");
+  PFR_REQUIRE(in && out, "null array");
+  PFR_REQUIRE(is_float(dtype) ? out_dtype == dtype : (is_index(dtype) && is_index(out_dtype)), "bad dtypes");
+  PFR_CHECK_LAUNCH(launch_adjacent_difference(in, out, n, dtype, out_dtype, status, (cudaStream_t)stream),
+                   "pfr_adjacent_difference");
+  return PFR_OK;
+}
+
+int pfr_lower_bound(const void* W, int64_t n, int dtype, const double* u, int64_t m, int32_t* out, void* stream) {
+  PFR_REQUIRE(valid_n(n) && m >= 0, "bad sizes");
+  PFR_REQUIRE(W && (m == 0 || (u && out)), "null array");
+  PFR_REQUIRE(is_float(dtype), "W must be float32 or float64");
+  if (m == 0) return PFR_OK;
+  PFR_CHECK_LAUNCH(launch_lower_bound(W, n, dtype, u, m, out, (cudaStream_t)stream), "pfr_lower_bound");
+  return PFR_OK;
+}
+
+int pfr_check_weights(const void* w, int64_t n, int dtype, uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && status, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_CHECK_LAUNCH(launch_check_weights(w, n, dtype, status, (cudaStream_t)stream), "pfr_check_weights");
+  return PFR_OK;
+}
+
+int pfr_logweights_to_weights(const void* lw, void* w, int64_t n, int dtype, uint32_t* status, void* ws_ptr,
+                              size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && lw && w, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "log-weights must be float32 or float64");
+  PFR_WS(PFR_OP_LOGWEIGHTS);
+  PFR_CHECK_LAUNCH(launch_logweights(lw, w, n, dtype, status, ws, (cudaStream_t)stream), "pfr_logweights_to_weights");
+  return PFR_OK;
+}
+
+int pfr_cumulative_offspring(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
+                             const double* uniforms, const pfr_rng* rng, int32_t* O, uint32_t* status, void* ws_ptr,
+                             size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && O, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  if (stratified) PFR_REQUIRE(uniforms || rng, "stratified needs uniforms or an rng");
+  PFR_WS(PFR_OP_OFFSPRING);
+  PFR_CHECK_LAUNCH(launch_offspring(w, n, dtype, accum, stratified, offset, uniforms, rng, O, status, ws,
+                                    (cudaStream_t)stream),
+                   "pfr_cumulative_offspring");
+  return PFR_OK;
+}
+
+int pfr_deliver_offspring(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
+                          const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out, int32_t* max_steps,
+                          uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && c, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  if (stratified) PFR_REQUIRE(uniforms || rng, "stratified needs uniforms or an rng");
+  PFR_WS(PFR_OP_DELIVER);
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* O = O_out ? O_out : ws.O;
+  PFR_CHECK_LAUNCH(launch_offspring(w, n, dtype, accum, stratified, offset, uniforms, rng, O, status, ws, s),
+                   "pfr_deliver_offspring (offspring)");
+  PFR_CHECK_LAUNCH(launch_permute_cumulative(O, n, c, max_steps, status, ws, s), "pfr_deliver_offspring (permute)");
+  return PFR_OK;
+}
+
+int pfr_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng, const double* uniforms,
+                    int sorted_serial, int32_t* a, uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && a, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(uniforms || rng, "multinomial needs uniforms or an rng");
+  PFR_WS(PFR_OP_MULTINOMIAL);
+  PFR_CHECK_LAUNCH(launch_multinomial(w, n, dtype, accum, rng, uniforms, sorted_serial, a, status, ws,
+                                      (cudaStream_t)stream),
+                   "pfr_multinomial");
+  return PFR_OK;
+}
+
+int pfr_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng, const double* u_draws,
+                   const void* j_draws, int idx_dtype, int32_t* a, uint32_t* status, void* ws_ptr, size_t ws_bytes,
+                   void* stream) {
+  (void)ws_ptr;
+  (void)ws_bytes;
+  PFR_REQUIRE(valid_n(n) && w && a, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(steps >= 0, "number of chain steps must be non-negative");
+  const bool arrays = !rng || rng->mode == PFR_RNG_ARRAYS;
+  if (arrays) PFR_REQUIRE((u_draws && j_draws && is_index(idx_dtype)) || steps == 0, "ARRAYS mode needs u and j draws");
+  PFR_CHECK_LAUNCH(launch_metropolis(w, n, dtype, steps, rng, u_draws, j_draws, idx_dtype, a, status,
+                                     (cudaStream_t)stream),
+                   "pfr_metropolis");
+  return PFR_OK;
+}
+
+int pfr_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
+                  int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status, void* ws_ptr,
+                  size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && a && status, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(rng, "rejection needs an rng");
+  const double b = cap > 0 ? cap : bound;
+  if (!(b > 0) || !std::isfinite(b)) return fail(PFR_E_ARG, "weight bound must be finite and positive");
+  if (cap > 0) PFR_REQUIRE(out_w, "capped rejection needs out_w");
+  PFR_WS(PFR_OP_REJECTION);
+  PFR_CHECK_LAUNCH(launch_rejection(w, n, dtype, bound, cap, rng, max_rounds, a, trips, out_w, status, ws,
+                                    (cudaStream_t)stream),
+                   "pfr_rejection");
+  return PFR_OK;
+}
+
+int pfr_cumulative_to_ancestors(const void* O, int64_t n, int idx_dtype, int32_t* a, uint32_t* status, void* ws_ptr,
+                                size_t ws_bytes, void* stream) {
+  (void)ws_ptr;
+  (void)ws_bytes;
+  PFR_REQUIRE(valid_n(n) && O && a, "bad arguments");
+  PFR_REQUIRE(is_index(idx_dtype), "O must be int32 or int64");
+  PFR_CHECK_LAUNCH(launch_expand(O, n, idx_dtype, a, status, status != nullptr, (cudaStream_t)stream),
+                   "pfr_cumulative_to_ancestors");
+  return PFR_OK;
+}
+
+int pfr_ancestors_to_offspring(const void* a, int64_t n, int idx_dtype, int32_t* o, uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n) && a && o, "bad arguments");
+  PFR_REQUIRE(is_index(idx_dtype), "a must be int32 or int64");
+  PFR_CHECK_LAUNCH(launch_histogram(a, n, idx_dtype, o, status, (cudaStream_t)stream), "pfr_ancestors_to_offspring");
+  return PFR_OK;
+}
+
+int pfr_prepermute(const void* a, int64_t n, int idx_dtype, int32_t* d, uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n) && a && d, "bad arguments");
+  PFR_REQUIRE(is_index(idx_dtype), "a must be int32 or int64");
+  PFR_CHECK_LAUNCH(launch_prepermute(a, n, idx_dtype, d, status, (cudaStream_t)stream), "pfr_prepermute");
+  return PFR_OK;
+}
+
+int pfr_permute(const void* a, int64_t n, int idx_dtype, int32_t* c, int32_t* max_steps, uint32_t* status,
+                void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && a && c, "bad arguments");
+  PFR_REQUIRE(is_index(idx_dtype), "a must be int32 or int64");
+  PFR_WS(PFR_OP_PERMUTE);
+  PFR_CHECK_LAUNCH(launch_permute(a, n, idx_dtype, c, max_steps, status, ws, (cudaStream_t)stream), "pfr_permute");
+  return PFR_OK;
+}
+
+int pfr_permute_cumulative(const int32_t* O, int64_t n, int32_t* c, int32_t* max_steps, uint32_t* status,
+                           void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && O && c, "bad arguments");
+  PFR_WS(PFR_OP_DELIVER);
+  PFR_CHECK_LAUNCH(launch_permute_cumulative(O, n, c, max_steps, status, ws, (cudaStream_t)stream),
+                   "pfr_permute_cumulative");
+  return PFR_OK;
+}
+
+int pfr_check_predicate(const void* c, int64_t n, int idx_dtype, int32_t* result, uint32_t* status, void* ws_ptr,
+                        size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && c && result, "bad arguments");
+  PFR_REQUIRE(is_index(idx_dtype), "c must be int32 or int64");
+  PFR_WS(PFR_OP_PREDICATE);
+  PFR_CHECK_LAUNCH(launch_predicate(c, n, idx_dtype, result, status, ws, (cudaStream_t)stream),
+                   "pfr_check_predicate");
+  return PFR_OK;
+}
+
+int pfr_copy_particles(double* x, int64_t n, int64_t width, const int32_t* c, void* stream) {
+  PFR_REQUIRE(valid_n(n) && width >= 1 && x && c, "bad arguments");
+  PFR_CHECK_LAUNCH(launch_copy_particles(x, n, width, c, (cudaStream_t)stream), "pfr_copy_particles");
+  return PFR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// Internal declarations shared by the .cu translation units of libpfr.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/pfr.h"
+#include "pfr_rng.cuh"
+
+namespace pfr {
+
+// ---------------------------------------------------------------------------
+// workspace layout (one layout for every op; sized by n and the widest dtype)
+struct WsHeader {
+  unsigned int ticket[8];  // tile tickets (start at 0xFFFFFFFF: +1 wraps to 0)
+  unsigned int done[8];    // last-block counters
+  uint64_t cell[8];        // scalar cells (Cell<A> encoded): [0] total W[N-1]
+  int32_t overflow;        // chain walk overflow marker (0xFFFFFFFF = none)
+  int32_t pad[15];
+};
+
+struct Workspace {
+  WsHeader* hdr;
+  uint64_t* sum_cells;  // lookback sum tree
+  uint64_t* max_cells;  // lookback max tree
+  int64_t tiles;
+  int32_t* O;  // cumulative offspring scratch
+  int32_t* d;  // claims
+  int32_t* a;  // sorted ancestry scratch (fallback)
+  int32_t* j0;
+  int32_t* j1;
+  int32_t* r0;
+  int32_t* r1;
+  double* f0;  // N+1 doubles (multinomial / logweights scratch)
+  double* f1;  // N doubles
+  size_t reset_bytes;  // header + trees: memset to 0xFF before each op
+  size_t bytes;
+};
+
+size_t workspace_bytes(int64_t n);
+bool workspace_carve(void* base, size_t bytes, int64_t n, Workspace& ws);
+cudaError_t workspace_reset(const Workspace& ws, cudaStream_t s);
+
+// launch accounting (pfr_launch_count)
+void note_launch(int k = 1);
+
+// ---------------------------------------------------------------------------
+// launchers (pfr_scan.cu)
+cudaError_t launch_scan(const void* in, void* out, int64_t n, int dtype, int out_dtype, int accum, int exclusive,
+                        void* total, int64_t expect_total, uint32_t* status, const Workspace& ws, cudaStream_t s);
+cudaError_t launch_offspring(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
+                             const double* uniforms, const pfr_rng* rng, int32_t* O, uint32_t* status,
+                             const Workspace& ws, cudaStream_t s);
+cudaError_t launch_check_weights(const void* w, int64_t n, int dtype, uint32_t* status, cudaStream_t s);
+cudaError_t launch_adjacent_difference(const void* in, void* out, int64_t n, int dtype, int out_dtype,
+                                       uint32_t* status, cudaStream_t s);
+cudaError_t launch_logweights(const void* lw, void* w, int64_t n, int dtype, uint32_t* status, const Workspace& ws,
+                              cudaStream_t s);
+
+// launchers (pfr_ancestry.cu)
+cudaError_t launch_permute_cumulative(const int32_t* O, int64_t n, int32_t* c, int32_t* max_steps, uint32_t* status,
+                                      const Workspace& ws, cudaStream_t s);
+cudaError_t launch_permute(const void* a, int64_t n, int idx_dtype, int32_t* c, int32_t* max_steps,
+                           uint32_t* status, const Workspace& ws, cudaStream_t s);
+cudaError_t launch_prepermute(const void* a, int64_t n, int idx_dtype, int32_t* d, uint32_t* status,
+                              cudaStream_t s);
+cudaError_t launch_expand(const void* O, int64_t n, int idx_dtype, int32_t* a, uint32_t* status, bool validate,
+                          cudaStream_t s);
+cudaError_t launch_histogram(const void* a, int64_t n, int idx_dtype, int32_t* o, uint32_t* status, cudaStream_t s);
+cudaError_t launch_predicate(const void* c, int64_t n, int idx_dtype, int32_t* result, uint32_t* status,
+                             const Workspace& ws, cudaStream_t s);
+cudaError_t launch_copy_particles(double* x, int64_t n, int64_t width, const int32_t* c, cudaStream_t s);
+
+// launchers (pfr_resample.cu)
+cudaError_t launch_lower_bound(const void* W, int64_t n, int dtype, const double* u, int64_t m, int32_t* out,
+                               cudaStream_t s);
+cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng,
+                               const double* uniforms, int sorted_serial, int32_t* a, uint32_t* status,
+                               const Workspace& ws, cudaStream_t s);
+cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng,
+                              const double* u_draws, const void* j_draws, int idx_dtype, int32_t* a,
+                              uint32_t* status, cudaStream_t s);
+cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
+                             int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
+                             const Workspace& ws, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace pfr

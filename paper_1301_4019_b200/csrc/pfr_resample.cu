@@ -1,0 +1,514 @@
+// Metropolis, rejection and multinomial resamplers, lower_bound.
+//
+// Reference: resamplers.py:56-102 (multinomial, serial/sorted variant),
+// 204-234 (Metropolis), 237-310 (rejection, capped), primitives.py:91-106
+// (lower_bound).
+//
+// Metropolis and rejection need no collective over the weights: each output
+// slot runs its own chain / proposal loop reading w through the read-only
+// path (ld.global.nc).  Random draws come from a counter-based generator so
+// they are a pure function of (stream, slot, step): no state in memory.
+#include <cmath>
+
+#include "pfr_internal.h"
+#include "pfr_tile.cuh"
+
+namespace pfr {
+
+namespace {
+
+constexpr int kChainsPerThread = 4;
+
+template <typename T>
+__device__ __forceinline__ T ldg(const T* p) {
+  return __ldg(p);
+}
+
+template <typename T>
+__device__ __forceinline__ T div_rn_t(T a, T b);
+template <>
+__device__ __forceinline__ float div_rn_t(float a, float b) {
+  return __fdiv_rn(a, b);
+}
+template <>
+__device__ __forceinline__ double div_rn_t(double a, double b) {
+  return __ddiv_rn(a, b);
+}
+
+// reference acceptance (resamplers.py:228-232): ratio rounded in the weight
+// dtype, compared against the float64 uniform; a zero current weight accepts
+template <typename T>
+__device__ __forceinline__ bool accept_ref(double u, T wk, T wj) {
+  if (wk == T(0)) return true;
+  const T ratio = div_rn_t(wj, wk);
+  return u <= (double)ratio;
+}
+
+// ---------------------------------------------------------------------------
+// Metropolis, own Philox4x32-10 stream: chain i, step b uses counter
+// (i, b/2, tag, 0): words (2*(b&1), 2*(b&1)+1) = (proposal, uniform).
+template <typename T>
+__global__ void __launch_bounds__(256) k_metropolis_philox(const T* __restrict__ w, int64_t n, int64_t steps,
+                                                           uint32_t k0, uint32_t k1, uint32_t threshold,
+                                                           int32_t* __restrict__ a) {
+  const int64_t first = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kChainsPerThread;
+  if (first >= n) return;
+  int64_t k[kChainsPerThread];
+  T wk[kChainsPerThread];
+#pragma unroll
+  for (int c = 0; c < kChainsPerThread; ++c) {
+    const int64_t i = min(first + c, n - 1);
+    k[c] = i;
+    wk[c] = ldg(w + i);
+  }
+  const uint32_t nn = (uint32_t)n;
+  for (int64_t b = 0; b < steps; b += 2) {
+    uint32_t j[kChainsPerThread][2];
+    T u[kChainsPerThread][2];
+    T wj[kChainsPerThread][2];
+#pragma unroll
+    for (int c = 0; c < kChainsPerThread; ++c) {
+      const uint32_t i = (uint32_t)(first + c);
+      uint32_t o[4];
+      philox4x32_10(i, (uint32_t)(b >> 1), kTagMetropolis, 0, k0, k1, o);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        j[c][h] = bounded_u32(o[2 * h], nn, threshold, i, (uint32_t)(b + h), kTagMetropolis, k0, k1);
+        if constexpr (sizeof(T) == 4)
+          u[c][h] = u32_to_unit_f(o[2 * h + 1]);
+        else
+          u[c][h] = u32_to_unit_d(o[2 * h + 1]);
+      }
+    }
+    // issue every gather of this step pair before consuming any (MLP)
+#pragma unroll
+    for (int c = 0; c < kChainsPerThread; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) wj[c][h] = ldg(w + j[c][h]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (b + h >= steps) break;
+#pragma unroll
+      for (int c = 0; c < kChainsPerThread; ++c) {
+        // u <= w[j]/w[k]  <=>  u * w[k] <= w[j]  (w[k] > 0); w[k] == 0 accepts
+        const bool acc = (wk[c] == T(0)) || (u[c][h] * wk[c] <= wj[c][h]);
+        if (acc) {
+          k[c] = j[c][h];
+          wk[c] = wj[c][h];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kChainsPerThread; ++c)
+    if (first + c < n) a[first + c] = (int32_t)k[c];
+}
+
+// Metropolis replaying numpy's stream (power-of-two N): per step the
+// generator yields N doubles then N integers (one u32 each, low half first).
+template <typename T>
+__global__ void __launch_bounds__(256) k_metropolis_numpy(const T* __restrict__ w, int64_t n, int64_t steps,
+                                                          Key2x64 key, int log2n, int32_t* __restrict__ a) {
+  const int64_t first = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kChainsPerThread;
+  if (first >= n) return;
+  int64_t k[kChainsPerThread];
+  T wk[kChainsPerThread];
+#pragma unroll
+  for (int c = 0; c < kChainsPerThread; ++c) {
+    const int64_t i = min(first + c, n - 1);
+    k[c] = i;
+    wk[c] = ldg(w + i);
+  }
+  const uint64_t per_step = (uint64_t)n + (uint64_t)n / 2;  // u64 words per step
+  for (int64_t b = 0; b < steps; ++b) {
+    const uint64_t ubase = (uint64_t)b * per_step;
+    const uint64_t jbase = ubase + (uint64_t)n;
+    double u[kChainsPerThread];
+    int64_t j[kChainsPerThread];
+#pragma unroll
+    for (int c = 0; c < kChainsPerThread; ++c) {
+      const uint64_t i = (uint64_t)(first + c);
+      u[c] = u64_to_unit(numpy_raw64(key, ubase + i));
+      const uint64_t word = numpy_raw64(key, jbase + i / 2);
+      const uint32_t x = (i & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+      j[c] = (int64_t)(((uint64_t)x << log2n) >> 32);
+    }
+    T wj[kChainsPerThread];
+#pragma unroll
+    for (int c = 0; c < kChainsPerThread; ++c) wj[c] = ldg(w + j[c]);
+#pragma unroll
+    for (int c = 0; c < kChainsPerThread; ++c) {
+      if (accept_ref<T>(u[c], wk[c], wj[c])) {
+        k[c] = j[c];
+        wk[c] = wj[c];
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kChainsPerThread; ++c)
+    if (first + c < n) a[first + c] = (int32_t)k[c];
+}
+
+// Metropolis from caller-supplied draws u[b*N + i] (float64), j[b*N + i]
+template <typename T, typename I>
+__global__ void __launch_bounds__(256) k_metropolis_arrays(const T* __restrict__ w, int64_t n, int64_t steps,
+                                                           const double* __restrict__ ud, const I* __restrict__ jd,
+                                                           int32_t* __restrict__ a, uint32_t* status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t k = i;
+  T wk = ldg(w + i);
+  uint32_t f = 0;
+  for (int64_t b = 0; b < steps; ++b) {
+    const int64_t j = (int64_t)jd[b * n + i];
+    if (j < 0 || j >= n) {
+      f |= PFR_ST_RANGE;
+      continue;
+    }
+    const T wj = ldg(w + j);
+    if (accept_ref<T>(ud[b * n + i], wk, wj)) {
+      k = j;
+      wk = wj;
+    }
+  }
+  status_or(status, f);
+  a[i] = (int32_t)k;
+}
+
+// ---------------------------------------------------------------------------
+// Rejection, own stream, warp-cooperative slot queue.  Slot i, trip t uses
+// counter (i, t/2, tag, 0), words (2*(t&1), 2*(t&1)+1) = (proposal, uniform);
+// trip 0 proposes i itself (resamplers.py:291-294).  Warps grab chunks of 256
+// slots with one atomic and refill idle lanes from the chunk via ballot/popc,
+// so lanes stay busy although trip counts vary by orders of magnitude.
+template <typename T>
+struct RejArgs {
+  const T* w;
+  int64_t n;
+  double bound;
+  double cap;  // > 0: capped variant, v = min(w, cap), bound = cap
+  uint32_t k0, k1, threshold;
+  int64_t max_trips;
+  int32_t* a;
+  int32_t* trips;
+  T* out_w;
+  unsigned long long* next_chunk;
+  uint32_t* status;
+};
+
+constexpr int kRejChunk = 256;
+
+template <typename T, bool kCapped>
+__global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
+  const int lane = threadIdx.x & 31;
+  const T bound = (T)A.bound;
+  const T capv = (T)A.cap;
+  const uint32_t nn = (uint32_t)A.n;
+  int64_t chunk_next = 0, chunk_end = 0;  // warp-uniform local queue
+  bool exhausted = false;                 // warp-uniform: no chunks left
+  int64_t slot = -1;
+  int64_t trip = 0;
+  uint32_t o[4];
+  uint32_t flags = 0;
+  int iter = 0;
+  while (true) {
+    // refill idle lanes
+    unsigned idle = __ballot_sync(0xffffffffu, slot < 0);
+    while (idle) {
+      if (chunk_next >= chunk_end) {
+        if (exhausted) break;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(A.next_chunk, (unsigned long long)kRejChunk);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if ((int64_t)base >= A.n) {
+          exhausted = true;
+          break;
+        }
+        chunk_next = (int64_t)base;
+        chunk_end = min((int64_t)base + kRejChunk, A.n);
+      }
+      const int rank = __popc(idle & ((1u << lane) - 1));
+      const int take = min((int64_t)__popc(idle), chunk_end - chunk_next);
+      if (slot < 0 && rank < take) {
+        slot = chunk_next + rank;
+        trip = 0;
+      }
+      chunk_next += take;
+      idle = __ballot_sync(0xffffffffu, slot < 0);
+    }
+    if (__ballot_sync(0xffffffffu, slot >= 0) == 0) break;
+    if (slot >= 0) {
+      if ((trip & 1) == 0) philox4x32_10((uint32_t)slot, (uint32_t)(trip >> 1), kTagRejection, 0, A.k0, A.k1, o);
+      const int h = (int)(trip & 1);
+      const int64_t j = trip == 0 ? slot
+                                  : (int64_t)bounded_u32(o[2 * h], nn, A.threshold, (uint32_t)slot,
+                                                         (uint32_t)trip, kTagRejection, A.k0, A.k1);
+      const T wj = ldg(A.w + j);
+      const T vj = kCapped ? (wj < capv ? wj : capv) : wj;
+      T uu;
+      if constexpr (sizeof(T) == 4) {
+        uu = u32_to_unit_f(o[2 * h + 1]);
+      } else {
+        uu = u32_to_unit_d(o[2 * h + 1]);
+      }
+      ++trip;
+      // beta <= v[j] / bound  <=>  beta * bound <= v[j]
+      if (uu * bound <= vj) {
+        A.a[slot] = (int32_t)j;
+        if (A.trips) A.trips[slot] = (int32_t)trip;
+        if (kCapped) A.out_w[slot] = (vj == T(0)) ? T(1) : div_rn_t(wj, vj);
+        slot = -1;
+      } else if (trip >= A.max_trips) {
+        flags |= PFR_ST_NOPROGRESS;
+        A.a[slot] = (int32_t)slot;
+        if (A.trips) A.trips[slot] = (int32_t)trip;
+        if (kCapped) A.out_w[slot] = T(1);
+        slot = -1;
+      }
+    }
+    if (((++iter) & 255) == 0) {
+      // give up early once any slot reported no progress (reference raises)
+      if (__ballot_sync(0xffffffffu, flags != 0) || (*(volatile uint32_t*)A.status & PFR_ST_NOPROGRESS)) {
+        flags |= PFR_ST_NOPROGRESS;
+        break;
+      }
+    }
+  }
+  status_or_warp(A.status, flags);
+}
+
+// ---------------------------------------------------------------------------
+// lower_bound: smallest j with W[j] >= u (compared in float64), clamped to N-1
+template <typename T>
+__device__ __forceinline__ int64_t lower_bound_dev(const T* __restrict__ W, int64_t n, double u) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((double)ldg(W + mid) < u)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo < n ? lo : n - 1;
+}
+
+template <typename T>
+__global__ void k_lower_bound(const T* __restrict__ W, int64_t n, const double* __restrict__ u, int64_t m,
+                              int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)lower_bound_dev(W, n, u[i]);
+}
+
+// multinomial, numpy stream: u_i = random()_i * float(W[N-1]) (resamplers.py:68-69)
+template <typename T>
+__global__ void k_multinomial_numpy(const T* __restrict__ W, int64_t n, Key2x64 key, int32_t* __restrict__ out) {
+  const double total = (double)W[n - 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double u = u64_to_unit(numpy_raw64(key, (uint64_t)i)) * total;
+    out[i] = (int32_t)lower_bound_dev(W, n, u);
+  }
+}
+
+// own stream sorted multinomial: exponential spacings E_k = -log(U_k), k in [0, N]
+__global__ void k_exponentials(int64_t n, uint32_t k0, uint32_t k1, double* __restrict__ E) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= n; k += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t o[4];
+    philox4x32_10((uint32_t)k, (uint32_t)(k >> 32), kTagMultinomial, 0, k0, k1, o);
+    const uint64_t x = ((uint64_t)o[0] << 32) | o[1];
+    const double u = ((double)(x >> 11) + 1.0) * (1.0 / 9007199254740992.0);  // (0, 1]
+    E[k] = -log(u);
+  }
+}
+
+// sorted uniforms U_(k) = S_k / S_N times W[N-1]; a[k] = lower_bound(W, .)
+template <typename T>
+__global__ void k_multinomial_sorted(const T* __restrict__ W, int64_t n, const double* __restrict__ S,
+                                     int32_t* __restrict__ out) {
+  const double total = (double)W[n - 1];
+  const double norm = S[n];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const double u = S[k] / norm * total;
+    out[k] = (int32_t)lower_bound_dev(W, n, u);
+  }
+}
+
+// Code 4 (multinomial_ancestors_serial) with numpy draws: L_p = ln(d_p)/(N-p)
+__global__ void k_serial_logs(int64_t n, Key2x64 key, double* __restrict__ L) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const double d = u64_to_unit(numpy_raw64(key, (uint64_t)p));
+    L[p] = (d > 0.0 ? log(d) : -INFINITY) / (double)(n - p);
+  }
+}
+
+// a[i] = (#{j : Wx[j] <= u}) - 1 with u = total * exp(lnmax_{N-1-i})
+template <typename T>
+__global__ void k_serial_sweep(const T* __restrict__ Wx, const T* __restrict__ w, int64_t n,
+                               const double* __restrict__ lnmax, int32_t* __restrict__ out) {
+  const double total = (double)Wx[n - 1] + (double)w[n - 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double u = total * exp(lnmax[n - 1 - i]);
+    int64_t lo = 0, hi = n;  // first j with Wx[j] > u
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((double)ldg(Wx + mid) <= u)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    out[i] = (int32_t)(lo > 0 ? lo - 1 : 0);
+  }
+}
+
+int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+uint32_t lemire_threshold(int64_t n) { return (uint32_t)((0x100000000ull - (uint64_t)n) % (uint64_t)n); }
+
+int log2_exact(int64_t n) {
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  return (int64_t(1) << l) == n ? l : -1;
+}
+
+}  // namespace
+
+cudaError_t launch_lower_bound(const void* W, int64_t n, int dtype, const double* u, int64_t m, int32_t* out,
+                               cudaStream_t s) {
+  const int g = grid_for(m, 256);
+  if (dtype == PFR_F64)
+    k_lower_bound<double><<<g, 256, 0, s>>>((const double*)W, n, u, m, out);
+  else
+    k_lower_bound<float><<<g, 256, 0, s>>>((const float*)W, n, u, m, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng,
+                              const double* u_draws, const void* j_draws, int idx_dtype, int32_t* a,
+                              uint32_t* status, cudaStream_t s) {
+  const int mode = rng ? rng->mode : PFR_RNG_ARRAYS;
+  const int64_t threads = (n + kChainsPerThread - 1) / kChainsPerThread;
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  if (mode == PFR_RNG_ARRAYS) {
+    const unsigned b1 = (unsigned)((n + 255) / 256);
+    if (dtype == PFR_F64) {
+      if (idx_dtype == PFR_I64)
+        k_metropolis_arrays<double, int64_t><<<b1, 256, 0, s>>>((const double*)w, n, steps, u_draws, (const int64_t*)j_draws, a, status);
+      else
+        k_metropolis_arrays<double, int32_t><<<b1, 256, 0, s>>>((const double*)w, n, steps, u_draws, (const int32_t*)j_draws, a, status);
+    } else {
+      if (idx_dtype == PFR_I64)
+        k_metropolis_arrays<float, int64_t><<<b1, 256, 0, s>>>((const float*)w, n, steps, u_draws, (const int64_t*)j_draws, a, status);
+      else
+        k_metropolis_arrays<float, int32_t><<<b1, 256, 0, s>>>((const float*)w, n, steps, u_draws, (const int32_t*)j_draws, a, status);
+    }
+  } else if (mode == PFR_RNG_NUMPY) {
+    const int l2 = log2_exact(n);
+    if (l2 < 0 || n < 2) return cudaErrorNotSupported;  // numpy replay needs a power-of-two N
+    Key2x64 key{rng->key0, rng->key1};
+    if (dtype == PFR_F64)
+      k_metropolis_numpy<double><<<blocks, 256, 0, s>>>((const double*)w, n, steps, key, l2, a);
+    else
+      k_metropolis_numpy<float><<<blocks, 256, 0, s>>>((const float*)w, n, steps, key, l2, a);
+  } else {
+    const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
+    const uint32_t thr = lemire_threshold(n);
+    if (dtype == PFR_F64)
+      k_metropolis_philox<double><<<blocks, 256, 0, s>>>((const double*)w, n, steps, k0, k1, thr, a);
+    else
+      k_metropolis_philox<float><<<blocks, 256, 0, s>>>((const float*)w, n, steps, k0, k1, thr, a);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
+                             int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
+                             const Workspace& ws, cudaStream_t s) {
+  if (!rng || rng->mode != PFR_RNG_PHILOX) return cudaErrorNotSupported;
+  unsigned long long* next = reinterpret_cast<unsigned long long*>(&ws.hdr->cell[2]);
+  cudaError_t e = cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
+  const int64_t max_trips = max_rounds + 1;
+  // persistent: enough warps to fill the machine, chunks hand out the slots
+  const int blocks = num_sms() * 8;
+  if (dtype == PFR_F64) {
+    RejArgs<double> A{(const double*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
+                      a, trips, (double*)out_w, next, status};
+    if (cap > 0)
+      k_rejection_philox<double, true><<<blocks, 256, 0, s>>>(A);
+    else
+      k_rejection_philox<double, false><<<blocks, 256, 0, s>>>(A);
+  } else {
+    RejArgs<float> A{(const float*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
+                     a, trips, (float*)out_w, next, status};
+    if (cap > 0)
+      k_rejection_philox<float, true><<<blocks, 256, 0, s>>>(A);
+    else
+      k_rejection_philox<float, false><<<blocks, 256, 0, s>>>(A);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng,
+                               const double* uniforms, int sorted_serial, int32_t* a, uint32_t* status,
+                               const Workspace& ws, cudaStream_t s) {
+  // W = inclusive scan of w (monotone, weights are non-negative) into scratch
+  void* W = ws.f1;
+  const int scan_flags = accum | PFR_SCAN_MONOTONE;
+  const int g = grid_for(n, 256);
+  if (sorted_serial) {
+    // Code 4: exclusive scan Wx, log spacings scanned in float64
+    if (!rng || rng->mode != PFR_RNG_NUMPY) return cudaErrorNotSupported;
+    cudaError_t e = launch_scan(w, W, n, dtype, dtype, scan_flags, 1, nullptr, -1, status, ws, s);
+    if (e != cudaSuccess) return e;
+    Key2x64 key{rng->key0, rng->key1};
+    k_serial_logs<<<g, 256, 0, s>>>(n, key, ws.f0);
+    note_launch();
+    // the log-spacing scan has negative terms: no monotone repair
+    e = launch_scan(ws.f0, ws.f0, n, PFR_F64, PFR_F64, PFR_ACC_F64, 0, nullptr, -1, status, ws, s);
+    if (e != cudaSuccess) return e;
+    if (dtype == PFR_F64)
+      k_serial_sweep<double><<<g, 256, 0, s>>>((const double*)W, (const double*)w, n, ws.f0, a);
+    else
+      k_serial_sweep<float><<<g, 256, 0, s>>>((const float*)W, (const float*)w, n, ws.f0, a);
+    note_launch();
+    return cudaGetLastError();
+  }
+  cudaError_t e = launch_scan(w, W, n, dtype, dtype, scan_flags, 0, nullptr, -1, status, ws, s);
+  if (e != cudaSuccess) return e;
+  const int mode = uniforms ? PFR_RNG_ARRAYS : (rng ? rng->mode : PFR_RNG_PHILOX);
+  if (mode == PFR_RNG_ARRAYS) {
+    return launch_lower_bound(W, n, dtype, uniforms, n, a, s);
+  } else if (mode == PFR_RNG_NUMPY) {
+    Key2x64 key{rng->key0, rng->key1};
+    if (dtype == PFR_F64)
+      k_multinomial_numpy<double><<<g, 256, 0, s>>>((const double*)W, n, key, a);
+    else
+      k_multinomial_numpy<float><<<g, 256, 0, s>>>((const float*)W, n, key, a);
+    note_launch();
+  } else {
+    const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
+    k_exponentials<<<grid_for(n + 1, 256), 256, 0, s>>>(n, k0, k1, ws.f0);
+    note_launch();
+    // in-place scan of the N+1 spacings (non-negative: monotone repair)
+    e = launch_scan(ws.f0, ws.f0, n + 1, PFR_F64, PFR_F64, PFR_ACC_F64 | PFR_SCAN_MONOTONE, 0, nullptr, -1, status,
+                    ws, s);
+    if (e != cudaSuccess) return e;
+    if (dtype == PFR_F64)
+      k_multinomial_sorted<double><<<g, 256, 0, s>>>((const double*)W, n, ws.f0, a);
+    else
+      k_multinomial_sorted<float><<<g, 256, 0, s>>>((const float*)W, n, ws.f0, a);
+    note_launch();
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace pfr
