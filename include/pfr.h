@@ -9,8 +9,10 @@
  *     aligned); scalars are passed by value;
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream); every
  *     call only ENQUEUES work on that stream and returns without synchronising;
- *   - `ws`/`ws_bytes` is caller-owned scratch sized by pfr_workspace_bytes();
- *     the library never allocates device memory on the hot path;
+ *   - `ws`/`ws_bytes` is caller-owned scratch sized by pfr_workspace_bytes(),
+ *     256-byte aligned and ZERO-FILLED when first allocated (the fused
+ *     delivery keeps self-resetting counters in it); one stream at a time may
+ *     use a given workspace; the library never allocates device memory;
  *   - inputs are never written (the reference never mutates inputs,
  *     SPEC.md:371); outputs are caller-allocated;
  *   - indices are int32 on output (N < 2^31); index inputs may be int32 or

@@ -234,7 +234,8 @@ def workspace(n: int) -> tuple[int, int]:
     need = int(lib().pfr_workspace_bytes(OP_ANY, int(n), 0))
     cur = _ws.get(dev.index)
     if cur is None or cur.numel() < need:
-        cur = torch.empty(max(need, 1 << 20), dtype=torch.uint8, device=dev)
+        # zero-filled once: the fused delivery keeps its counters in it (pfr.h)
+        cur = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
         _ws[dev.index] = cur
     return cur.data_ptr(), cur.numel()
 

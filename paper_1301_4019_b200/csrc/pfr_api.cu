@@ -20,14 +20,16 @@ thread_local uint64_t g_launches = 0;
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t hdr, sum, max, O, d, a, scratch, end;
+  size_t dv, hdr, sum, max, O, d, a, scratch, end;
 };
 
 Layout layout(int64_t n) {
   Layout L;
   const int64_t tiles = num_tiles(n < 1 ? 1 : n);
-  const size_t cells = (size_t)Tree::cells_needed(tiles) * sizeof(uint64_t);
+  const size_t cells = (size_t)(Tree::cells_needed(tiles) + 2) * sizeof(uint64_t);
   size_t off = 0;
+  L.dv = off;
+  off = align_up(off + sizeof(DvState), 256);
   L.hdr = off;
   off = align_up(off + sizeof(WsHeader), 256);
   L.sum = off;
@@ -120,11 +122,12 @@ bool workspace_carve(void* base, size_t bytes, int64_t n, Workspace& ws) {
   char* b = static_cast<char*>(base);
   if (reinterpret_cast<uintptr_t>(base) % 256) return false;
   if (bytes < L.O) return false;
+  ws.dv = reinterpret_cast<DvState*>(b + L.dv);
   ws.hdr = reinterpret_cast<WsHeader*>(b + L.hdr);
   ws.tiles = num_tiles(n);
   ws.sum_cells = reinterpret_cast<uint64_t*>(b + L.sum);
   ws.max_cells = reinterpret_cast<uint64_t*>(b + L.max);
-  ws.reset_bytes = L.O;
+  ws.reset_bytes = L.O - L.hdr;
   ws.bytes = bytes;
   if (bytes >= L.d) ws.O = reinterpret_cast<int32_t*>(b + L.O);
   if (bytes >= L.a) ws.d = reinterpret_cast<int32_t*>(b + L.d);
@@ -249,9 +252,10 @@ int pfr_deliver_offspring(const void* w, int64_t n, int dtype, int accum, int st
   PFR_WS(PFR_OP_DELIVER);
   cudaStream_t s = (cudaStream_t)stream;
   int32_t* O = O_out ? O_out : ws.O;
-  PFR_CHECK_LAUNCH(launch_offspring(w, n, dtype, accum, stratified, offset, uniforms, rng, O, status, ws, s),
-                   "pfr_deliver_offspring (offspring)");
-  PFR_CHECK_LAUNCH(launch_permute_cumulative(O, n, c, max_steps, status, ws, s), "pfr_deliver_offspring (permute)");
+  (void)O;
+  PFR_CHECK_LAUNCH(launch_deliver(w, n, dtype, accum, stratified, offset, uniforms, rng, c, O_out, max_steps, status,
+                                  ws, s),
+                   "pfr_deliver_offspring");
   return PFR_OK;
 }
 

@@ -20,7 +20,16 @@ struct WsHeader {
   int32_t pad[15];
 };
 
+// state of the fused delivery pipeline: zero at workspace allocation, kept
+// consistent by the kernels themselves (never memset per call)
+struct DvState {
+  unsigned int done;   // K1 CTAs finished (the last one resets it)
+  unsigned int flags;  // 1 = O needs the running-max repair, 2 = chain overflow
+  unsigned int pad[62];
+};
+
 struct Workspace {
+  DvState* dv;
   WsHeader* hdr;
   uint64_t* sum_cells;  // lookback sum tree
   uint64_t* max_cells;  // lookback max tree
@@ -52,6 +61,9 @@ cudaError_t launch_scan(const void* in, void* out, int64_t n, int dtype, int out
 cudaError_t launch_offspring(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
                              const double* uniforms, const pfr_rng* rng, int32_t* O, uint32_t* status,
                              const Workspace& ws, cudaStream_t s);
+cudaError_t launch_deliver(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
+                           const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,
+                           int32_t* max_steps, uint32_t* status, const Workspace& ws, cudaStream_t s);
 cudaError_t launch_check_weights(const void* w, int64_t n, int dtype, uint32_t* status, cudaStream_t s);
 cudaError_t launch_adjacent_difference(const void* in, void* out, int64_t n, int dtype, int out_dtype,
                                        uint32_t* status, cudaStream_t s);
