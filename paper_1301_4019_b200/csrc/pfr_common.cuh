@@ -43,12 +43,13 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
-// streaming 16-byte read-only load, no L1 allocation, L2 policy hint
+// streaming 16-byte read-only load, no L1 allocation, L2 policy hint.
+// Not volatile: the loads are pure, so the compiler may batch them (MLP).
 __device__ __forceinline__ uint4 ld_stream16(const void* ptr, uint64_t pol) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(ptr), "l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(ptr), "l"(pol));
   return r;
 }
 

@@ -230,9 +230,10 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
   }
 }
 
-// monotonicity of o across the tile and against the previous tile's last O
-__device__ __forceinline__ bool tile_monotone(const int32_t (&o)[kTileItems], int64_t o_prev, int64_t base,
-                                              int64_t n, int32_t* warp_last) {
+// true when o decreases anywhere inside the tile or against the previous
+// tile's last O (the caller then defers to the repair path)
+__device__ __forceinline__ bool tile_decreases(const int32_t (&o)[kTileItems], int64_t o_prev, int64_t base,
+                                               int64_t n, int32_t* warp_last) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   bool bad = false;
 #pragma unroll
@@ -245,42 +246,84 @@ __device__ __forceinline__ bool tile_monotone(const int32_t (&o)[kTileItems], in
   return __syncthreads_or(bad);
 }
 
-// smem O table with swizzled 16-byte slots: element x of the tile
-__device__ __forceinline__ int os_get(const int32_t* Os, int x) { return Os[(swz(x >> 2) << 2) | (x & 3)]; }
+// word staging in shared memory: 16-byte slots XOR-swizzled (bank spread
+// for the per-thread contiguous writes, conflict-free striped read-out)
+__device__ __forceinline__ int sw4(int pos) { return (swz(pos >> 2) << 2) | (pos & 3); }
 
-// expand the tile's parents over their slots: words + bitmap
+// smem O table (same swizzle): element x of the tile
+__device__ __forceinline__ int os_get(const int32_t* Os, int x) { return Os[sw4(x)]; }
+
+constexpr int kLightCap = 2 * kTile;  // words a light tile may stage (32 KB)
+constexpr int kLightMaxO = 64;         // per-parent offspring bound of the light path
+
+// Expand the tile's parents over their slots: words (parent | FIRST) and the
+// has-offspring bitmap.  Light path (the common case): every thread writes
+// its own 16 parents' slots into shared memory, then the CTA streams the
+// tile's slot range out with coalesced stores.  Heavy path (a parent with more
+// than kLightMaxO offspring, or a slot range over 8192): balanced chunks of
+// 4096 slots, each thread locating its parent by binary search.
 __device__ void tile_expand(const int32_t (&o)[kTileItems], int64_t o_prev, int64_t b, int64_t n, uint32_t* words,
-                            uint32_t* bitmap, int32_t* Os, uint32_t* wbuf) {
-  const int tid = threadIdx.x;
+                            uint32_t* bitmap, uint32_t* sbuf /* 32 KB */, int32_t* warp_last) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t base = b * kTile;
   const int len = (int)min((int64_t)kTile, n - base);
-  // O table in smem
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    int4 v = make_int4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-    reinterpret_cast<int4*>(Os)[swz(tid * 4 + q)] = v;
-  }
-  // bitmap: has-offspring bits of this thread's 16 parents, pairs of threads per word
+  // O of the element before this thread's first parent
   int prev = __shfl_up_sync(0xffffffffu, o[kTileItems - 1], 1);
+  if (lane == 31) warp_last[warp] = o[kTileItems - 1];
   __syncthreads();
-  if ((tid & 31) == 0) prev = tid ? os_get(Os, tid * kTileItems - 1) : (int)o_prev;
+  if (lane == 0) prev = warp ? warp_last[warp - 1] : (int)o_prev;
   uint32_t bits = 0;
+  int maxo = 0;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
     const int pv = j ? o[j - 1] : prev;
-    if (base + tid * kTileItems + j < n && o[j] > pv) bits |= 1u << j;
+    if (base + tid * kTileItems + j < n) {
+      if (o[j] > pv) bits |= 1u << j;
+      maxo = max(maxo, o[j] - pv);
+    }
   }
   const uint32_t hi = __shfl_down_sync(0xffffffffu, bits, 1);
   if ((tid & 1) == 0 && base + tid * kTileItems < n) bitmap[(base >> 5) + (tid >> 1)] = bits | (hi << 16);
-  // slots [S0, S1) of this tile's parents, 4096 per round
   const int64_t S0 = o_prev;
-  const int64_t S1 = os_get(Os, len - 1);
-  for (int64_t r0 = S0; r0 < S1; r0 += kTile) {
+  __shared__ int64_t s_end;  // O of the tile's last element: N for the final tile
+  if (tid == kTileThreads - 1) s_end = (base + kTile <= n) ? (int64_t)o[kTileItems - 1] : n;
+  const bool heavy = __syncthreads_or(maxo > kLightMaxO);
+  const int64_t end = s_end;
+  if (!heavy && end - S0 <= kLightCap) {
+    // light: own parents -> staged words
+    int64_t s = prev;
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      if (base + tid * kTileItems + j < n) {
+        const uint32_t parent = (uint32_t)(base + tid * kTileItems + j);
+        const int64_t e = o[j];
+        if (s < e) {
+          sbuf[sw4((int)(s - S0))] = parent | kFirst;
+          for (int64_t q = s + 1; q < e; ++q) sbuf[sw4((int)(q - S0))] = parent;
+        }
+        s = e;
+      }
+    }
+    __syncthreads();
+    const int cnt = (int)(end - S0);
+    for (int i = tid; i < cnt; i += kTileThreads) words[S0 + i] = sbuf[sw4(i)];
+    __syncthreads();
+    return;
+  }
+  // heavy: O table in the first 16 KB, 4096-slot chunks staged in the second
+  int32_t* Os = reinterpret_cast<int32_t*>(sbuf);
+  uint32_t* wbuf = sbuf + kTile;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int4 v = make_int4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+    reinterpret_cast<int4*>(Os)[swz(tid * 4 + q)] = v;
+  }
+  __syncthreads();
+  for (int64_t r0 = S0; r0 < end; r0 += kTile) {
     const int64_t sb = r0 + (int64_t)tid * kTileItems;
-    const int64_t se = min(sb + kTileItems, S1);
+    const int64_t se = min(sb + kTileItems, end);
     if (sb < se) {
-      // parent of slot sb: smallest x with O(x) > sb
-      int lo = 0, hi2 = len - 1;
+      int lo = 0, hi2 = len - 1;  // parent of slot sb: smallest x with O(x) > sb
       while (lo < hi2) {
         const int mid = (lo + hi2) >> 1;
         if (os_get(Os, mid) > sb)
@@ -297,12 +340,12 @@ __device__ void tile_expand(const int32_t (&o)[kTileItems], int64_t o_prev, int6
           oex = ox;
           ox = os_get(Os, xi);
         }
-        wbuf[s - r0] = (uint32_t)(base + xi) | (s == oex ? kFirst : 0u);
+        wbuf[sw4((int)(s - r0))] = (uint32_t)(base + xi) | (s == oex ? kFirst : 0u);
       }
     }
     __syncthreads();
-    const int cnt = (int)min((int64_t)kTile, S1 - r0);
-    for (int i = tid; i < cnt; i += kTileThreads) words[r0 + i] = wbuf[i];
+    const int cnt = (int)min((int64_t)kTile, end - r0);
+    for (int i = tid; i < cnt; i += kTileThreads) words[r0 + i] = wbuf[sw4(i)];
     __syncthreads();
   }
 }
@@ -310,11 +353,8 @@ __device__ void tile_expand(const int32_t (&o)[kTileItems], int64_t o_prev, int6
 // ---------------------------------------------------------------------------
 // K2
 template <typename T, typename A, int UM>
-__global__ void __launch_bounds__(kTileThreads) k_dv_expand(DvArgs<A> p) {
-  // one 32 KB buffer: the tile stage, then the O table (16 KB) + word staging (16 KB)
-  __shared__ __align__(16) uint4 stage[2 * kTile * 4 / 16];
-  int32_t* Os = reinterpret_cast<int32_t*>(stage);
-  uint32_t* wbuf = reinterpret_cast<uint32_t*>(stage) + kTile;
+__global__ void __launch_bounds__(kTileThreads, 4) k_dv_expand(DvArgs<A> p) {
+  __shared__ __align__(16) uint4 stage[2 * kTile * 4 / 16];  // tile stage, then word staging (32 KB)
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ int32_t warp_last[kTileThreads / 32];
   griddep_wait();
@@ -322,72 +362,75 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_expand(DvArgs<A> p) {
   int32_t o[kTileItems];
   int64_t o_prev;
   tile_offspring<T, A, UM>(p, b, stage, warp_sums, o, o_prev);
-  if (!tile_monotone(o, o_prev, b * kTile, p.n, warp_last)) {
+  if (p.O_out) tile_store<int32_t>(p.O_out, p.n, b * kTile, stage, o, policy_evict_last());
+  if (tile_decreases(o, o_prev, b * kTile, p.n, warp_last)) {
     if (threadIdx.x == 0) atomicOr(&p.state->flags, kNeedsRepair);
     griddep_launch();
     return;  // the rare-path kernel recomputes everything
   }
-  if (p.O_out) {
-    tile_store<int32_t>(p.O_out, p.n, b * kTile, stage, o, policy_evict_last());
-  }
-  // wbuf aliases the stage buffer (>= 16 KB for every T)
-  tile_expand(o, o_prev, b, p.n, p.words, p.bitmap, Os, wbuf);
+  tile_expand(o, o_prev, b, p.n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), warp_last);
   griddep_launch();
 }
 
 // ---------------------------------------------------------------------------
-// K3: one index per thread-slot, 4 per thread
-__device__ __forceinline__ int32_t resolve_index(int64_t i, uint32_t wd, bool has, const uint32_t* words,
-                                                 int& steps, bool& overflow) {
-  steps = 0;
-  if (has) return (int32_t)i;
-  if (!(wd & kFirst)) return (int32_t)(wd & kParentMask);  // slot i is a loser: claims its own hole
-  uint32_t z = wd & kParentMask;
-  while (true) {
-    ++steps;
-    const uint32_t wz = __ldcg(words + z);
-    if (!(wz & kFirst)) return (int32_t)(wz & kParentMask);
-    z = wz & kParentMask;
-    if (steps >= kBackBound) {
-      overflow = true;
-      return 0;
+// K3: 16 indices per thread, striped (index = base + 256 j + t), so the
+// coalesced word loads and the clustered chain loads of a warp share sectors;
+// all of a thread's pending chains advance together (16 loads in flight).
+constexpr int kInplaceItems = 16;
+
+__device__ __forceinline__ void resolve_tile(const uint32_t* __restrict__ words, const uint32_t* __restrict__ bitmap,
+                                             int64_t n, int32_t* __restrict__ c, int64_t base, int& longest,
+                                             bool& overflow) {
+  const int t = threadIdx.x;
+  // v[j]: the final output, or for a pending chain the current node
+  uint32_t v[kInplaceItems];
+  uint32_t active = 0;
+#pragma unroll
+  for (int j = 0; j < kInplaceItems; ++j) {
+    const int64_t i = base + (int64_t)j * kTileThreads + t;
+    v[j] = 0;
+    if (i < n) {
+      const uint32_t wd = __ldcg(words + i);
+      const bool has = (__ldcg(bitmap + (i >> 5)) >> (i & 31)) & 1u;
+      v[j] = has ? (uint32_t)i : (wd & kParentMask);
+      if (!has && (wd & kFirst)) active |= 1u << j;
     }
+  }
+  int steps = 0;
+  while (active) {
+    if (++steps > kBackBound) {
+      overflow = true;
+      break;
+    }
+    uint32_t wz[kInplaceItems];
+#pragma unroll
+    for (int j = 0; j < kInplaceItems; ++j)
+      if (active & (1u << j)) wz[j] = __ldcg(words + v[j]);
+#pragma unroll
+    for (int j = 0; j < kInplaceItems; ++j) {
+      if (active & (1u << j)) {
+        v[j] = wz[j] & kParentMask;
+        if (!(wz[j] & kFirst)) active &= ~(1u << j);
+      }
+    }
+  }
+  longest = max(longest, overflow ? kBackBound : steps);
+#pragma unroll
+  for (int j = 0; j < kInplaceItems; ++j) {
+    const int64_t i = base + (int64_t)j * kTileThreads + t;
+    if (i < n) __stcs(c + i, (int32_t)v[j]);
   }
 }
 
-__global__ void __launch_bounds__(256) k_dv_inplace(const uint32_t* __restrict__ words,
-                                                    const uint32_t* __restrict__ bitmap, int64_t n,
-                                                    int32_t* __restrict__ c, int32_t* max_steps, DvState* state,
-                                                    uint32_t* status) {
+__global__ void __launch_bounds__(kTileThreads, 5) k_dv_inplace(const uint32_t* __restrict__ words,
+                                                             const uint32_t* __restrict__ bitmap, int64_t n,
+                                                             int32_t* __restrict__ c, int32_t* max_steps,
+                                                             DvState* state, uint32_t* status) {
   griddep_wait();
   if (state->flags & kNeedsRepair) return;
-  const int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
-  if (i0 >= n) return;
-  uint32_t wd[4];
-  if (i0 + 4 <= n) {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(words + i0));
-    wd[0] = v.x;
-    wd[1] = v.y;
-    wd[2] = v.z;
-    wd[3] = v.w;
-  } else {
-    for (int e = 0; e < 4; ++e) wd[e] = i0 + e < n ? words[i0 + e] : 0u;
-  }
-  const uint32_t bw = __ldcs(bitmap + (i0 >> 5)) >> (i0 & 31);
-  int32_t out[4];
   int longest = 0;
   bool overflow = false;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    int steps;
-    out[e] = resolve_index(i0 + e, wd[e], (bw >> e) & 1u, words, steps, overflow);
-    longest = max(longest, steps);
-  }
-  if (i0 + 4 <= n) {
-    __stcs(reinterpret_cast<int4*>(c + i0), make_int4(out[0], out[1], out[2], out[3]));
-  } else {
-    for (int e = 0; e < 4 && i0 + e < n; ++e) c[i0 + e] = out[e];
-  }
+  resolve_tile(words, bitmap, n, c, (int64_t)blockIdx.x * kTileThreads * kInplaceItems, longest, overflow);
   if (overflow) {
     atomicOr(&state->flags, kOverflow);
     status_or(status, PFR_ST_OVERFLOW);
@@ -400,12 +443,10 @@ __global__ void __launch_bounds__(256) k_dv_inplace(const uint32_t* __restrict__
 // rare paths (cooperative): repair of non-monotone O, pointer jumping
 template <typename T, typename A, int UM>
 __global__ void __launch_bounds__(kTileThreads) k_dv_rare(DvArgs<A> p) {
-  // one 32 KB buffer: the tile stage, then the O table (16 KB) + word staging (16 KB)
   __shared__ __align__(16) uint4 stage[2 * kTile * 4 / 16];
-  int32_t* Os = reinterpret_cast<int32_t*>(stage);
-  uint32_t* wbuf = reinterpret_cast<uint32_t*>(stage) + kTile;
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ int64_t imax8[kTileThreads / 32];
+  __shared__ int32_t warp_last[kTileThreads / 32];
   griddep_wait();
   const uint32_t flags0 = *(volatile uint32_t*)&p.state->flags;
   if (!flags0) return;
@@ -460,18 +501,15 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_rare(DvArgs<A> p) {
       }
       const int64_t o_prev = b ? max(before_tiles, (int64_t)0) : 0;
       if (p.O_out) tile_store<int32_t>(p.O_out, n, b * kTile, stage, o, policy_evict_last());
-      tile_expand(o, o_prev, b, n, p.words, p.bitmap, Os, wbuf);
+      tile_expand(o, o_prev, b, n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), warp_last);
     }
     grid.sync();
     // D: in-place indices
     bool overflow = false;
     int longest = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-      int steps;
-      const bool has = (__ldcg(p.bitmap + (i >> 5)) >> (i & 31)) & 1u;
-      p.c[i] = resolve_index(i, __ldcg(p.words + i), has, p.words, steps, overflow);
-      longest = max(longest, steps);
-    }
+    const int64_t span = (int64_t)kTileThreads * kInplaceItems;
+    for (int64_t t = blockIdx.x; t * span < n; t += gridDim.x)
+      resolve_tile(p.words, p.bitmap, n, p.c, t * span, longest, overflow);
     if (overflow) atomicOr(&p.state->flags, kOverflow);
     if (p.max_steps && longest) atomicMax(p.max_steps, longest);
     grid.sync();
@@ -555,7 +593,7 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
   if (e != cudaSuccess) return e;
-  const unsigned blocks3 = (unsigned)((p.n + 1023) / 1024);
+  const unsigned blocks3 = (unsigned)((p.n + kTile - 1) / kTile);
   e = launch_pdl(k_dv_inplace, dim3(blocks3), dim3(256), s, false, (const uint32_t*)p.words,
                  (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
   if (e != cudaSuccess) return e;

@@ -137,11 +137,13 @@ __device__ __forceinline__ void tile_load(const T* __restrict__ in, int64_t n, i
   const int tid = threadIdx.x;
   const int64_t remain = n - base;
   if (remain >= kTile) {
+    // issue every load of the tile before the first shared-memory store
+    uint4 buf[kVecs / kTileThreads];
 #pragma unroll
-    for (int k = 0; k < kVecs / kTileThreads; ++k) {
-      const int v = k * kTileThreads + tid;
-      smem[swz(v)] = ld_stream16(in + base + (int64_t)v * kPerVec, pol);
-    }
+    for (int k = 0; k < kVecs / kTileThreads; ++k)
+      buf[k] = ld_stream16(in + base + (int64_t)(k * kTileThreads + tid) * kPerVec, pol);
+#pragma unroll
+    for (int k = 0; k < kVecs / kTileThreads; ++k) smem[swz(k * kTileThreads + tid)] = buf[k];
   } else {
 #pragma unroll
     for (int k = 0; k < kVecs / kTileThreads; ++k) {
