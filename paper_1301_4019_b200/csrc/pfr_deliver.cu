@@ -106,92 +106,109 @@ __device__ __forceinline__ A stratum_u(int64_t k0, const DvArgs<A>& p) {
 // the exact sequence whenever r or r+u lies within 2^-44 (relative) of an
 // integer -- far more than the <= 2^-51 gap between the two r's -- so both
 // floors are provably identical.
+// the exact IEEE sequence of the reference (rare: kept out of line so its
+// register needs do not inflate the streaming path)
 template <typename T, typename A, int UM>
-__device__ __forceinline__ int64_t offspring_of(A W, A total, A scale, int64_t n, const DvArgs<A>& p) {
+__device__ __noinline__ int32_t offspring_exact(A W, A total, int64_t n, const DvArgs<A>& p) {
+  A r;
+  if constexpr (sizeof(A) == 8)
+    r = __ddiv_rn(__dmul_rn(W, (double)n), total);
+  else
+    r = __fdiv_rn(__fmul_rn(W, (float)n), total);
+  int64_t k = (int64_t)floor((double)r) + 1;
+  if (k > n) k = n;
+  if (k < 1) k = 1;
+  const A u = stratum_u<T, A, UM>(k - 1, p);
+  int64_t o = (int64_t)floor((double)add_rn(r, u));
+  return (int32_t)(o > n ? n : (o < 0 ? 0 : o));
+}
+
+template <typename T, typename A, int UM>
+__device__ __forceinline__ int32_t offspring_of(A W, A total, A scale, int64_t n, const DvArgs<A>& p) {
   if constexpr (sizeof(A) == 8) {
     const double rf = __dmul_rn(W, scale);
     const double tol = fmax(rf, 1.0) * 5.684341886080802e-14;  // 2^-44
     const double fr = floor(rf);
-    bool exact = (rf - fr) < tol || (fr + 1.0 - rf) < tol;
-    int64_t k = (int64_t)fr + 1;
-    double r = rf;
-    if (!exact) {
+    if ((rf - fr) >= tol && (fr + 1.0 - rf) >= tol) {
+      int64_t k = (int64_t)fr + 1;
       if (k > n) k = n;
-      const double u = (double)stratum_u<T, A, UM>(k - 1, p);
-      const double tf = __dadd_rn(rf, u);
+      const double tf = __dadd_rn(rf, (double)stratum_u<T, A, UM>(k - 1, p));
       const double ft = floor(tf);
       if ((tf - ft) >= tol && (ft + 1.0 - tf) >= tol) {
-        int64_t o = (int64_t)ft;
-        return o > n ? n : (o < 0 ? 0 : o);
+        const int64_t o = (int64_t)ft;
+        return (int32_t)(o > n ? n : (o < 0 ? 0 : o));
       }
     }
-    r = __ddiv_rn(__dmul_rn(W, (double)n), total);
-    k = (int64_t)floor(r) + 1;
-    if (k > n) k = n;
-    if (k < 1) k = 1;
-    const double u = (double)stratum_u<T, A, UM>(k - 1, p);
-    int64_t o = (int64_t)floor(__dadd_rn(r, u));
-    return o > n ? n : (o < 0 ? 0 : o);
-  } else {
-    const float r = __fdiv_rn(__fmul_rn(W, (float)n), total);
-    int64_t k = (int64_t)floorf(r) + 1;
-    if (k > n) k = n;
-    if (k < 1) k = 1;
-    const float u = (float)stratum_u<T, A, UM>(k - 1, p);
-    int64_t o = (int64_t)floorf(__fadd_rn(r, u));
-    return o > n ? n : (o < 0 ? 0 : o);
   }
+  return offspring_exact<T, A, UM>(W, total, n, p);
 }
 
 // ---------------------------------------------------------------------------
-// K1: validation + tile aggregates; the last CTA scans them
+// K1: validation + tile aggregates; the last CTA scans them.  Per-tile flags
+// go to a plain array (no same-address atomics from thousands of CTAs); the
+// last CTA ORs them into the caller's status word once.
+template <typename A>
+__device__ __forceinline__ uint32_t* tile_flags(const DvArgs<A>& p) {
+  return reinterpret_cast<uint32_t*>(p.excl + p.tiles + 2);
+}
+
 template <typename T, typename A>
 __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   __shared__ __align__(16) uint4 stage[kTile * sizeof(T) / 16];
   __shared__ A warp_sums[kTileThreads / 32];
+  __shared__ uint32_t cta_flags;
   __shared__ bool is_last;
-  const int64_t b = blockIdx.x;
-  const int64_t base = b * kTile;
-  const T* w = (const T*)p.w;
+  const int b = blockIdx.x;
+  const int64_t base = (int64_t)b * kTile;
+  const int len = (int)min((int64_t)kTile, p.n - base);
+  if (threadIdx.x == 0) cta_flags = 0;
   T x[kTileItems];
-  tile_load<T>(w, p.n, base, stage, policy_evict_last(), x);  // keep w in L2 for K2
+  tile_load<T>((const T*)p.w, p.n, base, stage, policy_evict_last(), x);  // keep w in L2 for K2
   TileScan<A> s;
   uint32_t flags = 0;
+  const int e0 = threadIdx.x * kTileItems;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
-    if (base + threadIdx.x * kTileItems + j < p.n) flags |= wflags(x[j]);
+    if (e0 + j < len) flags |= wflags(x[j]);
     s.loc[j] = (A)x[j];
   }
-  status_or_warp(p.status, flags);
-  tile_scan<A>(s, warp_sums);
-  // aggregate := tile-local inclusive value at the tile's last position
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(&cta_flags, flags);
+  tile_scan<A>(s, warp_sums);  // (ends with a barrier: cta_flags is complete)
   if (threadIdx.x == kTileThreads - 1) {
+    // aggregate := tile-local inclusive value at the tile's last position
     p.agg[b] = add_rn(s.thread_excl, s.loc[kTileItems - 1]);
+    tile_flags(p)[b] = cta_flags;
     __threadfence();
     const unsigned t = atomicAdd(&p.state->done, 1u);
     is_last = (t == (unsigned)(p.tiles - 1));
   }
   __syncthreads();
-  griddep_launch();
   if (!is_last) return;
   __threadfence();
   // exclusive scan over the tile aggregates: serial within a thread's chunk,
   // Kogge-Stone across threads, serial across warps (fixed association)
-  const int64_t T_ = p.tiles;
-  const int64_t chunk = (T_ + kTileThreads - 1) / kTileThreads;
-  const int64_t c0 = threadIdx.x * chunk, c1 = min(c0 + chunk, T_);
+  const int T_ = (int)p.tiles;
+  const int chunk = (T_ + kTileThreads - 1) / kTileThreads;
+  const int c0 = threadIdx.x * chunk, c1 = min(c0 + chunk, T_);
   A mine = A(0);
-  for (int64_t i = c0; i < c1; ++i) mine = add_rn(mine, __ldcg(p.agg + i));
+  uint32_t fl = 0;
+  for (int i = c0; i < c1; ++i) {
+    mine = add_rn(mine, __ldcg(p.agg + i));
+    fl |= __ldcg(tile_flags(p) + i);
+  }
+  fl = __reduce_or_sync(0xffffffffu, fl);
   const A incl = warp_inclusive_scan(mine);
   A excl = __shfl_up_sync(0xffffffffu, incl, 1);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) excl = A(0);
   if (lane == 31) warp_sums[warp] = incl;
+  if (lane == 0 && fl) atomicOr(&cta_flags, fl);
   __syncthreads();
   A wp = A(0);
   for (int v = 0; v < warp; ++v) wp = add_rn(wp, warp_sums[v]);
   A run = lane ? add_rn(wp, excl) : wp;
-  for (int64_t i = c0; i < c1; ++i) {
+  for (int i = c0; i < c1; ++i) {
     p.excl[i] = run;
     run = add_rn(run, __ldcg(p.agg + i));
   }
@@ -199,14 +216,16 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   if (threadIdx.x == 0) {
     p.state->done = 0;
     p.state->flags = 0;
+    status_or(p.status, cta_flags);
   }
 }
 
 // ---------------------------------------------------------------------------
-// tile -> O (registers): shared by K2 and the repair path
+// tile -> O (registers): shared by K2 and the repair path.  Index math is
+// 32-bit inside the tile (N < 2^31).
 template <typename T, typename A, int UM>
 __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, uint4* stage, A* warp_sums,
-                                               int32_t (&o)[kTileItems], int64_t& o_prev) {
+                                               int32_t (&o)[kTileItems], int32_t& o_prev) {
   const int64_t base = b * kTile;
   T x[kTileItems];
   tile_load<T>((const T*)p.w, p.n, base, stage, policy_evict_first(), x);
@@ -217,32 +236,35 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
   const A total = p.excl[p.tiles];
   const A scale = (A)p.n / total;
   const A ex = p.excl[b];
+  const int last = (p.n - 1 - base < kTile) ? (int)(p.n - 1 - base) : -1;
+  const int e0 = threadIdx.x * kTileItems;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
     const A W = add_rn(ex, add_rn(s.thread_excl, s.loc[j]));
     o[j] = (int32_t)offspring_of<T, A, UM>(W, total, scale, p.n, p);
-    if (base + threadIdx.x * kTileItems + j == p.n - 1) o[j] = (int32_t)p.n;  // O[N-1] = N
+    if (e0 + j == last) o[j] = (int32_t)p.n;  // O[N-1] = N
   }
   o_prev = 0;
   if (b > 0) {
     const A Wp = add_rn(p.excl[b - 1], p.agg[b - 1]);  // W at the last position of tile b-1
-    o_prev = offspring_of<T, A, UM>(Wp, total, scale, p.n, p);
+    o_prev = (int32_t)offspring_of<T, A, UM>(Wp, total, scale, p.n, p);
   }
 }
 
 // true when o decreases anywhere inside the tile or against the previous
 // tile's last O (the caller then defers to the repair path)
-__device__ __forceinline__ bool tile_decreases(const int32_t (&o)[kTileItems], int64_t o_prev, int64_t base,
-                                               int64_t n, int32_t* warp_last) {
+__device__ __forceinline__ bool tile_decreases(const int32_t (&o)[kTileItems], int32_t o_prev, int len,
+                                               int32_t* warp_last) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e0 = threadIdx.x * kTileItems;
   bool bad = false;
 #pragma unroll
-  for (int j = 1; j < kTileItems; ++j) bad |= (base + threadIdx.x * kTileItems + j < n) && o[j] < o[j - 1];
+  for (int j = 1; j < kTileItems; ++j) bad |= (e0 + j < len) && o[j] < o[j - 1];
   int prev = __shfl_up_sync(0xffffffffu, o[kTileItems - 1], 1);
   if (lane == 31) warp_last[warp] = o[kTileItems - 1];
   __syncthreads();
-  if (lane == 0) prev = warp ? warp_last[warp - 1] : (int)o_prev;
-  if (base + threadIdx.x * kTileItems < n) bad |= o[0] < prev;
+  if (lane == 0) prev = warp ? warp_last[warp - 1] : o_prev;
+  if (e0 < len) bad |= o[0] < prev;
   return __syncthreads_or(bad);
 }
 
@@ -262,51 +284,53 @@ constexpr int kLightMaxO = 64;         // per-parent offspring bound of the ligh
 // tile's slot range out with coalesced stores.  Heavy path (a parent with more
 // than kLightMaxO offspring, or a slot range over 8192): balanced chunks of
 // 4096 slots, each thread locating its parent by binary search.
-__device__ void tile_expand(const int32_t (&o)[kTileItems], int64_t o_prev, int64_t b, int64_t n, uint32_t* words,
+__device__ void tile_expand(const int32_t (&o)[kTileItems], int32_t o_prev, int64_t b, int64_t n, uint32_t* words,
                             uint32_t* bitmap, uint32_t* sbuf /* 32 KB */, int32_t* warp_last) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t base = b * kTile;
   const int len = (int)min((int64_t)kTile, n - base);
+  const int e0 = tid * kTileItems;
+  const uint32_t pbase = (uint32_t)base + (uint32_t)e0;
   // O of the element before this thread's first parent
   int prev = __shfl_up_sync(0xffffffffu, o[kTileItems - 1], 1);
   if (lane == 31) warp_last[warp] = o[kTileItems - 1];
   __syncthreads();
-  if (lane == 0) prev = warp ? warp_last[warp - 1] : (int)o_prev;
+  if (lane == 0) prev = warp ? warp_last[warp - 1] : o_prev;
   uint32_t bits = 0;
   int maxo = 0;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
     const int pv = j ? o[j - 1] : prev;
-    if (base + tid * kTileItems + j < n) {
+    if (e0 + j < len) {
       if (o[j] > pv) bits |= 1u << j;
       maxo = max(maxo, o[j] - pv);
     }
   }
   const uint32_t hi = __shfl_down_sync(0xffffffffu, bits, 1);
-  if ((tid & 1) == 0 && base + tid * kTileItems < n) bitmap[(base >> 5) + (tid >> 1)] = bits | (hi << 16);
-  const int64_t S0 = o_prev;
-  __shared__ int64_t s_end;  // O of the tile's last element: N for the final tile
-  if (tid == kTileThreads - 1) s_end = (base + kTile <= n) ? (int64_t)o[kTileItems - 1] : n;
+  if ((tid & 1) == 0 && e0 < len) bitmap[(base >> 5) + (tid >> 1)] = bits | (hi << 16);
+  const int S0 = o_prev;
+  __shared__ int s_end;  // O of the tile's last element: N for the final tile
+  if (tid == kTileThreads - 1) s_end = (len == kTile) ? o[kTileItems - 1] : (int)n;
   const bool heavy = __syncthreads_or(maxo > kLightMaxO);
-  const int64_t end = s_end;
+  const int end = s_end;
   if (!heavy && end - S0 <= kLightCap) {
     // light: own parents -> staged words
-    int64_t s = prev;
+    int q = prev - S0;
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) {
-      if (base + tid * kTileItems + j < n) {
-        const uint32_t parent = (uint32_t)(base + tid * kTileItems + j);
-        const int64_t e = o[j];
-        if (s < e) {
-          sbuf[sw4((int)(s - S0))] = parent | kFirst;
-          for (int64_t q = s + 1; q < e; ++q) sbuf[sw4((int)(q - S0))] = parent;
+      if (e0 + j < len) {
+        const int e = o[j] - S0;
+        if (q < e) {
+          sbuf[sw4(q)] = (pbase + j) | kFirst;
+          for (int r = q + 1; r < e; ++r) sbuf[sw4(r)] = pbase + j;
         }
-        s = e;
+        q = e;
       }
     }
     __syncthreads();
-    const int cnt = (int)(end - S0);
-    for (int i = tid; i < cnt; i += kTileThreads) words[S0 + i] = sbuf[sw4(i)];
+    const int cnt = end - S0;
+    uint32_t* dst = words + S0;
+    for (int i = tid; i < cnt; i += kTileThreads) dst[i] = sbuf[sw4(i)];
     __syncthreads();
     return;
   }
@@ -319,9 +343,9 @@ __device__ void tile_expand(const int32_t (&o)[kTileItems], int64_t o_prev, int6
     reinterpret_cast<int4*>(Os)[swz(tid * 4 + q)] = v;
   }
   __syncthreads();
-  for (int64_t r0 = S0; r0 < end; r0 += kTile) {
-    const int64_t sb = r0 + (int64_t)tid * kTileItems;
-    const int64_t se = min(sb + kTileItems, end);
+  for (int r0 = S0; r0 < end; r0 += kTile) {
+    const int sb = r0 + e0;
+    const int se = min(sb + kTileItems, end);
     if (sb < se) {
       int lo = 0, hi2 = len - 1;  // parent of slot sb: smallest x with O(x) > sb
       while (lo < hi2) {
@@ -332,19 +356,19 @@ __device__ void tile_expand(const int32_t (&o)[kTileItems], int64_t o_prev, int6
           lo = mid + 1;
       }
       int xi = lo;
-      int64_t ox = os_get(Os, xi);
-      int64_t oex = xi ? os_get(Os, xi - 1) : o_prev;
-      for (int64_t s = sb; s < se; ++s) {
+      int ox = os_get(Os, xi);
+      int oex = xi ? os_get(Os, xi - 1) : o_prev;
+      for (int s = sb; s < se; ++s) {
         while (ox <= s) {
           ++xi;
           oex = ox;
           ox = os_get(Os, xi);
         }
-        wbuf[sw4((int)(s - r0))] = (uint32_t)(base + xi) | (s == oex ? kFirst : 0u);
+        wbuf[sw4(s - r0)] = ((uint32_t)base + xi) | (s == oex ? kFirst : 0u);
       }
     }
     __syncthreads();
-    const int cnt = (int)min((int64_t)kTile, end - r0);
+    const int cnt = min(kTile, end - r0);
     for (int i = tid; i < cnt; i += kTileThreads) words[r0 + i] = wbuf[sw4(i)];
     __syncthreads();
   }
@@ -353,23 +377,22 @@ __device__ void tile_expand(const int32_t (&o)[kTileItems], int64_t o_prev, int6
 // ---------------------------------------------------------------------------
 // K2
 template <typename T, typename A, int UM>
-__global__ void __launch_bounds__(kTileThreads, 4) k_dv_expand(DvArgs<A> p) {
+__global__ void __launch_bounds__(kTileThreads, 3) k_dv_expand(DvArgs<A> p) {
   __shared__ __align__(16) uint4 stage[2 * kTile * 4 / 16];  // tile stage, then word staging (32 KB)
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ int32_t warp_last[kTileThreads / 32];
   griddep_wait();
   const int64_t b = blockIdx.x;
+  const int len = (int)min((int64_t)kTile, p.n - b * kTile);
   int32_t o[kTileItems];
-  int64_t o_prev;
+  int32_t o_prev;
   tile_offspring<T, A, UM>(p, b, stage, warp_sums, o, o_prev);
   if (p.O_out) tile_store<int32_t>(p.O_out, p.n, b * kTile, stage, o, policy_evict_last());
-  if (tile_decreases(o, o_prev, b * kTile, p.n, warp_last)) {
+  if (tile_decreases(o, o_prev, len, warp_last)) {
     if (threadIdx.x == 0) atomicOr(&p.state->flags, kNeedsRepair);
-    griddep_launch();
     return;  // the rare-path kernel recomputes everything
   }
   tile_expand(o, o_prev, b, p.n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), warp_last);
-  griddep_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -436,7 +459,7 @@ __global__ void __launch_bounds__(kTileThreads, 5) k_dv_inplace(const uint32_t* 
     status_or(status, PFR_ST_OVERFLOW);
   }
   if (max_steps && longest) atomicMax(max_steps, longest);
-  griddep_launch();
+  // (no early trigger: dependents launch at grid completion)
 }
 
 // ---------------------------------------------------------------------------
@@ -457,7 +480,7 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_rare(DvArgs<A> p) {
     // A: raw O per tile -> global, tile maxima
     for (int64_t b = blockIdx.x; b < p.tiles; b += gridDim.x) {
       int32_t o[kTileItems];
-      int64_t o_prev;
+      int32_t o_prev;
       tile_offspring<T, A, UM>(p, b, stage, warp_sums, o, o_prev);
       int64_t mx = INT64_MIN;
 #pragma unroll
@@ -499,7 +522,7 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_rare(DvArgs<A> p) {
         }
         if (b * kTile + threadIdx.x * kTileItems + j == n - 1) o[j] = (int32_t)n;
       }
-      const int64_t o_prev = b ? max(before_tiles, (int64_t)0) : 0;
+      const int32_t o_prev = b ? (int32_t)max(before_tiles, (int64_t)0) : 0;
       if (p.O_out) tile_store<int32_t>(p.O_out, n, b * kTile, stage, o, policy_evict_last());
       tile_expand(o, o_prev, b, n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), warp_last);
     }
