@@ -123,21 +123,25 @@ __device__ __noinline__ int32_t offspring_exact(A W, A total, int64_t n, const D
   return (int32_t)(o > n ? n : (o < 0 ? 0 : o));
 }
 
+// Fast path in 31-bit fixed point: r_fx = round(W * N/total * 2^31) (one
+// multiply + one conversion), t_fx = r_fx + u_fx (exact integer add).  The
+// float64 products differ from the reference's r = (W*N)/total by at most
+// 2^-51 r, the conversions by one unit, so whenever r and r+u sit more than
+// delta = r_fx / 2^44 + 4 units (far above those bounds) from an integer,
+// the floors are the reference's; otherwise the exact sequence runs.
 template <typename T, typename A, int UM>
-__device__ __forceinline__ int32_t offspring_of(A W, A total, A scale, int64_t n, const DvArgs<A>& p) {
+__device__ __forceinline__ int32_t offspring_of(A W, A total, A scale_fx, int64_t n, const DvArgs<A>& p) {
   if constexpr (sizeof(A) == 8) {
-    const double rf = __dmul_rn(W, scale);
-    const double tol = fmax(rf, 1.0) * 5.684341886080802e-14;  // 2^-44
-    const double fr = floor(rf);
-    if ((rf - fr) >= tol && (fr + 1.0 - rf) >= tol) {
-      int64_t k = (int64_t)fr + 1;
-      if (k > n) k = n;
-      const double tf = __dadd_rn(rf, (double)stratum_u<T, A, UM>(k - 1, p));
-      const double ft = floor(tf);
-      if ((tf - ft) >= tol && (ft + 1.0 - tf) >= tol) {
-        const int64_t o = (int64_t)ft;
-        return (int32_t)(o > n ? n : (o < 0 ? 0 : o));
-      }
+    const long long r = __double2ll_rn(__dmul_rn(W, scale_fx));
+    const long long dr = (r >> 44) + 4;
+    const long long k0 = r >> 31;
+    if (((r - dr) >> 31) == k0 && ((r + dr) >> 31) == k0) {
+      const long long k = k0 + 1 > n ? n : k0 + 1;
+      const long long u = __double2ll_rn((double)stratum_u<T, A, UM>(k - 1, p) * 2147483648.0);
+      const long long t = r + u;
+      const long long dt = (t >> 44) + 6;
+      const long long o = t >> 31;
+      if (((t - dt) >> 31) == o && ((t + dt) >> 31) == o) return (int32_t)(o > n ? n : (o < 0 ? 0 : o));
     }
   }
   return offspring_exact<T, A, UM>(W, total, n, p);
@@ -186,34 +190,59 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  // exclusive scan over the tile aggregates: serial within a thread's chunk,
-  // Kogge-Stone across threads, serial across warps (fixed association)
+  // exclusive scan over the tile aggregates, 4096 at a time through shared
+  // memory (coalesced loads): serial within a thread's 16, Kogge-Stone across
+  // threads, serial across warps, serial carry across chunks (fixed
+  // association => deterministic)
+  A* sagg = reinterpret_cast<A*>(stage);  // >= 4096 * 4 bytes; A=double needs 32 KB -> 2 passes of 2048
+  constexpr int kChunk = (kTile * sizeof(T)) / sizeof(A);
+  constexpr int kPer = kChunk / kTileThreads;
   const int T_ = (int)p.tiles;
-  const int chunk = (T_ + kTileThreads - 1) / kTileThreads;
-  const int c0 = threadIdx.x * chunk, c1 = min(c0 + chunk, T_);
-  A mine = A(0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  A carry = A(0);
   uint32_t fl = 0;
-  for (int i = c0; i < c1; ++i) {
-    mine = add_rn(mine, __ldcg(p.agg + i));
-    fl |= __ldcg(tile_flags(p) + i);
+  for (int c0 = 0; c0 < T_; c0 += kChunk) {
+    const int cn = min(kChunk, T_ - c0);
+    for (int i = threadIdx.x; i < cn; i += kTileThreads) {
+      sagg[i] = __ldcg(p.agg + c0 + i);
+      fl |= __ldcg(tile_flags(p) + c0 + i);
+    }
+    __syncthreads();
+    A v[kPer];
+    A mine = A(0);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = threadIdx.x * kPer + k;
+      v[k] = i < cn ? sagg[i] : A(0);
+      mine = add_rn(mine, v[k]);
+    }
+    const A incl = warp_inclusive_scan(mine);
+    A ex = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) ex = A(0);
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    A wp = carry, tot = carry;
+    for (int u = 0; u < kTileThreads / 32; ++u) {
+      if (u < warp) wp = add_rn(wp, warp_sums[u]);
+      tot = add_rn(tot, warp_sums[u]);
+    }
+    A run = lane ? add_rn(wp, ex) : wp;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = threadIdx.x * kPer + k;
+      if (i < cn) sagg[i] = run;
+      run = add_rn(run, v[k]);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn; i += kTileThreads) p.excl[c0 + i] = sagg[i];
+    carry = tot;
+    __syncthreads();
   }
   fl = __reduce_or_sync(0xffffffffu, fl);
-  const A incl = warp_inclusive_scan(mine);
-  A excl = __shfl_up_sync(0xffffffffu, incl, 1);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) excl = A(0);
-  if (lane == 31) warp_sums[warp] = incl;
   if (lane == 0 && fl) atomicOr(&cta_flags, fl);
   __syncthreads();
-  A wp = A(0);
-  for (int v = 0; v < warp; ++v) wp = add_rn(wp, warp_sums[v]);
-  A run = lane ? add_rn(wp, excl) : wp;
-  for (int i = c0; i < c1; ++i) {
-    p.excl[i] = run;
-    run = add_rn(run, __ldcg(p.agg + i));
-  }
-  if (c0 < T_ && c1 == T_) p.excl[T_] = run;  // the total
   if (threadIdx.x == 0) {
+    p.excl[T_] = carry;  // the total
     p.state->done = 0;
     p.state->flags = 0;
     status_or(p.status, cta_flags);
@@ -234,7 +263,7 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
   for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
   tile_scan<A>(s, warp_sums);
   const A total = p.excl[p.tiles];
-  const A scale = (A)p.n / total;
+  const A scale = sizeof(A) == 8 ? (A)p.n / total * (A)2147483648.0 : A(0);  // N/total * 2^31
   const A ex = p.excl[b];
   const int last = (p.n - 1 - base < kTile) ? (int)(p.n - 1 - base) : -1;
   const int e0 = threadIdx.x * kTileItems;
@@ -396,70 +425,153 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_dv_expand(DvArgs<A> p) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: 16 indices per thread, striped (index = base + 256 j + t), so the
-// coalesced word loads and the clustered chain loads of a warp share sectors;
-// all of a thread's pending chains advance together (16 loads in flight).
-constexpr int kInplaceItems = 16;
+// K3: persistent, warp-pipelined.  Each warp owns a contiguous run of
+// 256-index chunks (index = chunk + 32 k + lane: coalesced).  Per iteration
+// it (1) loads a chunk and resolves the trivial indices (has offspring, or a
+// loser slot that claims its own hole), (2) appends the holes that are first
+// slots -- pending backward chains -- to its shared-memory queue, and (3)
+// advances every queued chain by one step.  Chunk loads and chain loads of an
+// iteration are independent, so each iteration costs about one L2 round trip
+// and the chain latency hides under the streaming; the queue drains at the end.
+constexpr int kQCap = 512;        // queue entries per warp
+constexpr int kChunkK = 8;        // indices per lane per chunk
+constexpr int kChunkSpan = 32 * kChunkK;
+constexpr int kInplaceWarps = 8;  // warps per CTA
 
-__device__ __forceinline__ void resolve_tile(const uint32_t* __restrict__ words, const uint32_t* __restrict__ bitmap,
-                                             int64_t n, int32_t* __restrict__ c, int64_t base, int& longest,
-                                             bool& overflow) {
-  const int t = threadIdx.x;
-  // v[j]: the final output, or for a pending chain the current node
-  uint32_t v[kInplaceItems];
-  uint32_t active = 0;
+struct WarpQueue {
+  int32_t elem[kQCap];
+  uint32_t node[kQCap];
+  uint8_t steps[kQCap];
+};
+
+// one round over the queue: every entry takes one backward step; finished
+// entries write c, the rest are compacted in place (order preserved)
+__device__ __forceinline__ int queue_round(WarpQueue& q, int qlen, const uint32_t* __restrict__ words,
+                                           int32_t* __restrict__ c, int& longest, bool& overflow) {
+  const int lane = threadIdx.x & 31;
+  int out = 0;
+  for (int g = 0; g < qlen; g += 128) {
+    uint32_t wz[4];
+    int idx[4];
 #pragma unroll
-  for (int j = 0; j < kInplaceItems; ++j) {
-    const int64_t i = base + (int64_t)j * kTileThreads + t;
-    v[j] = 0;
-    if (i < n) {
-      const uint32_t wd = __ldcg(words + i);
-      const bool has = (__ldcg(bitmap + (i >> 5)) >> (i & 31)) & 1u;
-      v[j] = has ? (uint32_t)i : (wd & kParentMask);
-      if (!has && (wd & kFirst)) active |= 1u << j;
+    for (int r = 0; r < 4; ++r) {
+      idx[r] = g + 32 * r + lane;
+      if (idx[r] < qlen) wz[r] = __ldcg(words + q.node[idx[r]]);
     }
-  }
-  int steps = 0;
-  while (active) {
-    if (++steps > kBackBound) {
-      overflow = true;
-      break;
-    }
-    uint32_t wz[kInplaceItems];
+    __syncwarp();
 #pragma unroll
-    for (int j = 0; j < kInplaceItems; ++j)
-      if (active & (1u << j)) wz[j] = __ldcg(words + v[j]);
-#pragma unroll
-    for (int j = 0; j < kInplaceItems; ++j) {
-      if (active & (1u << j)) {
-        v[j] = wz[j] & kParentMask;
-        if (!(wz[j] & kFirst)) active &= ~(1u << j);
+    for (int r = 0; r < 4; ++r) {
+      const bool valid = idx[r] < qlen;
+      bool keep = false;
+      int32_t e = 0;
+      int st = 0;
+      if (valid) {
+        e = q.elem[idx[r]];
+        st = q.steps[idx[r]] + 1;
+        if (!(wz[r] & kFirst)) {
+          c[e] = (int32_t)(wz[r] & kParentMask);
+          longest = max(longest, st);
+        } else if (st >= kBackBound) {
+          overflow = true;
+        } else {
+          keep = true;
+        }
       }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      if (keep) {
+        const int pos = out + __popc(m & ((1u << lane) - 1));
+        q.elem[pos] = e;
+        q.node[pos] = wz[r] & kParentMask;
+        q.steps[pos] = (uint8_t)st;
+      }
+      out += __popc(m);
+      __syncwarp();
     }
   }
-  longest = max(longest, overflow ? kBackBound : steps);
-#pragma unroll
-  for (int j = 0; j < kInplaceItems; ++j) {
-    const int64_t i = base + (int64_t)j * kTileThreads + t;
-    if (i < n) __stcs(c + i, (int32_t)v[j]);
-  }
+  return out;
 }
 
-__global__ void __launch_bounds__(kTileThreads, 5) k_dv_inplace(const uint32_t* __restrict__ words,
-                                                             const uint32_t* __restrict__ bitmap, int64_t n,
-                                                             int32_t* __restrict__ c, int32_t* max_steps,
-                                                             DvState* state, uint32_t* status) {
+__global__ void __launch_bounds__(32 * kInplaceWarps) k_dv_inplace(const uint32_t* __restrict__ words,
+                                                                  const uint32_t* __restrict__ bitmap, int64_t n,
+                                                                  int32_t* __restrict__ c, int32_t* max_steps,
+                                                                  DvState* state, uint32_t* status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   griddep_wait();
   if (state->flags & kNeedsRepair) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpQueue& q = reinterpret_cast<WarpQueue*>(smem_raw)[warp];
+  const int64_t chunks = (n + kChunkSpan - 1) / kChunkSpan;
+  const int64_t gw = (int64_t)blockIdx.x * kInplaceWarps + warp, nw = (int64_t)gridDim.x * kInplaceWarps;
+  const int64_t ch0 = chunks * gw / nw, ch1 = chunks * (gw + 1) / nw;
+  int qlen = 0;
   int longest = 0;
   bool overflow = false;
-  resolve_tile(words, bitmap, n, c, (int64_t)blockIdx.x * kTileThreads * kInplaceItems, longest, overflow);
+  for (int64_t ch = ch0; ch < ch1; ++ch) {
+    const int64_t cb = ch * kChunkSpan;
+    uint32_t wd[kChunkK], bw[kChunkK];
+#pragma unroll
+    for (int k = 0; k < kChunkK; ++k) {
+      const int64_t i = cb + 32 * k + lane;
+      wd[k] = i < n ? __ldcs(words + i) : 0u;
+      bw[k] = (cb + 32 * k < n) ? __ldcs(bitmap + ((cb >> 5) + k)) : 0u;
+    }
+    // advance the pending chains while the chunk loads are in flight
+    if (qlen) qlen = queue_round(q, qlen, words, c, longest, overflow);
+#pragma unroll
+    for (int k = 0; k < kChunkK; ++k) {
+      const int64_t i = cb + 32 * k + lane;
+      const bool in = i < n;
+      const bool has = (bw[k] >> lane) & 1u;
+      const bool pend = in && !has && (wd[k] & kFirst);
+      if (in) __stcs(c + i, has ? (int32_t)i : (int32_t)(wd[k] & kParentMask));
+      const unsigned m = __ballot_sync(0xffffffffu, pend);
+      if (pend) {
+        const int pos = qlen + __popc(m & ((1u << lane) - 1));
+        q.elem[pos] = (int32_t)i;
+        q.node[pos] = wd[k] & kParentMask;
+        q.steps[pos] = 0;
+      }
+      qlen += __popc(m);
+    }
+    __syncwarp();
+    // keep room for the next chunk
+    while (qlen > kQCap - kChunkSpan) qlen = queue_round(q, qlen, words, c, longest, overflow);
+  }
+  while (qlen) qlen = queue_round(q, qlen, words, c, longest, overflow);
   if (overflow) {
     atomicOr(&state->flags, kOverflow);
     status_or(status, PFR_ST_OVERFLOW);
   }
-  if (max_steps && longest) atomicMax(max_steps, longest);
-  // (no early trigger: dependents launch at grid completion)
+  if (max_steps) {
+    longest = __reduce_max_sync(0xffffffffu, longest);
+    if (lane == 0 && longest) atomicMax(max_steps, longest);
+  }
+}
+
+// the repair path's in-place pass: a plain (non-persistent) sweep
+__device__ void resolve_all(const uint32_t* __restrict__ words, const uint32_t* __restrict__ bitmap, int64_t n,
+                            int32_t* __restrict__ c, int& longest, bool& overflow) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t wd = __ldcg(words + i);
+    const bool has = (__ldcg(bitmap + (i >> 5)) >> (i & 31)) & 1u;
+    if (has) {
+      c[i] = (int32_t)i;
+      continue;
+    }
+    uint32_t v = wd;
+    int st = 0;
+    while (v & kFirst) {
+      if (++st > kBackBound) {
+        overflow = true;
+        break;
+      }
+      v = __ldcg(words + (v & kParentMask));
+    }
+    c[i] = (int32_t)(v & kParentMask);
+    longest = max(longest, st);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -530,9 +642,7 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_rare(DvArgs<A> p) {
     // D: in-place indices
     bool overflow = false;
     int longest = 0;
-    const int64_t span = (int64_t)kTileThreads * kInplaceItems;
-    for (int64_t t = blockIdx.x; t * span < n; t += gridDim.x)
-      resolve_tile(p.words, p.bitmap, n, p.c, t * span, longest, overflow);
+    resolve_all(p.words, p.bitmap, n, p.c, longest, overflow);
     if (overflow) atomicOr(&p.state->flags, kOverflow);
     if (p.max_steps && longest) atomicMax(p.max_steps, longest);
     grid.sync();
@@ -585,11 +695,12 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_rare(DvArgs<A> p) {
 
 // ---------------------------------------------------------------------------
 template <typename K, typename... Args>
-cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t s, bool cooperative, Args... args) {
+cudaError_t launch_pdl_smem(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool cooperative,
+                            Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int na = 0;
@@ -607,6 +718,11 @@ cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t s, bool coo
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+template <typename K, typename... Args>
+cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t s, bool cooperative, Args... args) {
+  return launch_pdl_smem(kernel, grid, block, 0, s, cooperative, args...);
+}
+
 template <typename T, typename A, int UM>
 cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   const unsigned tiles = (unsigned)p.tiles;
@@ -616,9 +732,17 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
   if (e != cudaSuccess) return e;
-  const unsigned blocks3 = (unsigned)((p.n + kTile - 1) / kTile);
-  e = launch_pdl(k_dv_inplace, dim3(blocks3), dim3(256), s, false, (const uint32_t*)p.words,
-                 (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
+  static int occ3 = -1;
+  const size_t smem3 = sizeof(WarpQueue) * kInplaceWarps;
+  if (occ3 < 0) {
+    e = cudaFuncSetAttribute(k_dv_inplace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_dv_inplace, 32 * kInplaceWarps, smem3);
+    if (e != cudaSuccess) return e;
+    if (occ3 < 1) occ3 = 1;
+  }
+  e = launch_pdl_smem(k_dv_inplace, dim3(num_sms() * occ3), dim3(32 * kInplaceWarps), smem3, s, false,
+                      (const uint32_t*)p.words, (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
   if (e != cudaSuccess) return e;
   static int occ = -1;
   if (occ < 0) {
