@@ -29,6 +29,8 @@
 // claim graph.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "pfr_internal.h"
 #include "pfr_tile.cuh"
 
@@ -126,25 +128,59 @@ __device__ __noinline__ int32_t offspring_exact(A W, A total, int64_t n, const D
 // Fast path in 31-bit fixed point: r_fx = round(W * N/total * 2^31) (one
 // multiply + one conversion), t_fx = r_fx + u_fx (exact integer add).  The
 // float64 products differ from the reference's r = (W*N)/total by at most
-// 2^-51 r, the conversions by one unit, so whenever r and r+u sit more than
-// delta = r_fx / 2^44 + 4 units (far above those bounds) from an integer,
-// the floors are the reference's; otherwise the exact sequence runs.
+// 2^-51 r, the conversions by one unit, so whenever the fractional parts of
+// r and r+u sit more than dr = N/2^13 + 16 units (far above those bounds)
+// from an integer, the floors are the reference's; otherwise the exact IEEE
+// sequence runs.  All checks are 32-bit on the low word.
 template <typename T, typename A, int UM>
-__device__ __forceinline__ int32_t offspring_of(A W, A total, A scale_fx, int64_t n, const DvArgs<A>& p) {
+__device__ __forceinline__ int32_t offspring_of(A W, A total, A sfx, long long ufx_sys, uint32_t dr, int64_t n,
+                                                const DvArgs<A>& p) {
   if constexpr (sizeof(A) == 8) {
-    const long long r = __double2ll_rn(__dmul_rn(W, scale_fx));
-    const long long dr = (r >> 44) + 4;
-    const long long k0 = r >> 31;
-    if (((r - dr) >> 31) == k0 && ((r + dr) >> 31) == k0) {
-      const long long k = k0 + 1 > n ? n : k0 + 1;
-      const long long u = __double2ll_rn((double)stratum_u<T, A, UM>(k - 1, p) * 2147483648.0);
-      const long long t = r + u;
-      const long long dt = (t >> 44) + 6;
+    const long long r = __double2ll_rn(__dmul_rn(W, sfx));
+    const uint32_t span = 0x7FFFFFFFu - 2u * dr;
+    bool ok = ((uint32_t)r & 0x7FFFFFFFu) - dr <= span;
+    long long ufx = ufx_sys;
+    if constexpr (UM != kUSys) {
+      long long k = (r >> 31) + 1;
+      if (k > n) k = n;
+      if (k < 1) k = 1;
+      ufx = __double2ll_rn((double)stratum_u<T, A, UM>(k - 1, p) * 2147483648.0);
+    }
+    const long long t = r + ufx;
+    ok &= ((uint32_t)t & 0x7FFFFFFFu) - dr <= span;
+    if (ok) {
       const long long o = t >> 31;
-      if (((t - dt) >> 31) == o && ((t + dt) >> 31) == o) return (int32_t)(o > n ? n : (o < 0 ? 0 : o));
+      return (int32_t)(o > n ? n : o);
     }
   }
   return offspring_exact<T, A, UM>(W, total, n, p);
+}
+
+// blocked direct loads: thread t gets elements [16t, 16t + 16) of the tile
+// (L1-allocating 16-byte loads; the 4-8 loads of a thread hit the same lines)
+template <typename T>
+__device__ __forceinline__ void tile_load_direct(const T* __restrict__ in, int64_t n, int64_t base,
+                                                 T (&x)[kTileItems]) {
+  constexpr int kPerVec = 16 / sizeof(T);
+  const int64_t e0 = base + (int64_t)threadIdx.x * kTileItems;
+  if (e0 + kTileItems <= n) {
+    uint4 v[kTileItems / kPerVec];
+#pragma unroll
+    for (int q = 0; q < kTileItems / kPerVec; ++q) v[q] = __ldg(reinterpret_cast<const uint4*>(in + e0) + q);
+#pragma unroll
+    for (int q = 0; q < kTileItems / kPerVec; ++q) {
+      union {
+        uint4 u;
+        T e[kPerVec];
+      } tmp;
+      tmp.u = v[q];
+#pragma unroll
+      for (int e = 0; e < kPerVec; ++e) x[q * kPerVec + e] = tmp.e[e];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) x[j] = (e0 + j < n) ? in[e0 + j] : T(0);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -162,33 +198,37 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ uint32_t cta_flags;
   __shared__ bool is_last;
-  const int b = blockIdx.x;
-  const int64_t base = (int64_t)b * kTile;
-  const int len = (int)min((int64_t)kTile, p.n - base);
+  // persistent: CTA-strided tiles, one fence + one counter bump per CTA
   if (threadIdx.x == 0) cta_flags = 0;
-  T x[kTileItems];
-  tile_load<T>((const T*)p.w, p.n, base, stage, policy_evict_last(), x);  // keep w in L2 for K2
-  TileScan<A> s;
   uint32_t flags = 0;
-  const int e0 = threadIdx.x * kTileItems;
+  for (int64_t b = blockIdx.x; b < p.tiles; b += gridDim.x) {
+    const int64_t base = b * kTile;
+    const int len = (int)min((int64_t)kTile, p.n - base);
+    T x[kTileItems];
+    tile_load_direct<T>((const T*)p.w, p.n, base, x);
+    TileScan<A> s;
+    const int e0 = threadIdx.x * kTileItems;
 #pragma unroll
-  for (int j = 0; j < kTileItems; ++j) {
-    if (e0 + j < len) flags |= wflags(x[j]);
-    s.loc[j] = (A)x[j];
+    for (int j = 0; j < kTileItems; ++j) {
+      if (e0 + j < len) flags |= wflags(x[j]);
+      s.loc[j] = (A)x[j];
+    }
+    tile_scan<A>(s, warp_sums);
+    // aggregate := tile-local inclusive value at the tile's last position
+    if (threadIdx.x == kTileThreads - 1) p.agg[b] = add_rn(s.thread_excl, s.loc[kTileItems - 1]);
   }
   flags = __reduce_or_sync(0xffffffffu, flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(&cta_flags, flags);
-  tile_scan<A>(s, warp_sums);  // (ends with a barrier: cta_flags is complete)
-  if (threadIdx.x == kTileThreads - 1) {
-    // aggregate := tile-local inclusive value at the tile's last position
-    p.agg[b] = add_rn(s.thread_excl, s.loc[kTileItems - 1]);
-    tile_flags(p)[b] = cta_flags;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tile_flags(p)[blockIdx.x] = cta_flags;
     __threadfence();
     const unsigned t = atomicAdd(&p.state->done, 1u);
-    is_last = (t == (unsigned)(p.tiles - 1));
+    is_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (!is_last) return;
+  if (threadIdx.x == 0) cta_flags = 0;
   __threadfence();
   // exclusive scan over the tile aggregates, 4096 at a time through shared
   // memory (coalesced loads): serial within a thread's 16, Kogge-Stone across
@@ -203,10 +243,7 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   uint32_t fl = 0;
   for (int c0 = 0; c0 < T_; c0 += kChunk) {
     const int cn = min(kChunk, T_ - c0);
-    for (int i = threadIdx.x; i < cn; i += kTileThreads) {
-      sagg[i] = __ldcg(p.agg + c0 + i);
-      fl |= __ldcg(tile_flags(p) + c0 + i);
-    }
+    for (int i = threadIdx.x; i < cn; i += kTileThreads) sagg[i] = __ldcg(p.agg + c0 + i);
     __syncthreads();
     A v[kPer];
     A mine = A(0);
@@ -238,6 +275,7 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
     carry = tot;
     __syncthreads();
   }
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += kTileThreads) fl |= __ldcg(tile_flags(p) + i);
   fl = __reduce_or_sync(0xffffffffu, fl);
   if (lane == 0 && fl) atomicOr(&cta_flags, fl);
   __syncthreads();
@@ -257,26 +295,29 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
                                                int32_t (&o)[kTileItems], int32_t& o_prev) {
   const int64_t base = b * kTile;
   T x[kTileItems];
-  tile_load<T>((const T*)p.w, p.n, base, stage, policy_evict_first(), x);
+  tile_load_direct<T>((const T*)p.w, p.n, base, x);
   TileScan<A> s;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
   tile_scan<A>(s, warp_sums);
   const A total = p.excl[p.tiles];
-  const A scale = sizeof(A) == 8 ? (A)p.n / total * (A)2147483648.0 : A(0);  // N/total * 2^31
+  const A sfx = sizeof(A) == 8 ? (A)p.n / total * (A)2147483648.0 : A(0);  // N/total * 2^31
+  const long long ufx = sizeof(A) == 8 ? __double2ll_rn((double)p.u_sys * 2147483648.0) : 0;
+  const uint32_t dr = (uint32_t)(p.n >> 13) + 16u;
   const A ex = p.excl[b];
+  const A tex = s.thread_excl;
   const int last = (p.n - 1 - base < kTile) ? (int)(p.n - 1 - base) : -1;
   const int e0 = threadIdx.x * kTileItems;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
-    const A W = add_rn(ex, add_rn(s.thread_excl, s.loc[j]));
-    o[j] = (int32_t)offspring_of<T, A, UM>(W, total, scale, p.n, p);
+    const A W = add_rn(ex, add_rn(tex, s.loc[j]));
+    o[j] = offspring_of<T, A, UM>(W, total, sfx, ufx, dr, p.n, p);
     if (e0 + j == last) o[j] = (int32_t)p.n;  // O[N-1] = N
   }
   o_prev = 0;
   if (b > 0) {
     const A Wp = add_rn(p.excl[b - 1], p.agg[b - 1]);  // W at the last position of tile b-1
-    o_prev = (int32_t)offspring_of<T, A, UM>(Wp, total, scale, p.n, p);
+    o_prev = offspring_of<T, A, UM>(Wp, total, sfx, ufx, dr, p.n, p);
   }
 }
 
@@ -725,13 +766,24 @@ cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t s, bool coo
 
 template <typename T, typename A, int UM>
 cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
+  // PFR_DV_STAGES (profiling aid): launch only the first k kernels
+  static const int stages = [] {
+    const char* v = getenv("PFR_DV_STAGES");
+    return v ? atoi(v) : 4;
+  }();
   const unsigned tiles = (unsigned)p.tiles;
-  k_dv_reduce<T, A><<<tiles, kTileThreads, 0, s>>>(p);
+  static int occ1 = -1;
+  if (occ1 < 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_dv_reduce<T, A>, kTileThreads, 0);
+    if (occ1 < 1) occ1 = 1;
+  }
+  const unsigned grid1 = (unsigned)min((int64_t)num_sms() * occ1, p.tiles);
+  k_dv_reduce<T, A><<<grid1, kTileThreads, 0, s>>>(p);
   note_launch();
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || stages < 2) return e;
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || stages < 3) return e;
   static int occ3 = -1;
   const size_t smem3 = sizeof(WarpQueue) * kInplaceWarps;
   if (occ3 < 0) {
@@ -743,7 +795,7 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   }
   e = launch_pdl_smem(k_dv_inplace, dim3(num_sms() * occ3), dim3(32 * kInplaceWarps), smem3, s, false,
                       (const uint32_t*)p.words, (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || stages < 4) return e;
   static int occ = -1;
   if (occ < 0) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dv_rare<T, A, UM>, kTileThreads, 0);
