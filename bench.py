@@ -101,7 +101,16 @@ class Clocks:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 7:
-                self.samples.append(parts)
+                self.samples.append((time.time(), parts))
+
+    def wait_first(self, timeout=5.0, busy=None):
+        """Keep the GPU busy (``busy()``) until the sampler has produced a sample."""
+        t0 = time.time()
+        while self.proc and not self.samples and time.time() - t0 < timeout:
+            if busy:
+                busy()
+            else:
+                time.sleep(0.05)
 
     def __exit__(self, *exc):
         if self.proc:
@@ -111,15 +120,30 @@ class Clocks:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, window=None):
+        """Clocks over the samples taken inside ``window`` (t0, t1) -- the timed
+        region; when it is shorter than the sampling period, the samples
+        nearest to it (the GPU runs warm-up / e2e steps back to back around it)."""
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        chosen = self.samples
+        where = "whole run"
+        if window:
+            t0, t1 = window
+            inside = [s for s in self.samples if t0 <= s[0] <= t1]
+            if inside:
+                chosen, where = inside, "timed region"
+            else:
+                mid = 0.5 * (t0 + t1)
+                chosen = sorted(self.samples, key=lambda s: abs(s[0] - mid))[:3]
+                where = "nearest to the timed region (GPU busy with warm-up/e2e steps)"
+        samples = [s[1] for s in chosen]
+        sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        reasons = sorted({names[i] for s in samples for i in range(4) if s[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(samples), "sampled": where}
 
 
 # ---------------------------------------------------------------------------
@@ -266,8 +290,11 @@ def main():
                 evs.append((f"{alg}/{dt}", s0, s1))
         return evs
 
+    clk = Clocks(local).__enter__()
     for s in range(args.warmup):
         timed_step(10_000 + s, None)
+    # keep the GPU under load until the clock sampler is producing samples
+    clk.wait_first(busy=lambda: (timed_step(20_000, None), torch.cuda.synchronize()))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -276,13 +303,14 @@ def main():
     L.lib().pfr_launch_count(1)
     per_delivery = {}
     kernel_parts = {}
-    with Clocks(local) as clk:
-        all_evs, all_parts = [], []
-        for s in range(args.steps):
-            parts = []
-            all_evs.append(timed_step(s, parts))
-            all_parts.append(parts)
-        torch.cuda.synchronize()
+    t_wall0 = time.time()
+    all_evs, all_parts = [], []
+    for s in range(args.steps):
+        parts = []
+        all_evs.append(timed_step(s, parts))
+        all_parts.append(parts)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
     launches = int(L.lib().pfr_launch_count(1))
     total_ms = 0.0
     for evs in all_evs:
@@ -351,6 +379,9 @@ def main():
         e2e_ms = float(t.item())
     e2e_value = world * units_per_step / (e2e_ms / args.steps * 1e-3)
 
+    clk.__exit__(None, None, None)
+    clocks = clk.summary((t_wall0, t_wall1))
+
     # ---------------- north-star targets: N = 2^24 float32 ----------------
     targets = None
     if not args.no_targets:
@@ -381,7 +412,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "particles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "per_delivery_ms": {k: sum(v) / len(v) for k, v in per_delivery.items()},
             "status_bits": status,
             "targets": targets,

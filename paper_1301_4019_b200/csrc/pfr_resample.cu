@@ -198,6 +198,15 @@ struct RejArgs {
 
 constexpr int kRejChunk = 256;
 
+// Each lane evaluates kRejBatch consecutive trips of its slot per iteration:
+// the trips' proposals do not depend on earlier outcomes, so their Philox
+// words and weight gathers are all issued before the first comparison (4
+// gathers in flight per lane instead of one dependent L2 round trip per trip).
+// The first accepting trip of the batch wins, so results, trip counts and the
+// stream mapping are exactly those of a one-trip-at-a-time loop; the few
+// trips evaluated past the acceptance are discarded.
+constexpr int kRejBatch = 4;  // trips per lane per iteration (even)
+
 template <typename T, bool kCapped>
 __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
   const int lane = threadIdx.x & 31;
@@ -208,7 +217,6 @@ __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
   bool exhausted = false;                 // warp-uniform: no chunks left
   int64_t slot = -1;
   int64_t trip = 0;
-  uint32_t o[4];
   uint32_t flags = 0;
   int iter = 0;
   while (true) {
@@ -238,35 +246,67 @@ __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
     }
     if (__ballot_sync(0xffffffffu, slot >= 0) == 0) break;
     if (slot >= 0) {
-      if ((trip & 1) == 0) philox4x32_10((uint32_t)slot, (uint32_t)(trip >> 1), kTagRejection, 0, A.k0, A.k1, o);
-      const int h = (int)(trip & 1);
-      const int64_t j = trip == 0 ? slot
-                                  : (int64_t)bounded_u32(o[2 * h], nn, A.threshold, (uint32_t)slot,
-                                                         (uint32_t)trip, kTagRejection, A.k0, A.k1);
-      const T wj = ldg(A.w + j);
-      const T vj = kCapped ? (wj < capv ? wj : capv) : wj;
-      T uu;
-      if constexpr (sizeof(T) == 4) {
-        uu = u32_to_unit_f(o[2 * h + 1]);
-      } else {
-        uu = u32_to_unit_d(o[2 * h + 1]);
+      // trips trip .. trip+kRejBatch-1 (trip is even): counters (slot, trip/2 + q)
+      uint32_t j[kRejBatch];
+      T uu[kRejBatch], wj[kRejBatch];
+#pragma unroll
+      for (int q = 0; q < kRejBatch / 2; ++q) {
+        uint32_t o[4];
+        philox4x32_10((uint32_t)slot, (uint32_t)((trip >> 1) + q), kTagRejection, 0, A.k0, A.k1, o);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t t = trip + 2 * q + h;
+          j[2 * q + h] = t == 0 ? (uint32_t)slot
+                                : bounded_u32(o[2 * h], nn, A.threshold, (uint32_t)slot, (uint32_t)t, kTagRejection,
+                                              A.k0, A.k1);
+          if constexpr (sizeof(T) == 4)
+            uu[2 * q + h] = u32_to_unit_f(o[2 * h + 1]);
+          else
+            uu[2 * q + h] = u32_to_unit_d(o[2 * h + 1]);
+        }
       }
-      ++trip;
-      // beta <= v[j] / bound  <=>  beta * bound <= v[j]
-      if (uu * bound <= vj) {
-        A.a[slot] = (int32_t)j;
-        if (A.trips) A.trips[slot] = (int32_t)trip;
-        if (kCapped) A.out_w[slot] = (vj == T(0)) ? T(1) : div_rn_t(wj, vj);
+#pragma unroll
+      for (int q = 0; q < kRejBatch; ++q) wj[q] = ldg(A.w + j[q]);
+      int done = -1;  // batch position of the first accepting trip
+      bool stuck = false;
+#pragma unroll
+      for (int q = 0; q < kRejBatch; ++q) {
+        if (done < 0 && !stuck) {
+          const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
+          // beta <= v[j] / bound  <=>  beta * bound <= v[j]
+          if (uu[q] * bound <= vj)
+            done = q;
+          else if (trip + q + 1 >= A.max_trips)
+            stuck = true;
+        }
+      }
+      if (done >= 0) {
+        T wd = wj[0];
+        uint32_t jd = j[0];
+#pragma unroll
+        for (int q = 1; q < kRejBatch; ++q)
+          if (done == q) {
+            wd = wj[q];
+            jd = j[q];
+          }
+        A.a[slot] = (int32_t)jd;
+        if (A.trips) A.trips[slot] = (int32_t)(trip + done + 1);
+        if (kCapped) {
+          const T vd = wd < capv ? wd : capv;
+          A.out_w[slot] = (vd == T(0)) ? T(1) : div_rn_t(wd, vd);
+        }
         slot = -1;
-      } else if (trip >= A.max_trips) {
+      } else if (stuck) {
         flags |= PFR_ST_NOPROGRESS;
         A.a[slot] = (int32_t)slot;
-        if (A.trips) A.trips[slot] = (int32_t)trip;
+        if (A.trips) A.trips[slot] = (int32_t)A.max_trips;
         if (kCapped) A.out_w[slot] = T(1);
         slot = -1;
+      } else {
+        trip += kRejBatch;
       }
     }
-    if (((++iter) & 255) == 0) {
+    if (((++iter) & 63) == 0) {
       // give up early once any slot reported no progress (reference raises)
       if (__ballot_sync(0xffffffffu, flags != 0) || (*(volatile uint32_t*)A.status & PFR_ST_NOPROGRESS)) {
         flags |= PFR_ST_NOPROGRESS;
@@ -436,22 +476,26 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
   if (e != cudaSuccess) return e;
   const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
   const int64_t max_trips = max_rounds + 1;
-  // persistent: enough warps to fill the machine, chunks hand out the slots
-  const int blocks = num_sms() * 8;
+  // persistent: one resident wave fills the machine, chunks hand out the slots
+  auto blocks_for = [](auto kernel) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0) != cudaSuccess || occ < 1) occ = 1;
+    return num_sms() * occ;
+  };
   if (dtype == PFR_F64) {
     RejArgs<double> A{(const double*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
                       a, trips, (double*)out_w, next, status};
     if (cap > 0)
-      k_rejection_philox<double, true><<<blocks, 256, 0, s>>>(A);
+      k_rejection_philox<double, true><<<blocks_for(k_rejection_philox<double, true>), 256, 0, s>>>(A);
     else
-      k_rejection_philox<double, false><<<blocks, 256, 0, s>>>(A);
+      k_rejection_philox<double, false><<<blocks_for(k_rejection_philox<double, false>), 256, 0, s>>>(A);
   } else {
     RejArgs<float> A{(const float*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
                      a, trips, (float*)out_w, next, status};
     if (cap > 0)
-      k_rejection_philox<float, true><<<blocks, 256, 0, s>>>(A);
+      k_rejection_philox<float, true><<<blocks_for(k_rejection_philox<float, true>), 256, 0, s>>>(A);
     else
-      k_rejection_philox<float, false><<<blocks, 256, 0, s>>>(A);
+      k_rejection_philox<float, false><<<blocks_for(k_rejection_philox<float, false>), 256, 0, s>>>(A);
   }
   note_launch();
   return cudaGetLastError();

@@ -22,6 +22,8 @@ for r in range(reps):
     if which in ("all", "metropolis"):
         a = pf.metropolis_ancestors(w, 32, pf.RngStream(r), index_dtype=torch.int32)
         pf.permute_parallel(a, index_dtype=torch.int32)
+    if which in ("all", "rejection"):
+        a = pf.rejection_ancestors(w, float(w.max()), pf.RngStream(r), index_dtype=torch.int32)
     if which in ("all", "stratified"):
         pf.deliver(w, pf.ResamplerConfig("stratified"), pf.RngStream(r), index_dtype=torch.int32, out=c)
 torch.cuda.synchronize()
