@@ -125,7 +125,8 @@ double pfr_stream_uniform(const pfr_rng* rng, uint64_t index, uint32_t tag);
 /* inclusive_prefix_sum (primitives.py:34-42), exclusive_prefix_sum (45-51),
  * vector_sum (60-66), offspring_to_cumulative (ancestry.py:85-88).
  * Single pass with a deterministic lookback tree.  `out_dtype` is the dtype of
- * `out` (float: same as input; integer input: PFR_I64 or PFR_I32).  `total`
+ * `out` (float: same as input, or PFR_F64 for float32 input; integer input:
+ * PFR_I64 or PFR_I32).  `total`
  * (nullable, device) receives the sum (double for floats, int64 for ints).
  * Validation bits: NONFINITE for floats, NEGCOUNT for negative ints. */
 int pfr_scan(const void* in, void* out, int64_t n, int dtype, int out_dtype, int accum, int exclusive,
@@ -223,6 +224,53 @@ int pfr_check_predicate(const void* c, int64_t n, int idx_dtype, int32_t* result
 /* in-place copy step of the bootstrap filter (pf.py:86-97):
  * x[i] = x[c[i]] wherever c[i] != i, for `width` float64 values per particle */
 int pfr_copy_particles(double* x, int64_t n, int64_t width, const int32_t* c, void* stream);
+
+/* ---- one weight-sharded filter across GPUs --------------
+ * Each rank holds a contiguous shard [index_base, index_base + n_loc) of the
+ * N weights.  The host protocol (paper_1301_4019_b200/sharded.py) runs, per
+ * rank: pfr_scan (float64 output) -> all-gather of shard totals -> the calls
+ * below -> all-to-all of slot words / walkers.  The reference has no
+ * distributed path; these calls reproduce resamplers.py:139-153 and
+ * ancestry.py:139-174 over shards. */
+
+/* metropolis_ancestors (resamplers.py:204-234) for chains [chain_begin,
+ * chain_begin + chain_count) of the N-chain resampler, a[i - chain_begin];
+ * draws are those of the global chain numbers (PHILOX or NUMPY stream), so
+ * the union over ranks equals the single-GPU result. */
+int pfr_metropolis_range(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng, int64_t chain_begin,
+                         int64_t chain_count, int32_t* a, uint32_t* status, void* stream);
+
+/* Cumulative offspring of this shard's parents in global slot numbers
+ * (_offspring_from_positions, resamplers.py:139-153): W = prefix + W_loc[i]
+ * (W_loc = the shard's inclusive scan in float64), r = (W*N)/total,
+ * O = min(N, floor(r + u[k-1])), O = N at the global last particle. */
+int pfr_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double prefix, double total, int64_t n_global,
+                        int last_global, int stratified, double offset, const double* uniforms, const pfr_rng* rng,
+                        int32_t* O, void* stream);
+
+/* Slot words of the shard's slot window [o_begin, O[n_loc-1]):
+ * words[s - o_begin] = parent | 0x80000000 on a parent's first slot
+ * (cumulative_offspring_to_ancestors, ancestry.py:69-76, + prepermute's
+ * winner flag, ancestry.py:125-136); has[i] = o_i > 0. */
+int pfr_shard_words(const int32_t* O_loc, int64_t n_loc, int64_t index_base, int32_t o_begin, uint32_t* words,
+                    uint8_t* has, uint32_t* status, void* stream);
+
+/* In-place ancestry of the shard's indices from the slot words of those
+ * indices (received from their producers): c[x] for every x whose loser
+ * chain stays in the shard; chains leaving it are appended to pend as
+ * (hole, slot, steps) int32 triples, *pend_count (device, zeroed by caller). */
+int pfr_shard_resolve(const uint32_t* words, const uint8_t* has, int64_t n_loc, int64_t index_base, int32_t* c,
+                      int32_t* pend, int32_t* pend_count, int32_t* max_steps, uint32_t* status, void* stream);
+
+/* Advance routed walkers (hole, slot, steps) whose slot lies in this shard:
+ * resolved chains -> done (hole, value) pairs, chains leaving again -> fwd. */
+int pfr_shard_advance(const int32_t* walkers, int64_t count, const uint32_t* words, int64_t n_loc, int64_t index_base,
+                      int32_t* done, int32_t* done_count, int32_t* fwd, int32_t* fwd_count, int32_t* max_steps,
+                      uint32_t* status, void* stream);
+
+/* c[hole - index_base] = value for routed (hole, value) pairs */
+int pfr_shard_scatter(const int32_t* done, int64_t count, int64_t index_base, int64_t n_loc, int32_t* c,
+                      uint32_t* status, void* stream);
 
 #ifdef __cplusplus
 }

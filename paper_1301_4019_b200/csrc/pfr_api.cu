@@ -185,7 +185,9 @@ int pfr_scan(const void* in, void* out, int64_t n, int dtype, int out_dtype, int
   PFR_REQUIRE(valid_n(n), "n must be in [1, 2^31)");
   PFR_REQUIRE(in && out, "null array");
   PFR_REQUIRE(is_float(dtype) || is_index(dtype), "unsupported dtype");
-  if (is_float(dtype)) PFR_REQUIRE(out_dtype == dtype, "float scan keeps the input dtype");
+  if (is_float(dtype))
+    PFR_REQUIRE(out_dtype == dtype || (dtype == PFR_F32 && out_dtype == PFR_F64),
+                "float scan keeps the input dtype (or widens float32 to float64)");
   if (is_index(dtype)) PFR_REQUIRE(is_index(out_dtype), "integer scan needs an integer output");
   PFR_WS(PFR_OP_SCAN);
   const int64_t expect = (accum & 0x200) ? n : -1;  // internal: offspring_to_cumulative sum check
@@ -362,4 +364,72 @@ int pfr_copy_particles(double* x, int64_t n, int64_t width, const int32_t* c, vo
   return PFR_OK;
 }
 
+
+/* ---- weight-sharded single filter (pfr_shard.cu) ------------------------- */
+
+int pfr_metropolis_range(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng, int64_t chain_begin,
+                         int64_t chain_count, int32_t* a, uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && (a || chain_count == 0), "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(steps >= 0, "number of chain steps must be non-negative");
+  PFR_REQUIRE(rng && rng->mode != PFR_RNG_ARRAYS, "chain ranges need a PHILOX or NUMPY stream");
+  PFR_REQUIRE(chain_begin >= 0 && chain_count >= 0 && chain_begin + chain_count <= n, "chain range outside [0, N)");
+  PFR_CHECK_LAUNCH(launch_metropolis(w, n, dtype, steps, rng, nullptr, nullptr, PFR_I64, a, status,
+                                     (cudaStream_t)stream, chain_begin, chain_count),
+                   "pfr_metropolis_range");
+  return PFR_OK;
+}
+
+int pfr_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double prefix, double total, int64_t n_global,
+                        int last_global, int stratified, double offset, const double* uniforms, const pfr_rng* rng,
+                        int32_t* O, void* stream) {
+  PFR_REQUIRE(valid_n(n_loc) && valid_n(n_global) && n_loc <= n_global, "bad sizes");
+  PFR_REQUIRE(W_loc && O, "null array");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(std::isfinite(total) && total > 0 && std::isfinite(prefix) && prefix >= 0, "bad prefix/total");
+  if (stratified) PFR_REQUIRE(uniforms || (rng && rng->mode != PFR_RNG_ARRAYS), "stratified needs uniforms or an rng");
+  PFR_CHECK_LAUNCH(launch_shard_offspring(W_loc, n_loc, dtype, prefix, total, n_global, last_global, stratified, offset,
+                                          uniforms, rng, O, (cudaStream_t)stream),
+                   "pfr_shard_offspring");
+  return PFR_OK;
+}
+
+int pfr_shard_words(const int32_t* O_loc, int64_t n_loc, int64_t index_base, int32_t o_begin, uint32_t* words,
+                    uint8_t* has, uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n_loc) && index_base >= 0 && o_begin >= 0, "bad sizes");
+  PFR_REQUIRE(O_loc && words, "null array");
+  PFR_CHECK_LAUNCH(launch_shard_words(O_loc, n_loc, index_base, o_begin, words, has, status, (cudaStream_t)stream),
+                   "pfr_shard_words");
+  return PFR_OK;
+}
+
+int pfr_shard_resolve(const uint32_t* words, const uint8_t* has, int64_t n_loc, int64_t index_base, int32_t* c,
+                      int32_t* pend, int32_t* pend_count, int32_t* max_steps, uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n_loc) && index_base >= 0, "bad sizes");
+  PFR_REQUIRE(words && has && c && pend && pend_count, "null array");
+  PFR_CHECK_LAUNCH(launch_shard_resolve(words, has, n_loc, index_base, c, pend, pend_count, max_steps, status,
+                                        (cudaStream_t)stream),
+                   "pfr_shard_resolve");
+  return PFR_OK;
+}
+
+int pfr_shard_advance(const int32_t* walkers, int64_t count, const uint32_t* words, int64_t n_loc, int64_t index_base,
+                      int32_t* done, int32_t* done_count, int32_t* fwd, int32_t* fwd_count, int32_t* max_steps,
+                      uint32_t* status, void* stream) {
+  PFR_REQUIRE(count >= 0 && valid_n(n_loc) && index_base >= 0, "bad sizes");
+  PFR_REQUIRE(count == 0 || (walkers && words && done && done_count && fwd && fwd_count), "null array");
+  PFR_CHECK_LAUNCH(launch_shard_advance(walkers, count, words, n_loc, index_base, done, done_count, fwd, fwd_count,
+                                        max_steps, status, (cudaStream_t)stream),
+                   "pfr_shard_advance");
+  return PFR_OK;
+}
+
+int pfr_shard_scatter(const int32_t* done, int64_t count, int64_t index_base, int64_t n_loc, int32_t* c,
+                      uint32_t* status, void* stream) {
+  PFR_REQUIRE(count >= 0 && valid_n(n_loc), "bad sizes");
+  PFR_REQUIRE(count == 0 || (done && c), "null array");
+  PFR_CHECK_LAUNCH(launch_shard_scatter(done, count, index_base, n_loc, c, status, (cudaStream_t)stream),
+                   "pfr_shard_scatter");
+  return PFR_OK;
+}
 }  // extern "C"

@@ -92,10 +92,25 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
                                const Workspace& ws, cudaStream_t s);
 cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng,
                               const double* u_draws, const void* j_draws, int idx_dtype, int32_t* a,
-                              uint32_t* status, cudaStream_t s);
+                              uint32_t* status, cudaStream_t s, int64_t c_begin = 0, int64_t c_count = -1);
 cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
                              int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
                              const Workspace& ws, cudaStream_t s);
+
+// launchers (pfr_shard.cu): weight-sharded single filter
+cudaError_t launch_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double prefix, double total,
+                                   int64_t n_global, int last_global, int stratified, double offset,
+                                   const double* uniforms, const pfr_rng* rng, int32_t* O, cudaStream_t s);
+cudaError_t launch_shard_words(const int32_t* O, int64_t n_loc, int64_t index_base, int32_t o_begin, uint32_t* words,
+                               uint8_t* has, uint32_t* status, cudaStream_t s);
+cudaError_t launch_shard_resolve(const uint32_t* words, const uint8_t* has, int64_t n_loc, int64_t index_base,
+                                 int32_t* c, int32_t* pend, int32_t* pend_count, int32_t* max_steps, uint32_t* status,
+                                 cudaStream_t s);
+cudaError_t launch_shard_advance(const int32_t* walkers, int64_t count, const uint32_t* words, int64_t n_loc,
+                                 int64_t index_base, int32_t* done, int32_t* done_count, int32_t* fwd,
+                                 int32_t* fwd_count, int32_t* max_steps, uint32_t* status, cudaStream_t s);
+cudaError_t launch_shard_scatter(const int32_t* done, int64_t count, int64_t index_base, int64_t n_loc, int32_t* c,
+                                 uint32_t* status, cudaStream_t s);
 
 int num_sms();
 

@@ -50,14 +50,18 @@ __device__ __forceinline__ bool accept_ref(double u, T wk, T wj) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_metropolis_philox(const T* __restrict__ w, int64_t n, int64_t steps,
                                                            uint32_t k0, uint32_t k1, uint32_t threshold,
+                                                           int64_t c_begin, int64_t c_count,
                                                            int32_t* __restrict__ a) {
-  const int64_t first = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kChainsPerThread;
-  if (first >= n) return;
+  // chains [c_begin, c_begin + c_count) of the N-chain resampler (a sharded
+  // rank runs its slice with global chain numbers: same draws, same result)
+  const int64_t local = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kChainsPerThread;
+  if (local >= c_count) return;
+  const int64_t first = c_begin + local;
   int64_t k[kChainsPerThread];
   T wk[kChainsPerThread];
 #pragma unroll
   for (int c = 0; c < kChainsPerThread; ++c) {
-    const int64_t i = min(first + c, n - 1);
+    const int64_t i = min(first + c, c_begin + c_count - 1);
     k[c] = i;
     wk[c] = ldg(w + i);
   }
@@ -101,21 +105,23 @@ __global__ void __launch_bounds__(256) k_metropolis_philox(const T* __restrict__
   }
 #pragma unroll
   for (int c = 0; c < kChainsPerThread; ++c)
-    if (first + c < n) a[first + c] = (int32_t)k[c];
+    if (local + c < c_count) a[local + c] = (int32_t)k[c];
 }
 
 // Metropolis replaying numpy's stream (power-of-two N): per step the
 // generator yields N doubles then N integers (one u32 each, low half first).
 template <typename T>
 __global__ void __launch_bounds__(256) k_metropolis_numpy(const T* __restrict__ w, int64_t n, int64_t steps,
-                                                          Key2x64 key, int log2n, int32_t* __restrict__ a) {
-  const int64_t first = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kChainsPerThread;
-  if (first >= n) return;
+                                                          Key2x64 key, int log2n, int64_t c_begin, int64_t c_count,
+                                                          int32_t* __restrict__ a) {
+  const int64_t local = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kChainsPerThread;
+  if (local >= c_count) return;
+  const int64_t first = c_begin + local;
   int64_t k[kChainsPerThread];
   T wk[kChainsPerThread];
 #pragma unroll
   for (int c = 0; c < kChainsPerThread; ++c) {
-    const int64_t i = min(first + c, n - 1);
+    const int64_t i = min(first + c, c_begin + c_count - 1);
     k[c] = i;
     wk[c] = ldg(w + i);
   }
@@ -146,7 +152,7 @@ __global__ void __launch_bounds__(256) k_metropolis_numpy(const T* __restrict__ 
   }
 #pragma unroll
   for (int c = 0; c < kChainsPerThread; ++c)
-    if (first + c < n) a[first + c] = (int32_t)k[c];
+    if (local + c < c_count) a[local + c] = (int32_t)k[c];
 }
 
 // Metropolis from caller-supplied draws u[b*N + i] (float64), j[b*N + i]
@@ -430,9 +436,12 @@ cudaError_t launch_lower_bound(const void* W, int64_t n, int dtype, const double
 
 cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng,
                               const double* u_draws, const void* j_draws, int idx_dtype, int32_t* a,
-                              uint32_t* status, cudaStream_t s) {
+                              uint32_t* status, cudaStream_t s, int64_t c_begin, int64_t c_count) {
   const int mode = rng ? rng->mode : PFR_RNG_ARRAYS;
-  const int64_t threads = (n + kChainsPerThread - 1) / kChainsPerThread;
+  if (c_count < 0) c_count = n;
+  if (mode == PFR_RNG_ARRAYS && (c_begin != 0 || c_count != n)) return cudaErrorNotSupported;
+  if (c_count == 0) return cudaSuccess;
+  const int64_t threads = (c_count + kChainsPerThread - 1) / kChainsPerThread;
   const unsigned blocks = (unsigned)((threads + 255) / 256);
   if (mode == PFR_RNG_ARRAYS) {
     const unsigned b1 = (unsigned)((n + 255) / 256);
@@ -452,16 +461,16 @@ cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps
     if (l2 < 0 || n < 2) return cudaErrorNotSupported;  // numpy replay needs a power-of-two N
     Key2x64 key{rng->key0, rng->key1};
     if (dtype == PFR_F64)
-      k_metropolis_numpy<double><<<blocks, 256, 0, s>>>((const double*)w, n, steps, key, l2, a);
+      k_metropolis_numpy<double><<<blocks, 256, 0, s>>>((const double*)w, n, steps, key, l2, c_begin, c_count, a);
     else
-      k_metropolis_numpy<float><<<blocks, 256, 0, s>>>((const float*)w, n, steps, key, l2, a);
+      k_metropolis_numpy<float><<<blocks, 256, 0, s>>>((const float*)w, n, steps, key, l2, c_begin, c_count, a);
   } else {
     const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
     const uint32_t thr = lemire_threshold(n);
     if (dtype == PFR_F64)
-      k_metropolis_philox<double><<<blocks, 256, 0, s>>>((const double*)w, n, steps, k0, k1, thr, a);
+      k_metropolis_philox<double><<<blocks, 256, 0, s>>>((const double*)w, n, steps, k0, k1, thr, c_begin, c_count, a);
     else
-      k_metropolis_philox<float><<<blocks, 256, 0, s>>>((const float*)w, n, steps, k0, k1, thr, a);
+      k_metropolis_philox<float><<<blocks, 256, 0, s>>>((const float*)w, n, steps, k0, k1, thr, c_begin, c_count, a);
   }
   note_launch();
   return cudaGetLastError();

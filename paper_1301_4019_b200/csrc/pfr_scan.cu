@@ -445,6 +445,7 @@ cudaError_t launch_scan(const void* in, void* out, int64_t n, int dtype, int out
     case PFR_F64:
       return scan_typed<double, double, double, true>(PFR_SCAN_ARGS);
     case PFR_F32:
+      if (out_dtype == PFR_F64) return scan_typed<float, double, double, true>(PFR_SCAN_ARGS);
       if (native) return scan_typed<float, float, float, true>(PFR_SCAN_ARGS);
       return scan_typed<float, double, float, true>(PFR_SCAN_ARGS);
     case PFR_I32:

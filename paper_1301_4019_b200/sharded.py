@@ -1,0 +1,409 @@
+"""One resampling problem spread over several GPUs.
+
+The reference has no distributed path; its single-process
+semantics (resamplers.py:105-153, 204-234; ancestry.py:139-174) are kept
+exactly, and the data is partitioned so that each GPU streams only its share:
+
+* **systematic / stratified, one weight-sharded filter** -- rank g holds the
+  contiguous weight shard [base_g, base_g + n_g).  It scans its shard locally
+  (float64), an all-gather of the G shard totals gives every rank the weight
+  before its shard and W_N, and each rank computes the cumulative offspring
+  of its own parents in GLOBAL slot numbers (pfr_shard_offspring).  The slot
+  words of those parents (parent | FIRST) go, by one all-to-all, to the ranks
+  that own the slot indices; each rank then resolves the in-place ancestry
+  of its indices (pfr_shard_resolve).  Loser chains that cross a shard
+  boundary continue as walkers (hole, slot, steps) routed to the owner of
+  `slot` (pfr_shard_advance) until they reach their loser, and the value goes
+  back to the owner of the hole.  Drift between slot and parent is ~sqrt(N),
+  so only a thin band at each boundary travels.
+* **Metropolis** -- the weight vector is all-gathered once; rank g runs the
+  chains of its output slice with their global chain numbers
+  (pfr_metropolis_range), so the union is bit-identical to the single-GPU
+  result; the ancestry is all-gathered and permuted (permute is replicated).
+* **multinomial / rejection** -- replicated over the all-gathered weights
+  (same stream on every rank, identical results), each rank keeps its slice.
+* **batched independent filters** need no communication at all (each rank
+  calls the single-GPU API on its own filters).
+
+Collectives go through a small `Comm` interface: `DistComm` wraps
+torch.distributed (NCCL on B200s, gloo for CPU tests); `ThreadComm` runs G
+virtual ranks as threads of one process (one GPU), which is how the GPU tests
+exercise the sharded path on a single device.  The per-rank compute goes
+through `CudaShardOps` (libpfr kernels); there is no CPU implementation in
+the product.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .rng import as_stream
+
+__all__ = ["DistComm", "ThreadComm", "CudaShardOps", "deliver_sharded", "metropolis_sharded", "shard_bounds"]
+
+_FIRST = 0x80000000
+_TAG_SYSTEMATIC = 0x5359
+
+
+# ---------------------------------------------------------------------------
+# collectives
+
+
+class DistComm:
+    """torch.distributed collectives on `group` (payload tensors live on `device`:
+    CUDA for NCCL, CPU for gloo)."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
+                else torch.device("cpu")
+        self.device = torch.device(device)
+
+    def all_gather_scalars(self, x, dtype) -> list:
+        t = torch.tensor([x], dtype=dtype, device=self.device)
+        out = torch.empty(self.world, dtype=dtype, device=self.device)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.cpu().tolist()
+
+    def all_to_all(self, send: torch.Tensor, send_counts: list[int], width: int = 1) -> torch.Tensor:
+        """Variable all-to-all of rows of `width` int32; returns received rows in rank order."""
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=self.device)
+        rc = torch.empty_like(sc)
+        self.dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = rc.cpu().tolist()
+        flat = send.reshape(-1).to(self.device)
+        out = torch.empty(sum(recv_counts) * width, dtype=send.dtype, device=self.device)
+        self.dist.all_to_all_single(out, flat, [c * width for c in recv_counts], [c * width for c in send_counts],
+                                    group=self.group)
+        return out.reshape(-1, width) if width > 1 else out
+
+    def all_gather_var(self, t: torch.Tensor) -> torch.Tensor:
+        sizes = [int(s) for s in self.all_gather_scalars(t.numel(), torch.int64)]
+        m = max(sizes)
+        pad = torch.zeros(m, dtype=t.dtype, device=self.device)
+        pad[: t.numel()] = t.to(self.device)
+        out = torch.empty(m * self.world, dtype=t.dtype, device=self.device)
+        self.dist.all_gather_into_tensor(out, pad, group=self.group)
+        return torch.cat([out[r * m: r * m + sizes[r]] for r in range(self.world)])
+
+
+class _ThreadHub:
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+
+class ThreadComm:
+    """G virtual ranks as threads of one process (shared device memory); the
+    collectives exchange references under a barrier.  Create one hub per
+    group with `ThreadComm.group(G)` and give thread g `comms[g]`."""
+
+    def __init__(self, hub: _ThreadHub, rank: int, device=None):
+        self.hub = hub
+        self.rank = rank
+        self.world = hub.world
+        self.device = torch.device(device) if device is not None else None  # None: tensors stay where they are
+
+    @staticmethod
+    def group(world: int, device=None) -> list["ThreadComm"]:
+        hub = _ThreadHub(world)
+        return [ThreadComm(hub, r, device) for r in range(world)]
+
+    def _exchange(self, obj):
+        h = self.hub
+        h.barrier.wait()
+        h.slots[self.rank] = obj
+        h.barrier.wait()
+        got = list(h.slots)
+        h.barrier.wait()
+        return got
+
+    def all_gather_scalars(self, x, dtype) -> list:
+        return [type(x)(v) if not isinstance(x, torch.Tensor) else v for v in self._exchange(x)]
+
+    def all_to_all(self, send: torch.Tensor, send_counts: list[int], width: int = 1) -> torch.Tensor:
+        rows = send.reshape(-1, width) if width > 1 else send.reshape(-1)
+        starts = np.concatenate([[0], np.cumsum(send_counts)]).astype(np.int64)
+        pieces = [rows[starts[r]: starts[r + 1]] for r in range(self.world)]
+        if rows.is_cuda:
+            torch.cuda.current_stream().synchronize()  # producers' kernels done before peers read
+        got = self._exchange(pieces)
+        parts = [got[q][self.rank] for q in range(self.world)]
+        dev = self.device or send.device
+        return torch.cat([p.to(dev) for p in parts])
+
+    def all_gather_var(self, t: torch.Tensor) -> torch.Tensor:
+        if t.is_cuda:
+            torch.cuda.current_stream().synchronize()
+        got = self._exchange(t)
+        dev = self.device or t.device
+        return torch.cat([g.to(dev) for g in got])
+
+
+# ---------------------------------------------------------------------------
+# per-rank compute on the GPU (libpfr)
+
+
+class CudaShardOps:
+    """The per-rank kernels of the sharded path (include/pfr.h, 'weight-sharded').
+    Owns its workspace and status word, so virtual ranks sharing a device do
+    not share scratch."""
+
+    def __init__(self):
+        self.dev = L.device()
+        self._ws = None
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
+    def _workspace(self, n):
+        need = int(L.lib().pfr_workspace_bytes(L.OP_ANY, int(n), 0))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=self.dev)
+        return self._ws.data_ptr(), self._ws.numel()
+
+    def tensor(self, x, dtype):
+        return torch.as_tensor(x, dtype=dtype).to(self.dev)
+
+    def status_bits(self) -> int:
+        return L.read_status(self.status)
+
+    def check(self):
+        bits = L.read_status(self.status)
+        L.raise_weight_errors(bits & ~L.ST_POSITIVE, "w", False)
+        if bits & L.ST_NONTERMINATION:
+            raise RuntimeError("permutation chain walk failed to terminate")
+        if bits & (L.ST_RANGE | L.ST_NOTMONOTONE):
+            raise RuntimeError(f"sharded resampling: inconsistent shard data (status {bits:#x})")
+
+    def local_scan(self, w: torch.Tensor):
+        w = L.as_weights(w)
+        n = w.numel()
+        W = torch.empty(n, dtype=torch.float64, device=self.dev)
+        ws, wsb = self._workspace(n)
+        L.call("pfr_check_weights", w.data_ptr(), n, L.dtype_code(w), self.status.data_ptr(), L.stream_handle())
+        L.call("pfr_scan", w.data_ptr(), W.data_ptr(), n, L.dtype_code(w), L.F64, L.ACC_F64 | L.SCAN_MONOTONE, 0, None,
+               self.status.data_ptr(), ws, wsb, L.stream_handle())
+        return W, float(W[-1].item())
+
+    def systematic_offset(self, rng, mode):
+        k0, k1 = as_stream(rng).key()
+        r = L.PfrRng(k0, k1, L.rng_mode_code(mode), 0)
+        return float(L.lib().pfr_stream_uniform(r, 0, _TAG_SYSTEMATIC))
+
+    def offspring(self, W, wdtype, prefix, total, n_global, last, stratified, offset, uniforms, rng, mode):
+        n = W.numel()
+        O = torch.empty(n, dtype=torch.int32, device=self.dev)
+        k0, k1 = as_stream(rng).key() if rng is not None else (0, 0)
+        r = L.PfrRng(k0, k1, L.rng_mode_code(mode), 0)
+        uni = None if uniforms is None else torch.as_tensor(uniforms, dtype=torch.float64).to(self.dev).contiguous()
+        L.call("pfr_shard_offspring", W.data_ptr(), n, L.F32 if wdtype == torch.float32 else L.F64, float(prefix),
+               float(total), int(n_global), int(last), int(stratified), float(offset), L.ptr(uni), r, O.data_ptr(),
+               L.stream_handle())
+        return O
+
+    def words(self, O, base, o_begin):
+        n = O.numel()
+        o_end = int(O[-1].item())
+        words = torch.empty(max(o_end - o_begin, 0), dtype=torch.int32, device=self.dev)
+        has = torch.empty(n, dtype=torch.uint8, device=self.dev)
+        L.call("pfr_shard_words", O.data_ptr(), n, int(base), int(o_begin), words.data_ptr(), has.data_ptr(),
+               self.status.data_ptr(), L.stream_handle())
+        return words, has
+
+    def resolve(self, words, has, base):
+        n = has.numel()
+        c = torch.empty(n, dtype=torch.int32, device=self.dev)
+        pend = torch.empty((n, 3), dtype=torch.int32, device=self.dev)
+        cnt = torch.zeros(2, dtype=torch.int32, device=self.dev)  # [pending, max steps]
+        L.call("pfr_shard_resolve", words.data_ptr(), has.data_ptr(), n, int(base), c.data_ptr(), pend.data_ptr(),
+               cnt.data_ptr(), cnt[1:].data_ptr(), self.status.data_ptr(), L.stream_handle())
+        k, steps = cnt.tolist()
+        return c, pend[:k], steps
+
+    def advance(self, walkers, words, base, n_loc):
+        k = walkers.shape[0]
+        done = torch.empty((max(k, 1), 2), dtype=torch.int32, device=self.dev)
+        fwd = torch.empty((max(k, 1), 3), dtype=torch.int32, device=self.dev)
+        cnt = torch.zeros(3, dtype=torch.int32, device=self.dev)  # [done, fwd, max steps]
+        if k:
+            walkers = walkers.contiguous()
+            L.call("pfr_shard_advance", walkers.data_ptr(), k, words.data_ptr(), int(n_loc), int(base),
+                   done.data_ptr(), cnt[0:].data_ptr(), fwd.data_ptr(), cnt[1:].data_ptr(), cnt[2:].data_ptr(),
+                   self.status.data_ptr(), L.stream_handle())
+        nd, nf, steps = cnt.tolist()
+        return done[:nd], fwd[:nf], steps
+
+    def scatter(self, done, base, c):
+        k = done.shape[0]
+        if k:
+            done = done.contiguous()
+            L.call("pfr_shard_scatter", done.data_ptr(), k, int(base), c.numel(), c.data_ptr(),
+                   self.status.data_ptr(), L.stream_handle())
+
+    def metropolis_range(self, w_full, b, rng, mode, c_begin, c_count):
+        w_full = L.as_weights(w_full)
+        a = torch.empty(c_count, dtype=torch.int32, device=self.dev)
+        k0, k1 = as_stream(rng).key()
+        r = L.PfrRng(k0, k1, L.rng_mode_code(mode), 0)
+        L.call("pfr_metropolis_range", w_full.data_ptr(), w_full.numel(), L.dtype_code(w_full), int(b), r,
+               int(c_begin), int(c_count), a.data_ptr(), self.status.data_ptr(), L.stream_handle())
+        return a
+
+    def full_ancestors(self, w_full, config, rng, mode):
+        from .resamplers import resample_ancestors
+
+        kw = {"rng_mode": mode, "index_dtype": torch.int32}
+        return resample_ancestors(w_full, config, rng, **kw).ancestors
+
+    def permute(self, a_full):
+        from .ancestry import permute_parallel
+
+        return permute_parallel(a_full, index_dtype=torch.int32)
+
+
+# ---------------------------------------------------------------------------
+# the protocol
+
+
+def shard_bounds(sizes):
+    """Start index of every shard (rank order) and N."""
+    offs = np.concatenate([[0], np.cumsum(np.asarray(sizes, dtype=np.int64))])
+    return offs, int(offs[-1])
+
+
+def _owner(idx: torch.Tensor, offs: np.ndarray) -> torch.Tensor:
+    """rank owning each global index (shards are contiguous, in rank order)"""
+    b = torch.as_tensor(offs[1:-1], dtype=torch.int64, device=idx.device)
+    return torch.bucketize(idx.to(torch.int64), b, right=True)
+
+
+def _route(rows: torch.Tensor, key_col: int, offs: np.ndarray, comm, width: int) -> torch.Tensor:
+    """send each row to the rank owning rows[:, key_col]; returns the rows received"""
+    if rows.shape[0]:
+        dest = _owner(rows[:, key_col], offs)
+        order = torch.argsort(dest, stable=True)
+        rows = rows[order]
+        counts = torch.bincount(dest, minlength=comm.world).cpu().tolist()
+    else:
+        counts = [0] * comm.world
+    return comm.all_to_all(rows.contiguous(), counts, width).reshape(-1, width)
+
+
+def _fold(values):
+    """left fold in float64, the same association on every rank"""
+    acc = 0.0
+    out = []
+    for v in values:
+        out.append(acc)
+        acc = acc + float(v)
+    return out, acc
+
+
+def deliver_sharded(w_local, config, rng, *, comm, ops=None, rng_mode=None, uniforms=None,
+                    return_max_steps: bool = False):
+    """permute_parallel(resample_ancestors(w, config, rng).ancestors) for the
+    global weight vector w = concat(shards in rank order); returns this rank's
+    slice c[base:base+n_local] (global parent indices, int32).
+
+    systematic / stratified: weight-sharded (see module docstring);
+    metropolis: chain-partitioned over the all-gathered weights;
+    multinomial / rejection: replicated over the all-gathered weights."""
+    ops = ops or CudaShardOps()
+    alg = config.algorithm
+    if alg in ("systematic", "stratified"):
+        return _deliver_offspring_sharded(w_local, alg == "stratified", rng, comm, ops, rng_mode, uniforms,
+                                          return_max_steps)
+    sizes = [int(s) for s in comm.all_gather_scalars(int(w_local.numel()), torch.int64)]
+    offs, n = shard_bounds(sizes)
+    base, n_loc = int(offs[comm.rank]), sizes[comm.rank]
+    w_full = comm.all_gather_var(torch.as_tensor(w_local))
+    if alg == "metropolis":
+        a_loc = metropolis_sharded(w_local, config, rng, comm=comm, ops=ops, rng_mode=rng_mode, _w_full=w_full,
+                                   _sizes=sizes)
+        a_full = comm.all_gather_var(a_loc)
+    else:
+        a_full = ops.full_ancestors(w_full, config, rng, rng_mode)
+    c_full = ops.permute(torch.as_tensor(a_full))
+    c = c_full[base: base + n_loc]
+    ops.check()
+    return (c, None) if return_max_steps else c
+
+
+def metropolis_sharded(w_local, config_or_b, rng, *, comm, ops=None, rng_mode=None, _w_full=None, _sizes=None):
+    """metropolis_ancestors (resamplers.py:204-234) with the N chains split over
+    the ranks: returns this rank's slice of the ancestry (global indices)."""
+    from .resamplers import ResamplerConfig, resolve_metropolis_steps
+
+    ops = ops or CudaShardOps()
+    sizes = _sizes or [int(s) for s in comm.all_gather_scalars(int(w_local.numel()), torch.int64)]
+    offs, n = shard_bounds(sizes)
+    w_full = _w_full if _w_full is not None else comm.all_gather_var(torch.as_tensor(w_local))
+    if isinstance(config_or_b, ResamplerConfig):
+        b = resolve_metropolis_steps(w_full, config_or_b)
+    else:
+        b = int(config_or_b)
+    return ops.metropolis_range(w_full, b, rng, rng_mode, int(offs[comm.rank]), sizes[comm.rank])
+
+
+def _deliver_offspring_sharded(w_local, stratified, rng, comm, ops, rng_mode, uniforms, return_max_steps):
+    rank, world = comm.rank, comm.world
+    w_local = torch.as_tensor(w_local)
+    sizes = [int(s) for s in comm.all_gather_scalars(int(w_local.numel()), torch.int64)]
+    offs, n = shard_bounds(sizes)
+    base, n_loc = int(offs[rank]), sizes[rank]
+    if n_loc < 1:
+        raise ValueError("every rank needs a non-empty weight shard")
+
+    # 1. local scan, all-gather of shard totals -> prefix before this shard, W_N
+    W_loc, t_loc = ops.local_scan(w_local)
+    totals = comm.all_gather_scalars(float(t_loc), torch.float64)
+    # validation bits travel with the totals so every rank raises together
+    bits = 0
+    for b in comm.all_gather_scalars(ops.status_bits(), torch.int64):
+        bits |= int(b)
+    L.raise_weight_errors(bits & ~L.ST_POSITIVE, "w", False)
+    prefixes, total = _fold(totals)
+    if not total > 0:
+        raise ValueError("w must contain at least one strictly positive weight")
+
+    # 2. offspring of this rank's parents in global slot numbers
+    offset = 0.0 if stratified else ops.systematic_offset(rng, rng_mode)
+    O = ops.offspring(W_loc, w_local.dtype, prefixes[rank], total, n, rank == world - 1, stratified, offset,
+                      uniforms, rng, rng_mode)
+    ends = [int(e) for e in comm.all_gather_scalars(int(O[-1].item()), torch.int64)]
+    o_begin = ends[rank - 1] if rank else 0
+    o_end = ends[rank]
+
+    # 3. slot words of this rank's slot window -> the owners of those indices
+    words, has = ops.words(O, base, o_begin)
+    send = [max(0, min(o_end, int(offs[r + 1])) - max(o_begin, int(offs[r]))) for r in range(world)]
+    words_here = comm.all_to_all(words, send, 1).reshape(-1)
+    if words_here.numel() != n_loc:
+        raise RuntimeError(f"sharded delivery: received {words_here.numel()} slot words for {n_loc} indices")
+
+    # 4. local resolution, then walkers across shard boundaries
+    c, pend, steps = ops.resolve(words_here, has, base)
+    while True:
+        counts = comm.all_gather_scalars(int(pend.shape[0]), torch.int64)
+        if sum(counts) == 0:
+            break
+        arrived = _route(pend, 1, offs, comm, 3)
+        done, fwd, st = ops.advance(arrived, words_here, base, n_loc)
+        steps = max(steps, st)
+        back = _route(done, 0, offs, comm, 2)
+        ops.scatter(back, base, c)
+        pend = fwd
+    ops.check()
+    if return_max_steps:
+        return c, int(max(comm.all_gather_scalars(int(steps), torch.int64)))
+    return c

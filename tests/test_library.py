@@ -87,8 +87,14 @@ def test_argument_validation_without_gpu(lib):
     assert rc == L.E_ARG
     assert b"n must be" in lib.pfr_last_error()
     buf = ctypes.create_string_buffer(16)
-    rc = lib.pfr_scan(ctypes.addressof(buf), ctypes.addressof(buf), 4, L.F32, L.F64, 0, 0, None, None, None, 0, None)
-    assert rc == L.E_ARG
+    rc = lib.pfr_scan(ctypes.addressof(buf), ctypes.addressof(buf), 4, L.F64, L.F32, 0, 0, None, None, None, 0, None)
+    assert rc == L.E_ARG  # float scans never narrow (float32 -> float64 widening is allowed)
+    rc = lib.pfr_metropolis_range(ctypes.addressof(buf), 4, L.F32, 2, L.PfrRng(0, 0, 0, 0), 3, 2,
+                                  ctypes.addressof(buf), None, None)
+    assert rc == L.E_ARG and b"chain range" in lib.pfr_last_error()
+    rc = lib.pfr_shard_offspring(ctypes.addressof(buf), 4, L.F32, 0.0, 0.0, 8, 0, 0, 0.5, None, None,
+                                 ctypes.addressof(buf), None)
+    assert rc == L.E_ARG and b"prefix/total" in lib.pfr_last_error()
     rc = lib.pfr_metropolis(ctypes.addressof(buf), 4, L.F32, -1, None, None, None, L.I64, ctypes.addressof(buf),
                             None, None, 0, None)
     assert rc == L.E_ARG and b"non-negative" in lib.pfr_last_error()
