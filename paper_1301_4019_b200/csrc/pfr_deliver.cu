@@ -67,20 +67,50 @@ struct DvArgs {
   int32_t* max_steps;
   DvState* state;
   uint32_t* status;
+  int fx_S;          // fixed-point fraction bits of the offspring fast path
   // rare-path scratch
   int32_t* O;        // [n]
   int64_t* tmax;     // [tiles]
   int32_t *d, *J0, *J1, *R0, *R1;
 };
 
+// check_weights (diagnostics.py:38-51) on bit patterns: three integer maxima
+// per element instead of float classification.  Non-finite <=> magnitude
+// bits >= the infinity pattern; some x < 0 <=> unsigned max > the -0.0
+// pattern; some x > 0 <=> signed max > 0.  Zero padding is neutral.
 template <typename T>
-__device__ __forceinline__ uint32_t wflags(T x) {
-  uint32_t f = 0;
-  if (!isfinite((double)x)) f |= PFR_ST_NONFINITE;
-  if (x < T(0)) f |= PFR_ST_NEGATIVE;
-  if (x > T(0)) f |= PFR_ST_POSITIVE;
-  return f;
-}
+struct FlagAcc;
+template <>
+struct FlagAcc<float> {
+  uint32_t mag = 0u, ub = 0u;
+  int32_t sb = INT32_MIN;
+  __device__ __forceinline__ void add(float x) {
+    const uint32_t b = __float_as_uint(x);
+    mag = max(mag, b & 0x7FFFFFFFu);
+    ub = max(ub, b);
+    sb = max(sb, (int32_t)b);
+  }
+  __device__ __forceinline__ uint32_t flags() const {
+    return (mag >= 0x7F800000u ? PFR_ST_NONFINITE : 0u) | (ub > 0x80000000u ? PFR_ST_NEGATIVE : 0u) |
+           (sb > 0 ? PFR_ST_POSITIVE : 0u);
+  }
+};
+template <>
+struct FlagAcc<double> {
+  uint64_t mag = 0u, ub = 0u;
+  int64_t sb = INT64_MIN;
+  __device__ __forceinline__ void add(double x) {
+    const uint64_t b = (uint64_t)__double_as_longlong(x);
+    const uint64_t m = b & 0x7FFFFFFFFFFFFFFFull;
+    mag = m > mag ? m : mag;
+    ub = b > ub ? b : ub;
+    sb = (int64_t)b > sb ? (int64_t)b : sb;
+  }
+  __device__ __forceinline__ uint32_t flags() const {
+    return (mag >= 0x7FF0000000000000ull ? PFR_ST_NONFINITE : 0u) |
+           (ub > 0x8000000000000000ull ? PFR_ST_NEGATIVE : 0u) | (sb > 0 ? PFR_ST_POSITIVE : 0u);
+  }
+};
 
 // ---------------------------------------------------------------------------
 // stratum offsets (cast to the weight dtype, resamplers.py:124/135)
@@ -125,33 +155,66 @@ __device__ __noinline__ int32_t offspring_exact(A W, A total, int64_t n, const D
   return (int32_t)(o > n ? n : (o < 0 ? 0 : o));
 }
 
-// Fast path in 31-bit fixed point: r_fx = round(W * N/total * 2^31) (one
-// multiply + one conversion), t_fx = r_fx + u_fx (exact integer add).  The
-// float64 products differ from the reference's r = (W*N)/total by at most
-// 2^-51 r, the conversions by one unit, so whenever the fractional parts of
-// r and r+u sit more than dr = N/2^13 + 16 units (far above those bounds)
-// from an integer, the floors are the reference's; otherwise the exact IEEE
-// sequence runs.  All checks are 32-bit on the low word.
+// Fast path in S-bit fixed point, S = min(32, 51 - ceil(log2(N+1))):
+// r_fx = round(W * fl(N/total) * 2^S) from ONE fma against 2^52 (the integer
+// appears in the low mantissa bits: no float->int conversion), t_fx = r_fx +
+// u_fx (exact integer add).  Against the reference's r = fl(fl(W*N)/total) and
+// fl(r + u) the fixed-point values differ by at most 2 units of 2^-S
+// (3 roundings of 2^-53 relative on r < N, N*2^S < 2^51, plus the
+// quantisations), so whenever the fractional parts of r and r+u sit more than
+// dr = 4 units from an integer, both floors are the reference's; otherwise
+// the exact IEEE sequence runs (probability ~2^-S+4 per element).
+struct FxParams {
+  double sfx;       // fl(N / total) * 2^S
+  double scale;     // 2^S
+  long long ufx;    // round(u_sys * 2^S)
+  uint32_t mask;    // 2^S - 1
+  int S;
+};
+constexpr uint32_t kFxMargin = 4;
+
+__device__ __forceinline__ long long fx_round(double x, double scale) {
+  // round(x * scale) for 0 <= x * scale < 2^51
+  return __double_as_longlong(__fma_rn(x, scale, 4503599627370496.0)) - 0x4330000000000000LL;
+}
+
+__device__ __forceinline__ bool fx_safe(long long v, uint32_t mask) {
+  return (((uint32_t)v + kFxMargin) & mask) > 2 * kFxMargin;
+}
+
+// S = min(32, 51 - ceil(log2(N+1))) (host side: fx_bits)
+inline int fx_bits(int64_t n) {
+  int L = 1;
+  while ((int64_t(1) << L) <= n) ++L;  // 2^L > N
+  return L >= 19 ? 51 - L : 32;
+}
+
+template <typename A>
+__device__ __forceinline__ FxParams fx_params(int64_t n, A total, A u_sys, int S) {
+  FxParams f;
+  f.S = S;
+  f.scale = __longlong_as_double((long long)(1023 + S) << 52);  // 2^S
+  f.mask = S >= 32 ? 0xFFFFFFFFu : ((1u << S) - 1u);
+  f.sfx = __ddiv_rn((double)n, (double)total) * f.scale;
+  f.ufx = fx_round((double)u_sys, f.scale);
+  return f;
+}
+
 template <typename T, typename A, int UM>
-__device__ __forceinline__ int32_t offspring_of(A W, A total, A sfx, long long ufx_sys, uint32_t dr, int64_t n,
-                                                const DvArgs<A>& p) {
+__device__ __forceinline__ int32_t offspring_of(A W, A total, const FxParams& f, int64_t n, const DvArgs<A>& p) {
   if constexpr (sizeof(A) == 8) {
-    const long long r = __double2ll_rn(__dmul_rn(W, sfx));
-    const uint32_t span = 0x7FFFFFFFu - 2u * dr;
-    bool ok = ((uint32_t)r & 0x7FFFFFFFu) - dr <= span;
-    long long ufx = ufx_sys;
+    const long long r = fx_round(W, f.sfx);
+    bool ok = fx_safe(r, f.mask);
+    long long ufx = f.ufx;
     if constexpr (UM != kUSys) {
-      long long k = (r >> 31) + 1;
+      long long k = (r >> f.S) + 1;
       if (k > n) k = n;
       if (k < 1) k = 1;
-      ufx = __double2ll_rn((double)stratum_u<T, A, UM>(k - 1, p) * 2147483648.0);
+      ufx = fx_round((double)stratum_u<T, A, UM>(k - 1, p), f.scale);
     }
     const long long t = r + ufx;
-    ok &= ((uint32_t)t & 0x7FFFFFFFu) - dr <= span;
-    if (ok) {
-      const long long o = t >> 31;
-      return (int32_t)(o > n ? n : o);
-    }
+    ok &= fx_safe(t, f.mask);
+    if (ok) return min((int32_t)(t >> f.S), (int32_t)n);
   }
   return offspring_exact<T, A, UM>(W, total, n, p);
 }
@@ -200,24 +263,22 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   __shared__ bool is_last;
   // persistent: CTA-strided tiles, one fence + one counter bump per CTA
   if (threadIdx.x == 0) cta_flags = 0;
-  uint32_t flags = 0;
+  FlagAcc<T> facc;
   for (int64_t b = blockIdx.x; b < p.tiles; b += gridDim.x) {
     const int64_t base = b * kTile;
-    const int len = (int)min((int64_t)kTile, p.n - base);
     T x[kTileItems];
     tile_load_direct<T>((const T*)p.w, p.n, base, x);
     TileScan<A> s;
-    const int e0 = threadIdx.x * kTileItems;
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) {
-      if (e0 + j < len) flags |= wflags(x[j]);
+      facc.add(x[j]);
       s.loc[j] = (A)x[j];
     }
     tile_scan<A>(s, warp_sums);
     // aggregate := tile-local inclusive value at the tile's last position
     if (threadIdx.x == kTileThreads - 1) p.agg[b] = add_rn(s.thread_excl, s.loc[kTileItems - 1]);
   }
-  flags = __reduce_or_sync(0xffffffffu, flags);
+  const uint32_t flags = __reduce_or_sync(0xffffffffu, facc.flags());
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(&cta_flags, flags);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -301,9 +362,7 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
   for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
   tile_scan<A>(s, warp_sums);
   const A total = p.excl[p.tiles];
-  const A sfx = sizeof(A) == 8 ? (A)p.n / total * (A)2147483648.0 : A(0);  // N/total * 2^31
-  const long long ufx = sizeof(A) == 8 ? __double2ll_rn((double)p.u_sys * 2147483648.0) : 0;
-  const uint32_t dr = (uint32_t)(p.n >> 13) + 16u;
+  const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
   const A ex = p.excl[b];
   const A tex = s.thread_excl;
   const int last = (p.n - 1 - base < kTile) ? (int)(p.n - 1 - base) : -1;
@@ -311,13 +370,13 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
     const A W = add_rn(ex, add_rn(tex, s.loc[j]));
-    o[j] = offspring_of<T, A, UM>(W, total, sfx, ufx, dr, p.n, p);
+    o[j] = offspring_of<T, A, UM>(W, total, fx, p.n, p);
     if (e0 + j == last) o[j] = (int32_t)p.n;  // O[N-1] = N
   }
   o_prev = 0;
   if (b > 0) {
     const A Wp = add_rn(p.excl[b - 1], p.agg[b - 1]);  // W at the last position of tile b-1
-    o_prev = offspring_of<T, A, UM>(Wp, total, sfx, ufx, dr, p.n, p);
+    o_prev = offspring_of<T, A, UM>(Wp, total, fx, p.n, p);
   }
 }
 
@@ -339,23 +398,27 @@ __device__ __forceinline__ bool tile_decreases(const int32_t (&o)[kTileItems], i
 }
 
 // word staging in shared memory: 16-byte slots XOR-swizzled (bank spread
-// for the per-thread contiguous writes, conflict-free striped read-out)
+// for the per-thread contiguous accesses, conflict-free striped read-out)
 __device__ __forceinline__ int sw4(int pos) { return (swz(pos >> 2) << 2) | (pos & 3); }
 
-// smem O table (same swizzle): element x of the tile
-__device__ __forceinline__ int os_get(const int32_t* Os, int x) { return Os[sw4(x)]; }
+constexpr int kSlotCap = 2 * kTile;        // staged slot positions per chunk (32 KB of words)
+constexpr int kChunkSlots = kSlotCap - 4;  // slots per chunk (room for the 16-byte alignment shift)
+constexpr int kSlotsPerThread = kSlotCap / kTileThreads;  // 32
 
-constexpr int kLightCap = 2 * kTile;  // words a light tile may stage (32 KB)
-constexpr int kLightMaxO = 64;         // per-parent offspring bound of the light path
-
-// Expand the tile's parents over their slots: words (parent | FIRST) and the
-// has-offspring bitmap.  Light path (the common case): every thread writes
-// its own 16 parents' slots into shared memory, then the CTA streams the
-// tile's slot range out with coalesced stores.  Heavy path (a parent with more
-// than kLightMaxO offspring, or a slot range over 8192): balanced chunks of
-// 4096 slots, each thread locating its parent by binary search.
+// Expand the tile's parents over their slots: words (parent | FIRST) for the
+// tile's slot range [O(base-1), O(base+len-1)), and the has-offspring bitmap.
+// Per chunk of <= kChunkSlots slots: every parent whose first slot falls in
+// the chunk writes its head word and sets a head bit (no loops over
+// offspring counts, so no divergence however skewed the weights are); each
+// thread then owns 32 consecutive slot positions and fills the non-head slots
+// with the latest head's parent -- a block-wide exclusive max-scan of "last
+// head in my range" carries parents across threads (parents increase with
+// slot) and a running carry across chunks.  The chunk is written out with
+// coalesced 16-byte stores (positions are shifted so that global vectors are
+// aligned; partial edge vectors are written element-wise).
 __device__ void tile_expand(const int32_t (&o)[kTileItems], int32_t o_prev, int64_t b, int64_t n, uint32_t* words,
-                            uint32_t* bitmap, uint32_t* sbuf /* 32 KB */, int32_t* warp_last) {
+                            uint32_t* bitmap, uint32_t* sbuf /* kSlotCap words */, uint32_t* heads /* 256 */,
+                            int32_t* warp_last /* 8 */) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t base = b * kTile;
   const int len = (int)min((int64_t)kTile, n - base);
@@ -367,79 +430,96 @@ __device__ void tile_expand(const int32_t (&o)[kTileItems], int32_t o_prev, int6
   __syncthreads();
   if (lane == 0) prev = warp ? warp_last[warp - 1] : o_prev;
   uint32_t bits = 0;
-  int maxo = 0;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
     const int pv = j ? o[j - 1] : prev;
-    if (e0 + j < len) {
-      if (o[j] > pv) bits |= 1u << j;
-      maxo = max(maxo, o[j] - pv);
-    }
+    if (e0 + j < len && o[j] > pv) bits |= 1u << j;
   }
   const uint32_t hi = __shfl_down_sync(0xffffffffu, bits, 1);
   if ((tid & 1) == 0 && e0 < len) bitmap[(base >> 5) + (tid >> 1)] = bits | (hi << 16);
-  const int S0 = o_prev;
   __shared__ int s_end;  // O of the tile's last element: N for the final tile
   if (tid == kTileThreads - 1) s_end = (len == kTile) ? o[kTileItems - 1] : (int)n;
-  const bool heavy = __syncthreads_or(maxo > kLightMaxO);
-  const int end = s_end;
-  if (!heavy && end - S0 <= kLightCap) {
-    // light: own parents -> staged words
-    int q = prev - S0;
-#pragma unroll
-    for (int j = 0; j < kTileItems; ++j) {
-      if (e0 + j < len) {
-        const int e = o[j] - S0;
-        if (q < e) {
-          sbuf[sw4(q)] = (pbase + j) | kFirst;
-          for (int r = q + 1; r < e; ++r) sbuf[sw4(r)] = pbase + j;
-        }
-        q = e;
-      }
-    }
-    __syncthreads();
-    const int cnt = end - S0;
-    uint32_t* dst = words + S0;
-    for (int i = tid; i < cnt; i += kTileThreads) dst[i] = sbuf[sw4(i)];
-    __syncthreads();
-    return;
-  }
-  // heavy: O table in the first 16 KB, 4096-slot chunks staged in the second
-  int32_t* Os = reinterpret_cast<int32_t*>(sbuf);
-  uint32_t* wbuf = sbuf + kTile;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int4 v = make_int4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-    reinterpret_cast<int4*>(Os)[swz(tid * 4 + q)] = v;
-  }
   __syncthreads();
-  for (int r0 = S0; r0 < end; r0 += kTile) {
-    const int sb = r0 + e0;
-    const int se = min(sb + kTileItems, end);
-    if (sb < se) {
-      int lo = 0, hi2 = len - 1;  // parent of slot sb: smallest x with O(x) > sb
-      while (lo < hi2) {
-        const int mid = (lo + hi2) >> 1;
-        if (os_get(Os, mid) > sb)
-          hi2 = mid;
-        else
-          lo = mid + 1;
-      }
-      int xi = lo;
-      int ox = os_get(Os, xi);
-      int oex = xi ? os_get(Os, xi - 1) : o_prev;
-      for (int s = sb; s < se; ++s) {
-        while (ox <= s) {
-          ++xi;
-          oex = ox;
-          ox = os_get(Os, xi);
+  const int end = s_end;
+  int carry = -1;  // parent of the last slot of the previous chunk
+  for (int c0 = o_prev; c0 < end; c0 += kChunkSlots) {
+    const int cn = min(kChunkSlots, end - c0);
+    const int sh = c0 & 3;  // position = slot - c0 + sh keeps global vectors 16-byte aligned
+    heads[tid] = 0u;
+    __syncthreads();
+    // heads: parents whose first slot lies in this chunk.  A thread's heads
+    // are increasing and usually span one or two head words: their bits are
+    // gathered in registers and published with <= 2 shared atomics.
+    {
+      int q = prev;
+      const int wbase = max(prev - c0 + sh, 0) >> 5;
+      uint32_t m0 = 0u, m1 = 0u;
+#pragma unroll
+      for (int j = 0; j < kTileItems; ++j) {
+        if (bits & (1u << j)) {
+          const int r = q - c0;
+          if ((unsigned)r < (unsigned)cn) {
+            const int pos = r + sh;
+            sbuf[sw4(pos)] = (pbase + j) | kFirst;
+            const int d = (pos >> 5) - wbase;
+            const uint32_t bit = 1u << (pos & 31);
+            if (d == 0)
+              m0 |= bit;
+            else if (d == 1)
+              m1 |= bit;
+            else
+              atomicOr(&heads[pos >> 5], bit);
+          }
         }
-        wbuf[sw4(s - r0)] = ((uint32_t)base + xi) | (s == oex ? kFirst : 0u);
+        if (e0 + j < len) q = o[j];
       }
+      if (m0) atomicOr(&heads[wbase], m0);
+      if (m1) atomicOr(&heads[wbase + 1], m1);
     }
     __syncthreads();
-    const int cnt = min(kTile, end - r0);
-    for (int i = tid; i < cnt; i += kTileThreads) words[r0 + i] = wbuf[sw4(i)];
+    // fill: thread owns positions [32 tid, 32 tid + 32)
+    const int p0 = tid * kSlotsPerThread;
+    const bool active = p0 < cn + sh;  // warp-uniform for all but one warp
+    const uint32_t hb = active ? heads[tid] : 0u;
+    int last_head = -1;
+    if (hb) last_head = (int)(sbuf[sw4(p0 + 31 - __clz(hb))] & kParentMask);
+    int blk_max;
+    const int before = block_excl_max<int>(last_head, -1, warp_last, blk_max);
+    if (active) {
+      uint32_t cur = (uint32_t)max(carry, before);
+      uint4* sv = reinterpret_cast<uint4*>(sbuf);
+#pragma unroll
+      for (int k = 0; k < kSlotsPerThread / 4; ++k) {
+        uint4 v = sv[swz(p0 / 4 + k)];
+        uint32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (hb & (1u << (4 * k + t)))
+            cur = e[t] & kParentMask;
+          else
+            e[t] = cur;
+        }
+        sv[swz(p0 / 4 + k)] = make_uint4(e[0], e[1], e[2], e[3]);
+      }
+    }
+    carry = max(carry, blk_max);
+    __syncthreads();
+    // write out positions [sh, sh + cn) -> words[c0 - sh + pos]
+    uint32_t* dst = words + (c0 - sh);
+    const int nvec = (cn + sh + 3) >> 2;
+    const uint4* sv = reinterpret_cast<const uint4*>(sbuf);
+    for (int v = tid; v < nvec; v += kTileThreads) {
+      const uint4 x = sv[swz(v)];
+      const int p = 4 * v;
+      if (p >= sh && p + 4 <= sh + cn) {
+        reinterpret_cast<uint4*>(dst)[v] = x;
+      } else {
+        const uint32_t e[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (p + t >= sh && p + t < sh + cn) dst[p + t] = e[t];
+      }
+    }
     __syncthreads();
   }
 }
@@ -448,7 +528,8 @@ __device__ void tile_expand(const int32_t (&o)[kTileItems], int32_t o_prev, int6
 // K2
 template <typename T, typename A, int UM>
 __global__ void __launch_bounds__(kTileThreads, 3) k_dv_expand(DvArgs<A> p) {
-  __shared__ __align__(16) uint4 stage[2 * kTile * 4 / 16];  // tile stage, then word staging (32 KB)
+  __shared__ __align__(16) uint4 stage[kSlotCap * 4 / 16];  // word staging (32 KB)
+  __shared__ uint32_t heads[kTileThreads];
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ int32_t warp_last[kTileThreads / 32];
   griddep_wait();
@@ -462,124 +543,139 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_dv_expand(DvArgs<A> p) {
     if (threadIdx.x == 0) atomicOr(&p.state->flags, kNeedsRepair);
     return;  // the rare-path kernel recomputes everything
   }
-  tile_expand(o, o_prev, b, p.n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), warp_last);
+  tile_expand(o, o_prev, b, p.n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), heads, warp_last);
 }
 
 // ---------------------------------------------------------------------------
-// K3: persistent, warp-pipelined.  Each warp owns a contiguous run of
-// 256-index chunks (index = chunk + 32 k + lane: coalesced).  Per iteration
-// it (1) loads a chunk and resolves the trivial indices (has offspring, or a
-// loser slot that claims its own hole), (2) appends the holes that are first
-// slots -- pending backward chains -- to its shared-memory queue, and (3)
-// advances every queued chain by one step.  Chunk loads and chain loads of an
-// iteration are independent, so each iteration costs about one L2 round trip
-// and the chain latency hides under the streaming; the queue drains at the end.
-constexpr int kQCap = 512;        // queue entries per warp
-constexpr int kChunkK = 8;        // indices per lane per chunk
-constexpr int kChunkSpan = 32 * kChunkK;
-constexpr int kInplaceWarps = 8;  // warps per CTA
+// K3: persistent; each warp owns a contiguous run of 32-index groups (lane l
+// takes index 32k + l: coalesced loads of the slot words, coalesced stores of
+// c).  c[x] = x for indices with offspring and the slot's parent for
+// non-first holes.  A first-slot hole starts a backward chain (z = parent(z)
+// while z is a first slot): chains are appended to a per-warp queue in shared
+// memory (ballot compaction) and advanced in STEP PASSES that run only when
+// the queue holds >= 8 chains per lane: each pass issues up to 8 independent
+// chain loads per lane, resolves, and compacts the survivors in place.  So a
+// chain step costs one full-lane slot (no divergence) and its L2 latency is
+// shared by 8 loads.  Chain steps reach 10^4+ slots (drift x steps), so they
+// are L2 reads of the words written by K2.
+constexpr int kIpThreads = 256;
+constexpr int kIpWarps = kIpThreads / 32;
+constexpr int kQ = 512;          // queue entries per warp
+constexpr int kStepPer = 4;      // chain loads per lane per step batch
+constexpr int kScanG = 4;        // 32-index groups scanned per iteration
+constexpr int kGroup = 32;
 
-struct WarpQueue {
-  int32_t elem[kQCap];
-  uint32_t node[kQCap];
-  uint8_t steps[kQCap];
+struct IpQueue {
+  uint32_t x[kIpWarps][kQ];
+  uint32_t z[kIpWarps][kQ];
+  uint8_t st[kIpWarps][kQ];
 };
 
-// one round over the queue: every entry takes one backward step; finished
-// entries write c, the rest are compacted in place (order preserved)
-__device__ __forceinline__ int queue_round(WarpQueue& q, int qlen, const uint32_t* __restrict__ words,
-                                           int32_t* __restrict__ c, int& longest, bool& overflow) {
-  const int lane = threadIdx.x & 31;
+// one step for every queued chain; survivors compacted to the front
+__device__ __forceinline__ int step_pass(IpQueue& Q, int warp, int lane, int qlen, const uint32_t* __restrict__ words,
+                                         int32_t* __restrict__ c, int& longest, bool& overflow) {
   int out = 0;
-  for (int g = 0; g < qlen; g += 128) {
-    uint32_t wz[4];
-    int idx[4];
+  for (int b = 0; b < qlen; b += 32 * kStepPer) {
+    uint32_t x[kStepPer], z[kStepPer], w[kStepPer];
+    int st[kStepPer];
+    bool valid[kStepPer];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      idx[r] = g + 32 * r + lane;
-      if (idx[r] < qlen) wz[r] = __ldcg(words + q.node[idx[r]]);
+    for (int i = 0; i < kStepPer; ++i) {
+      const int e = b + 32 * i + lane;
+      valid[i] = e < qlen;
+      if (valid[i]) {
+        x[i] = Q.x[warp][e];
+        z[i] = Q.z[warp][e];
+        st[i] = Q.st[warp][e] + 1;
+        w[i] = __ldcg(words + z[i]);
+      }
     }
     __syncwarp();
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const bool valid = idx[r] < qlen;
+    for (int i = 0; i < kStepPer; ++i) {
+      if (b + 32 * i >= qlen) break;  // warp-uniform
       bool keep = false;
-      int32_t e = 0;
-      int st = 0;
-      if (valid) {
-        e = q.elem[idx[r]];
-        st = q.steps[idx[r]] + 1;
-        if (!(wz[r] & kFirst)) {
-          c[e] = (int32_t)(wz[r] & kParentMask);
-          longest = max(longest, st);
-        } else if (st >= kBackBound) {
-          overflow = true;
+      if (valid[i]) {
+        if (!(w[i] & kFirst)) {
+          c[x[i]] = (int32_t)(w[i] & kParentMask);
+          longest = max(longest, st[i]);
+        } else if (st[i] >= kBackBound) {
+          overflow = true;  // abandoned: the rare-path kernel resolves every chain
         } else {
           keep = true;
         }
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
-      __syncwarp();
       if (keep) {
         const int pos = out + __popc(m & ((1u << lane) - 1));
-        q.elem[pos] = e;
-        q.node[pos] = wz[r] & kParentMask;
-        q.steps[pos] = (uint8_t)st;
+        Q.x[warp][pos] = x[i];
+        Q.z[warp][pos] = w[i] & kParentMask;
+        Q.st[warp][pos] = (uint8_t)st[i];
       }
       out += __popc(m);
-      __syncwarp();
     }
+    __syncwarp();
   }
   return out;
 }
 
-__global__ void __launch_bounds__(32 * kInplaceWarps) k_dv_inplace(const uint32_t* __restrict__ words,
-                                                                  const uint32_t* __restrict__ bitmap, int64_t n,
-                                                                  int32_t* __restrict__ c, int32_t* max_steps,
-                                                                  DvState* state, uint32_t* status) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// classify one 32-index group: trivial indices store c, first-slot holes queue
+__device__ __forceinline__ void scan_group(IpQueue& Q, int warp, int lane, uint32_t x, bool in, uint32_t wd,
+                                           uint32_t bw, int& qlen, int32_t* __restrict__ c) {
+  const bool has = (bw >> lane) & 1u;
+  const bool pend = in && !has && (wd & kFirst);
+  if (in && !pend) __stcs(c + x, has ? (int32_t)x : (int32_t)(wd & kParentMask));
+  const unsigned m = __ballot_sync(0xffffffffu, pend);
+  if (pend) {
+    const int pos = qlen + __popc(m & ((1u << lane) - 1));
+    Q.x[warp][pos] = x;
+    Q.z[warp][pos] = wd & kParentMask;
+    Q.st[warp][pos] = 0;
+  }
+  qlen += __popc(m);
+}
+
+__global__ void __launch_bounds__(kIpThreads) k_dv_inplace(const uint32_t* __restrict__ words,
+                                                          const uint32_t* __restrict__ bitmap, int64_t n,
+                                                          int32_t* __restrict__ c, int32_t* max_steps,
+                                                          DvState* state, uint32_t* status) {
+  __shared__ IpQueue Q;
   griddep_wait();
   if (state->flags & kNeedsRepair) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpQueue& q = reinterpret_cast<WarpQueue*>(smem_raw)[warp];
-  const int64_t chunks = (n + kChunkSpan - 1) / kChunkSpan;
-  const int64_t gw = (int64_t)blockIdx.x * kInplaceWarps + warp, nw = (int64_t)gridDim.x * kInplaceWarps;
-  const int64_t ch0 = chunks * gw / nw, ch1 = chunks * (gw + 1) / nw;
+  const uint32_t nn = (uint32_t)n;
+  const uint32_t groups = (nn + kGroup - 1) / kGroup;
+  const uint32_t gw = blockIdx.x * kIpWarps + warp, nw = gridDim.x * kIpWarps;
+  const uint32_t g0 = (uint32_t)((uint64_t)groups * gw / nw), g1 = (uint32_t)((uint64_t)groups * (gw + 1) / nw);
+  const uint32_t gfull = nn / kGroup;  // groups entirely below n
   int qlen = 0;
   int longest = 0;
   bool overflow = false;
-  for (int64_t ch = ch0; ch < ch1; ++ch) {
-    const int64_t cb = ch * kChunkSpan;
-    uint32_t wd[kChunkK], bw[kChunkK];
+  uint32_t g = g0;
+  // steady state: whole iterations, no bounds checks
+  for (; g + kScanG <= min(g1, gfull); g += kScanG) {
+    if (qlen >= 64) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
+    while (qlen > kQ - 32 * kScanG) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
+    uint32_t wd[kScanG], bw[kScanG];
 #pragma unroll
-    for (int k = 0; k < kChunkK; ++k) {
-      const int64_t i = cb + 32 * k + lane;
-      wd[k] = i < n ? __ldcs(words + i) : 0u;
-      bw[k] = (cb + 32 * k < n) ? __ldcs(bitmap + ((cb >> 5) + k)) : 0u;
+    for (int q = 0; q < kScanG; ++q) {
+      wd[q] = __ldcs(words + (g + q) * kGroup + lane);
+      bw[q] = __ldg(bitmap + g + q);
     }
-    // advance the pending chains while the chunk loads are in flight
-    if (qlen) qlen = queue_round(q, qlen, words, c, longest, overflow);
 #pragma unroll
-    for (int k = 0; k < kChunkK; ++k) {
-      const int64_t i = cb + 32 * k + lane;
-      const bool in = i < n;
-      const bool has = (bw[k] >> lane) & 1u;
-      const bool pend = in && !has && (wd[k] & kFirst);
-      if (in) __stcs(c + i, has ? (int32_t)i : (int32_t)(wd[k] & kParentMask));
-      const unsigned m = __ballot_sync(0xffffffffu, pend);
-      if (pend) {
-        const int pos = qlen + __popc(m & ((1u << lane) - 1));
-        q.elem[pos] = (int32_t)i;
-        q.node[pos] = wd[k] & kParentMask;
-        q.steps[pos] = 0;
-      }
-      qlen += __popc(m);
-    }
+    for (int q = 0; q < kScanG; ++q) scan_group(Q, warp, lane, (g + q) * kGroup + lane, true, wd[q], bw[q], qlen, c);
     __syncwarp();
-    // keep room for the next chunk
-    while (qlen > kQCap - kChunkSpan) qlen = queue_round(q, qlen, words, c, longest, overflow);
   }
-  while (qlen) qlen = queue_round(q, qlen, words, c, longest, overflow);
+  // tail groups
+  for (; g < g1; ++g) {
+    if (qlen > kQ - 32) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
+    const uint32_t x = g * kGroup + lane;
+    const bool in = x < nn;
+    const uint32_t wd = in ? __ldcs(words + x) : 0u;
+    scan_group(Q, warp, lane, x, in, wd, __ldg(bitmap + g), qlen, c);
+    __syncwarp();
+  }
+  while (qlen) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
   if (overflow) {
     atomicOr(&state->flags, kOverflow);
     status_or(status, PFR_ST_OVERFLOW);
@@ -619,7 +715,8 @@ __device__ void resolve_all(const uint32_t* __restrict__ words, const uint32_t* 
 // rare paths (cooperative): repair of non-monotone O, pointer jumping
 template <typename T, typename A, int UM>
 __global__ void __launch_bounds__(kTileThreads) k_dv_rare(DvArgs<A> p) {
-  __shared__ __align__(16) uint4 stage[2 * kTile * 4 / 16];
+  __shared__ __align__(16) uint4 stage[kSlotCap * 4 / 16];
+  __shared__ uint32_t heads[kTileThreads];
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ int64_t imax8[kTileThreads / 32];
   __shared__ int32_t warp_last[kTileThreads / 32];
@@ -677,7 +774,7 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_rare(DvArgs<A> p) {
       }
       const int32_t o_prev = b ? (int32_t)max(before_tiles, (int64_t)0) : 0;
       if (p.O_out) tile_store<int32_t>(p.O_out, n, b * kTile, stage, o, policy_evict_last());
-      tile_expand(o, o_prev, b, n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), warp_last);
+      tile_expand(o, o_prev, b, n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), heads, warp_last);
     }
     grid.sync();
     // D: in-place indices
@@ -785,16 +882,18 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
   if (e != cudaSuccess || stages < 3) return e;
   static int occ3 = -1;
-  const size_t smem3 = sizeof(WarpQueue) * kInplaceWarps;
   if (occ3 < 0) {
-    e = cudaFuncSetAttribute(k_dv_inplace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_dv_inplace, 32 * kInplaceWarps, smem3);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_dv_inplace, kIpThreads, 0);
     if (e != cudaSuccess) return e;
     if (occ3 < 1) occ3 = 1;
   }
-  e = launch_pdl_smem(k_dv_inplace, dim3(num_sms() * occ3), dim3(32 * kInplaceWarps), smem3, s, false,
-                      (const uint32_t*)p.words, (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
+  {
+    const int64_t warps_needed = (p.n + 32 * 64 - 1) / (32 * 64);  // >= 64 groups per warp
+    const unsigned grid3 =
+        (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
+    e = launch_pdl(k_dv_inplace, dim3(grid3), dim3(kIpThreads), s, false, (const uint32_t*)p.words,
+                   (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
+  }
   if (e != cudaSuccess || stages < 4) return e;
   static int occ = -1;
   if (occ < 0) {
@@ -832,6 +931,7 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
   p.max_steps = max_steps;
   p.state = ws.dv;
   p.status = status;
+  p.fx_S = fx_bits(n);
   p.O = ws.O;
   p.tmax = reinterpret_cast<int64_t*>(ws.j1);  // tiles << n
   p.d = ws.O;  // O is dead once the words exist

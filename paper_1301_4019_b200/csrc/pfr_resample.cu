@@ -9,6 +9,7 @@
 // path (ld.global.nc).  Random draws come from a counter-based generator so
 // they are a pure function of (stream, slot, step): no state in memory.
 #include <cmath>
+#include <cstdlib>
 
 #include "pfr_internal.h"
 #include "pfr_tile.cuh"
@@ -211,9 +212,7 @@ constexpr int kRejChunk = 256;
 // The first accepting trip of the batch wins, so results, trip counts and the
 // stream mapping are exactly those of a one-trip-at-a-time loop; the few
 // trips evaluated past the acceptance are discarded.
-constexpr int kRejBatch = 4;  // trips per lane per iteration (even)
-
-template <typename T, bool kCapped>
+template <typename T, bool kCapped, int kRejBatch>
 __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
   const int lane = threadIdx.x & 31;
   const T bound = (T)A.bound;
@@ -491,21 +490,38 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0) != cudaSuccess || occ < 1) occ = 1;
     return num_sms() * occ;
   };
+  // trips evaluated per lane and iteration (PFR_REJ_BATCH: profiling aid)
+  static const int batch = [] {
+    const char* v = getenv("PFR_REJ_BATCH");
+    return v && atoi(v) == 8 ? 8 : (v && atoi(v) == 2 ? 2 : 4);
+  }();
+#define PFR_REJ_LAUNCH(T, CAP, B) k_rejection_philox<T, CAP, B><<<blocks_for(k_rejection_philox<T, CAP, B>), 256, 0, s>>>(A)
+#define PFR_REJ_DISPATCH(T, CAP)     \
+  do {                               \
+    if (batch == 8)                  \
+      PFR_REJ_LAUNCH(T, CAP, 8);     \
+    else if (batch == 2)             \
+      PFR_REJ_LAUNCH(T, CAP, 2);     \
+    else                             \
+      PFR_REJ_LAUNCH(T, CAP, 4);     \
+  } while (0)
   if (dtype == PFR_F64) {
     RejArgs<double> A{(const double*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
                       a, trips, (double*)out_w, next, status};
     if (cap > 0)
-      k_rejection_philox<double, true><<<blocks_for(k_rejection_philox<double, true>), 256, 0, s>>>(A);
+      PFR_REJ_DISPATCH(double, true);
     else
-      k_rejection_philox<double, false><<<blocks_for(k_rejection_philox<double, false>), 256, 0, s>>>(A);
+      PFR_REJ_DISPATCH(double, false);
   } else {
     RejArgs<float> A{(const float*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
                      a, trips, (float*)out_w, next, status};
     if (cap > 0)
-      k_rejection_philox<float, true><<<blocks_for(k_rejection_philox<float, true>), 256, 0, s>>>(A);
+      PFR_REJ_DISPATCH(float, true);
     else
-      k_rejection_philox<float, false><<<blocks_for(k_rejection_philox<float, false>), 256, 0, s>>>(A);
+      PFR_REJ_DISPATCH(float, false);
   }
+#undef PFR_REJ_DISPATCH
+#undef PFR_REJ_LAUNCH
   note_launch();
   return cudaGetLastError();
 }

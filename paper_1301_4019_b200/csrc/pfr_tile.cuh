@@ -74,6 +74,7 @@ struct MaxOp {
   __device__ static double combine(double a, double b) { return fmax(a, b); }
   __device__ static float combine(float a, float b) { return fmaxf(a, b); }
   __device__ static int64_t combine(int64_t a, int64_t b) { return a > b ? a : b; }
+  __device__ static int combine(int a, int b) { return a > b ? a : b; }
 };
 
 // Publish leaf (0, b) = v and complete every node whose rightmost leaf is b.
