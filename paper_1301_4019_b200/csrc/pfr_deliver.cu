@@ -56,7 +56,8 @@ struct DvArgs {
   int64_t n;
   int64_t tiles;
   A* agg;        // [tiles]
-  A* excl;       // [tiles + 1]; excl[tiles] = total
+  A* excl;       // see K1: in-group tile prefixes, total, group prefixes, tile flags
+  A* sum_scratch;  // [groups] group totals
   A u_sys;       // systematic offset (cast to the weight dtype)
   const double* uniforms;
   Key2x64 key;
@@ -247,27 +248,65 @@ __device__ __forceinline__ void tile_load_direct(const T* __restrict__ in, int64
 }
 
 // ---------------------------------------------------------------------------
-// K1: validation + tile aggregates; the last CTA scans them.  Per-tile flags
-// go to a plain array (no same-address atomics from thousands of CTAs); the
-// last CTA ORs them into the caller's status word once.
+// K1: one CTA per 4096-element tile: validation flags and the tile aggregate.
+// Tile prefixes are built hierarchically so no single CTA serialises the
+// tail: the last tile to finish in each group of 64 tiles scans the group's
+// aggregates (one warp), and the last group to finish scans the group totals.
+// Every floating-point association is fixed by tile and group indices alone
+// (deterministic, schedule independent).  Layout in p.excl:
+//   [0, tiles)            exclusive prefix of the tile inside its group
+//   [tiles]               the total W_N
+//   [tiles+1, +groups+1)  exclusive prefix of the group totals
+// followed by per-tile validation flags (uint32).
+constexpr int kGroupTiles = 64;
+
+template <typename A>
+__device__ __forceinline__ int64_t num_groups(const DvArgs<A>& p) {
+  return (p.tiles + kGroupTiles - 1) / kGroupTiles;
+}
+template <typename A>
+__device__ __forceinline__ A* group_prefix(const DvArgs<A>& p) {
+  return p.excl + p.tiles + 1;
+}
 template <typename A>
 __device__ __forceinline__ uint32_t* tile_flags(const DvArgs<A>& p) {
-  return reinterpret_cast<uint32_t*>(p.excl + p.tiles + 2);
+  return reinterpret_cast<uint32_t*>(p.excl + p.tiles + 2 + num_groups(p));
+}
+// exclusive prefix of tile b (the association K2 and the repair path use)
+template <typename A>
+__device__ __forceinline__ A tile_excl(const DvArgs<A>& p, int64_t b) {
+  return add_rn(__ldcg(group_prefix(p) + b / kGroupTiles), __ldcg(p.excl + b));
+}
+
+// exclusive scan of v[0..cnt) (cnt <= 64) by one warp: lane l holds v[2l],
+// v[2l+1]; pair sums, Kogge-Stone across lanes.  Writes out[k] and returns
+// the total in every lane.
+template <typename A>
+__device__ __forceinline__ A warp_excl64(const A* v, int cnt, A* out) {
+  const int lane = threadIdx.x & 31;
+  const A a0 = 2 * lane < cnt ? __ldcg(v + 2 * lane) : A(0);
+  const A a1 = 2 * lane + 1 < cnt ? __ldcg(v + 2 * lane + 1) : A(0);
+  const A pr = add_rn(a0, a1);
+  const A incl = warp_inclusive_scan(pr);
+  A ex = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) ex = A(0);
+  if (2 * lane < cnt) out[2 * lane] = ex;
+  if (2 * lane + 1 < cnt) out[2 * lane + 1] = add_rn(ex, a0);
+  return __shfl_sync(0xffffffffu, incl, 31);
 }
 
 template <typename T, typename A>
 __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
-  __shared__ __align__(16) uint4 stage[kTile * sizeof(T) / 16];
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ uint32_t cta_flags;
-  __shared__ bool is_last;
-  // persistent: CTA-strided tiles, one fence + one counter bump per CTA
+  __shared__ int stage_flag;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = blockIdx.x;
   if (threadIdx.x == 0) cta_flags = 0;
-  FlagAcc<T> facc;
-  for (int64_t b = blockIdx.x; b < p.tiles; b += gridDim.x) {
-    const int64_t base = b * kTile;
+  {
     T x[kTileItems];
-    tile_load_direct<T>((const T*)p.w, p.n, base, x);
+    tile_load_direct<T>((const T*)p.w, p.n, b * kTile, x);
+    FlagAcc<T> facc;
     TileScan<A> s;
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) {
@@ -277,71 +316,62 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
     tile_scan<A>(s, warp_sums);
     // aggregate := tile-local inclusive value at the tile's last position
     if (threadIdx.x == kTileThreads - 1) p.agg[b] = add_rn(s.thread_excl, s.loc[kTileItems - 1]);
+    const uint32_t flags = __reduce_or_sync(0xffffffffu, facc.flags());
+    if (lane == 0 && flags) atomicOr(&cta_flags, flags);
   }
-  const uint32_t flags = __reduce_or_sync(0xffffffffu, facc.flags());
-  if ((threadIdx.x & 31) == 0 && flags) atomicOr(&cta_flags, flags);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    tile_flags(p)[blockIdx.x] = cta_flags;
+  const int64_t g = b / kGroupTiles;
+  const int64_t G = num_groups(p);
+  if (threadIdx.x == kTileThreads - 1) {
+    tile_flags(p)[b] = cta_flags;
     __threadfence();
-    const unsigned t = atomicAdd(&p.state->done, 1u);
-    is_last = (t == gridDim.x - 1);
+    const int64_t gsize = min((int64_t)kGroupTiles, p.tiles - g * kGroupTiles);
+    const unsigned t = atomicAdd(&p.state->gcnt[g], 1u);
+    stage_flag = (t == (unsigned)gsize - 1) ? 1 : 0;
   }
   __syncthreads();
-  if (!is_last) return;
-  if (threadIdx.x == 0) cta_flags = 0;
-  __threadfence();
-  // exclusive scan over the tile aggregates, 4096 at a time through shared
-  // memory (coalesced loads): serial within a thread's 16, Kogge-Stone across
-  // threads, serial across warps, serial carry across chunks (fixed
-  // association => deterministic)
-  A* sagg = reinterpret_cast<A*>(stage);  // >= 4096 * 4 bytes; A=double needs 32 KB -> 2 passes of 2048
-  constexpr int kChunk = (kTile * sizeof(T)) / sizeof(A);
-  constexpr int kPer = kChunk / kTileThreads;
-  const int T_ = (int)p.tiles;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  A carry = A(0);
-  uint32_t fl = 0;
-  for (int c0 = 0; c0 < T_; c0 += kChunk) {
-    const int cn = min(kChunk, T_ - c0);
-    for (int i = threadIdx.x; i < cn; i += kTileThreads) sagg[i] = __ldcg(p.agg + c0 + i);
-    __syncthreads();
-    A v[kPer];
-    A mine = A(0);
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int i = threadIdx.x * kPer + k;
-      v[k] = i < cn ? sagg[i] : A(0);
-      mine = add_rn(mine, v[k]);
+  if (!stage_flag) return;
+  // last tile of group g: scan the group's aggregates
+  if (warp == 0) {
+    __threadfence();
+    const int64_t t0 = g * kGroupTiles;
+    const int cnt = (int)min((int64_t)kGroupTiles, p.tiles - t0);
+    const A gt = warp_excl64(p.agg + t0, cnt, p.excl + t0);
+    if (lane == 0) {
+      p.sum_scratch[g] = gt;
+      p.state->gcnt[g] = 0;
+      __threadfence();
+      const unsigned t = atomicAdd(&p.state->done, 1u);
+      stage_flag = (t == (unsigned)G - 1) ? 2 : 0;
     }
-    const A incl = warp_inclusive_scan(mine);
-    A ex = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane == 0) ex = A(0);
-    if (lane == 31) warp_sums[warp] = incl;
-    __syncthreads();
-    A wp = carry, tot = carry;
-    for (int u = 0; u < kTileThreads / 32; ++u) {
-      if (u < warp) wp = add_rn(wp, warp_sums[u]);
-      tot = add_rn(tot, warp_sums[u]);
-    }
-    A run = lane ? add_rn(wp, ex) : wp;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int i = threadIdx.x * kPer + k;
-      if (i < cn) sagg[i] = run;
-      run = add_rn(run, v[k]);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < cn; i += kTileThreads) p.excl[c0 + i] = sagg[i];
-    carry = tot;
-    __syncthreads();
   }
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += kTileThreads) fl |= __ldcg(tile_flags(p) + i);
+  __syncthreads();
+  if (stage_flag != 2) return;
+  // last group: exclusive scan of the group totals (64 per warp-pass, serial
+  // carry across passes), the total, the validation flags
+  __threadfence();
+  if (warp == 0) {
+    A carry = A(0);
+    for (int64_t g0 = 0; g0 < G; g0 += 64) {
+      const int cnt = (int)min((int64_t)64, G - g0);
+      A* out = group_prefix(p) + g0;
+      const A tot = warp_excl64(p.sum_scratch + g0, cnt, out);
+      __syncwarp();
+      if (g0) {  // shift by the carry of the previous passes
+        if (2 * lane < cnt) out[2 * lane] = add_rn(carry, out[2 * lane]);
+        if (2 * lane + 1 < cnt) out[2 * lane + 1] = add_rn(carry, out[2 * lane + 1]);
+      }
+      carry = g0 ? add_rn(carry, tot) : tot;
+      __syncwarp();
+    }
+    if (lane == 0) p.excl[p.tiles] = carry;  // the total
+  }
+  uint32_t fl = 0;
+  for (int64_t i = threadIdx.x; i < p.tiles; i += kTileThreads) fl |= __ldcg(tile_flags(p) + i);
   fl = __reduce_or_sync(0xffffffffu, fl);
   if (lane == 0 && fl) atomicOr(&cta_flags, fl);
   __syncthreads();
   if (threadIdx.x == 0) {
-    p.excl[T_] = carry;  // the total
     p.state->done = 0;
     p.state->flags = 0;
     status_or(p.status, cta_flags);
@@ -361,9 +391,9 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
   tile_scan<A>(s, warp_sums);
-  const A total = p.excl[p.tiles];
+  const A total = __ldcg(p.excl + p.tiles);
   const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
-  const A ex = p.excl[b];
+  const A ex = tile_excl(p, b);
   const A tex = s.thread_excl;
   const int last = (p.n - 1 - base < kTile) ? (int)(p.n - 1 - base) : -1;
   const int e0 = threadIdx.x * kTileItems;
@@ -375,7 +405,7 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
   }
   o_prev = 0;
   if (b > 0) {
-    const A Wp = add_rn(p.excl[b - 1], p.agg[b - 1]);  // W at the last position of tile b-1
+    const A Wp = add_rn(tile_excl(p, b - 1), __ldcg(p.agg + b - 1));  // W at the last position of tile b-1
     o_prev = offspring_of<T, A, UM>(Wp, total, fx, p.n, p);
   }
 }
@@ -874,7 +904,8 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_dv_reduce<T, A>, kTileThreads, 0);
     if (occ1 < 1) occ1 = 1;
   }
-  const unsigned grid1 = (unsigned)min((int64_t)num_sms() * occ1, p.tiles);
+  const unsigned grid1 = (unsigned)p.tiles;
+  (void)occ1;
   k_dv_reduce<T, A><<<grid1, kTileThreads, 0, s>>>(p);
   note_launch();
   cudaError_t e = cudaGetLastError();
@@ -888,7 +919,9 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
     if (occ3 < 1) occ3 = 1;
   }
   {
-    const int64_t warps_needed = (p.n + 32 * 64 - 1) / (32 * 64);  // >= 64 groups per warp
+    // >= 8 groups per warp: small problems spread over many warps (the chain
+    // walks are latency bound), large ones fill the machine once (persistent)
+    const int64_t warps_needed = (p.n + 32 * 8 - 1) / (32 * 8);
     const unsigned grid3 =
         (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
     e = launch_pdl(k_dv_inplace, dim3(grid3), dim3(kIpThreads), s, false, (const uint32_t*)p.words,
@@ -901,7 +934,10 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
   }
-  return launch_pdl(k_dv_rare<T, A, UM>, dim3(num_sms() * occ), dim3(kTileThreads), s, true, p);
+  // one CTA per SM: the grid only has to be co-resident (grid.sync), and in
+  // the common case every CTA returns at once, so a small grid launches fastest
+  (void)occ;
+  return launch_pdl(k_dv_rare<T, A, UM>, dim3(num_sms()), dim3(kTileThreads), s, true, p);
 }
 
 template <typename T, typename A>
@@ -920,6 +956,7 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
   p.n = n;
   p.tiles = num_tiles(n);
   p.agg = reinterpret_cast<A*>(ws.sum_cells);
+  p.sum_scratch = p.agg + p.tiles + 8;  // the sum tree region holds >= 2 * tiles cells
   p.excl = reinterpret_cast<A*>(ws.max_cells);
   p.u_sys = (A)(T)offset;
   p.uniforms = uniforms;

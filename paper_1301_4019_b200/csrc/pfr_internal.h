@@ -23,9 +23,10 @@ struct WsHeader {
 // state of the fused delivery pipeline: zero at workspace allocation, kept
 // consistent by the kernels themselves (never memset per call)
 struct DvState {
-  unsigned int done;   // K1 CTAs finished (the last one resets it)
+  unsigned int done;   // K1 groups finished (the last one resets it)
   unsigned int flags;  // 1 = O needs the running-max repair, 2 = chain overflow
   unsigned int pad[62];
+  unsigned int gcnt[8192];  // K1 tiles finished per group of 64 tiles (self-resetting)
 };
 
 struct Workspace {

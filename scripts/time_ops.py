@@ -31,6 +31,7 @@ c = torch.empty(n, dtype=torch.int32, device="cuda")
 ts = []
 for r in range(13):
     flush.zero_()
+    torch.cuda._sleep(400_000)  # ~200 us: the host enqueues the work while the GPU spins
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()

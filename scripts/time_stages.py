@@ -20,6 +20,7 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ts = []
 for r in range(15):
     flush.zero_()
+    torch.cuda._sleep(400_000)  # ~200 us: the host enqueues the work while the GPU spins
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(); pf.deliver(w, pf.ResamplerConfig("systematic"), pf.RngStream(r), index_dtype=torch.int32, out=c); e1.record()
     torch.cuda.synchronize()
