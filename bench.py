@@ -7,7 +7,10 @@ step = the ten deliveries (resample + permute to an in-place-valid ancestry,
 the timed region of the reference's bench.py:155-161), i.e. 10 * 2^20
 particles.  Weights are resident in HBM before timing; L2 is flushed
 (256 MiB write) before every delivery and every delivery is timed with CUDA
-events on the launching stream; the flush is outside the timed region.
+events on the launching stream; the flush is outside the timed region, and a
+short GPU spin between the flush and the start event lets the host enqueue
+the delivery so that the events see device work only (the host-side cost of
+the API is what `e2e` measures).
 
 Also reported (north-star targets): systematic delivery
 and Metropolis(B=32) at N = 2^24 float32 against the measured HBM roofline.
@@ -44,6 +47,7 @@ METRIC = "particles resampled/sec vs N per resampler (1/2/4/8 B200); % HBM roofl
 N_DEFAULT = 1 << 20
 B_STEPS = 32
 SIGMA = 1.0
+PREROLL_CYCLES = 400_000  # ~0.2 ms GPU spin before each timed delivery (outside the events)
 
 
 def peaks():
@@ -282,6 +286,9 @@ def main():
         for i, alg in enumerate(ALGS):
             for j, dt in enumerate(DTYPES):
                 flush.zero_()
+                # the GPU spins while the host enqueues the delivery, so the
+                # events time device work only (host cost is in `e2e`)
+                torch.cuda._sleep(PREROLL_CYCLES)
                 s0 = torch.cuda.Event(enable_timing=True)
                 s1 = torch.cuda.Event(enable_timing=True)
                 s0.record(stream)
@@ -435,6 +442,7 @@ def north_star_targets(pf, torch, dev, stream, flush, hbm, reps=10):
         ts = []
         for r in range(reps + 3):
             flush.zero_()
+            torch.cuda._sleep(PREROLL_CYCLES)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)

@@ -54,7 +54,6 @@ size_t op_bytes(int op, int64_t n) {
   const Layout L = layout(n);
   switch (op) {
     case PFR_OP_SCAN:
-    case PFR_OP_OFFSPRING:
     case PFR_OP_METROPOLIS:
     case PFR_OP_REJECTION:
     case PFR_OP_EXPAND:

@@ -29,6 +29,44 @@ __device__ __forceinline__ void status_or_warp(uint32_t* status, uint32_t bits) 
   if ((threadIdx.x & 31) == (__ffs(m) - 1)) status_or(status, agg);
 }
 
+// check_weights (diagnostics.py:38-51) on bit patterns: three integer maxima
+// per element instead of float classification.  Non-finite <=> magnitude
+// bits >= the infinity pattern; some x < 0 <=> unsigned max > the -0.0
+// pattern; some x > 0 <=> signed max > 0.  Zero padding is neutral.
+template <typename T>
+struct FlagAcc;
+template <>
+struct FlagAcc<float> {
+  uint32_t mag = 0u, ub = 0u;
+  int32_t sb = INT32_MIN;
+  __device__ __forceinline__ void add(float x) {
+    const uint32_t b = __float_as_uint(x);
+    mag = max(mag, b & 0x7FFFFFFFu);
+    ub = max(ub, b);
+    sb = max(sb, (int32_t)b);
+  }
+  __device__ __forceinline__ uint32_t flags() const {
+    return (mag >= 0x7F800000u ? PFR_ST_NONFINITE : 0u) | (ub > 0x80000000u ? PFR_ST_NEGATIVE : 0u) |
+           (sb > 0 ? PFR_ST_POSITIVE : 0u);
+  }
+};
+template <>
+struct FlagAcc<double> {
+  uint64_t mag = 0u, ub = 0u;
+  int64_t sb = INT64_MIN;
+  __device__ __forceinline__ void add(double x) {
+    const uint64_t b = (uint64_t)__double_as_longlong(x);
+    const uint64_t m = b & 0x7FFFFFFFFFFFFFFFull;
+    mag = m > mag ? m : mag;
+    ub = b > ub ? b : ub;
+    sb = (int64_t)b > sb ? (int64_t)b : sb;
+  }
+  __device__ __forceinline__ uint32_t flags() const {
+    return (mag >= 0x7FF0000000000000ull ? PFR_ST_NONFINITE : 0u) |
+           (ub > 0x8000000000000000ull ? PFR_ST_NEGATIVE : 0u) | (sb > 0 ? PFR_ST_POSITIVE : 0u);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // L2 cache policies (createpolicy) and hinted loads/stores
 

@@ -31,6 +31,7 @@
 
 #include <cstdlib>
 
+#include "pfr_hier.cuh"
 #include "pfr_internal.h"
 #include "pfr_tile.cuh"
 
@@ -69,48 +70,11 @@ struct DvArgs {
   DvState* state;
   uint32_t* status;
   int fx_S;          // fixed-point fraction bits of the offspring fast path
+  int expand;        // 1: full delivery; 0: cumulative offspring O_out only
   // rare-path scratch
   int32_t* O;        // [n]
   int64_t* tmax;     // [tiles]
   int32_t *d, *J0, *J1, *R0, *R1;
-};
-
-// check_weights (diagnostics.py:38-51) on bit patterns: three integer maxima
-// per element instead of float classification.  Non-finite <=> magnitude
-// bits >= the infinity pattern; some x < 0 <=> unsigned max > the -0.0
-// pattern; some x > 0 <=> signed max > 0.  Zero padding is neutral.
-template <typename T>
-struct FlagAcc;
-template <>
-struct FlagAcc<float> {
-  uint32_t mag = 0u, ub = 0u;
-  int32_t sb = INT32_MIN;
-  __device__ __forceinline__ void add(float x) {
-    const uint32_t b = __float_as_uint(x);
-    mag = max(mag, b & 0x7FFFFFFFu);
-    ub = max(ub, b);
-    sb = max(sb, (int32_t)b);
-  }
-  __device__ __forceinline__ uint32_t flags() const {
-    return (mag >= 0x7F800000u ? PFR_ST_NONFINITE : 0u) | (ub > 0x80000000u ? PFR_ST_NEGATIVE : 0u) |
-           (sb > 0 ? PFR_ST_POSITIVE : 0u);
-  }
-};
-template <>
-struct FlagAcc<double> {
-  uint64_t mag = 0u, ub = 0u;
-  int64_t sb = INT64_MIN;
-  __device__ __forceinline__ void add(double x) {
-    const uint64_t b = (uint64_t)__double_as_longlong(x);
-    const uint64_t m = b & 0x7FFFFFFFFFFFFFFFull;
-    mag = m > mag ? m : mag;
-    ub = b > ub ? b : ub;
-    sb = (int64_t)b > sb ? (int64_t)b : sb;
-  }
-  __device__ __forceinline__ uint32_t flags() const {
-    return (mag >= 0x7FF0000000000000ull ? PFR_ST_NONFINITE : 0u) |
-           (ub > 0x8000000000000000ull ? PFR_ST_NEGATIVE : 0u) | (sb > 0 ? PFR_ST_POSITIVE : 0u);
-  }
 };
 
 // ---------------------------------------------------------------------------
@@ -220,92 +184,29 @@ __device__ __forceinline__ int32_t offspring_of(A W, A total, const FxParams& f,
   return offspring_exact<T, A, UM>(W, total, n, p);
 }
 
-// blocked direct loads: thread t gets elements [16t, 16t + 16) of the tile
-// (L1-allocating 16-byte loads; the 4-8 loads of a thread hit the same lines)
-template <typename T>
-__device__ __forceinline__ void tile_load_direct(const T* __restrict__ in, int64_t n, int64_t base,
-                                                 T (&x)[kTileItems]) {
-  constexpr int kPerVec = 16 / sizeof(T);
-  const int64_t e0 = base + (int64_t)threadIdx.x * kTileItems;
-  if (e0 + kTileItems <= n) {
-    uint4 v[kTileItems / kPerVec];
-#pragma unroll
-    for (int q = 0; q < kTileItems / kPerVec; ++q) v[q] = __ldg(reinterpret_cast<const uint4*>(in + e0) + q);
-#pragma unroll
-    for (int q = 0; q < kTileItems / kPerVec; ++q) {
-      union {
-        uint4 u;
-        T e[kPerVec];
-      } tmp;
-      tmp.u = v[q];
-#pragma unroll
-      for (int e = 0; e < kPerVec; ++e) x[q * kPerVec + e] = tmp.e[e];
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kTileItems; ++j) x[j] = (e0 + j < n) ? in[e0 + j] : T(0);
-  }
-}
-
 // ---------------------------------------------------------------------------
-// K1: one CTA per 4096-element tile: validation flags and the tile aggregate.
-// Tile prefixes are built hierarchically so no single CTA serialises the
-// tail: the last tile to finish in each group of 64 tiles scans the group's
-// aggregates (one warp), and the last group to finish scans the group totals.
-// Every floating-point association is fixed by tile and group indices alone
-// (deterministic, schedule independent).  Layout in p.excl:
-//   [0, tiles)            exclusive prefix of the tile inside its group
-//   [tiles]               the total W_N
-//   [tiles+1, +groups+1)  exclusive prefix of the group totals
-// followed by per-tile validation flags (uint32).
-constexpr int kGroupTiles = 64;
-
+// K1: one CTA per 4096-element tile: validation flags and the tile aggregate
+// (the tile-local inclusive value at its last position, in exactly the
+// association K2 uses); tile prefixes built hierarchically (pfr_hier.cuh).
 template <typename A>
-__device__ __forceinline__ int64_t num_groups(const DvArgs<A>& p) {
-  return (p.tiles + kGroupTiles - 1) / kGroupTiles;
+__device__ __forceinline__ Hier<A> hier_of(const DvArgs<A>& p) {
+  return Hier<A>{p.agg, p.excl, p.sum_scratch, p.state, p.tiles};
 }
-template <typename A>
-__device__ __forceinline__ A* group_prefix(const DvArgs<A>& p) {
-  return p.excl + p.tiles + 1;
-}
-template <typename A>
-__device__ __forceinline__ uint32_t* tile_flags(const DvArgs<A>& p) {
-  return reinterpret_cast<uint32_t*>(p.excl + p.tiles + 2 + num_groups(p));
-}
-// exclusive prefix of tile b (the association K2 and the repair path use)
 template <typename A>
 __device__ __forceinline__ A tile_excl(const DvArgs<A>& p, int64_t b) {
-  return add_rn(__ldcg(group_prefix(p) + b / kGroupTiles), __ldcg(p.excl + b));
-}
-
-// exclusive scan of v[0..cnt) (cnt <= 64) by one warp: lane l holds v[2l],
-// v[2l+1]; pair sums, Kogge-Stone across lanes.  Writes out[k] and returns
-// the total in every lane.
-template <typename A>
-__device__ __forceinline__ A warp_excl64(const A* v, int cnt, A* out) {
-  const int lane = threadIdx.x & 31;
-  const A a0 = 2 * lane < cnt ? __ldcg(v + 2 * lane) : A(0);
-  const A a1 = 2 * lane + 1 < cnt ? __ldcg(v + 2 * lane + 1) : A(0);
-  const A pr = add_rn(a0, a1);
-  const A incl = warp_inclusive_scan(pr);
-  A ex = __shfl_up_sync(0xffffffffu, incl, 1);
-  if (lane == 0) ex = A(0);
-  if (2 * lane < cnt) out[2 * lane] = ex;
-  if (2 * lane + 1 < cnt) out[2 * lane + 1] = add_rn(ex, a0);
-  return __shfl_sync(0xffffffffu, incl, 31);
+  return hier_of(p).tile_excl(b);
 }
 
 template <typename T, typename A>
 __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ uint32_t cta_flags;
-  __shared__ int stage_flag;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int stage;
   const int64_t b = blockIdx.x;
   if (threadIdx.x == 0) cta_flags = 0;
   {
     T x[kTileItems];
-    tile_load_direct<T>((const T*)p.w, p.n, b * kTile, x);
+    tile_load_any<T>((const T*)p.w, p.n, b * kTile, x);
     FlagAcc<T> facc;
     TileScan<A> s;
 #pragma unroll
@@ -314,68 +215,12 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
       s.loc[j] = (A)x[j];
     }
     tile_scan<A>(s, warp_sums);
-    // aggregate := tile-local inclusive value at the tile's last position
     if (threadIdx.x == kTileThreads - 1) p.agg[b] = add_rn(s.thread_excl, s.loc[kTileItems - 1]);
     const uint32_t flags = __reduce_or_sync(0xffffffffu, facc.flags());
-    if (lane == 0 && flags) atomicOr(&cta_flags, flags);
+    if ((threadIdx.x & 31) == 0 && flags) atomicOr(&cta_flags, flags);
   }
-  __syncthreads();
-  const int64_t g = b / kGroupTiles;
-  const int64_t G = num_groups(p);
-  if (threadIdx.x == kTileThreads - 1) {
-    tile_flags(p)[b] = cta_flags;
-    __threadfence();
-    const int64_t gsize = min((int64_t)kGroupTiles, p.tiles - g * kGroupTiles);
-    const unsigned t = atomicAdd(&p.state->gcnt[g], 1u);
-    stage_flag = (t == (unsigned)gsize - 1) ? 1 : 0;
-  }
-  __syncthreads();
-  if (!stage_flag) return;
-  // last tile of group g: scan the group's aggregates
-  if (warp == 0) {
-    __threadfence();
-    const int64_t t0 = g * kGroupTiles;
-    const int cnt = (int)min((int64_t)kGroupTiles, p.tiles - t0);
-    const A gt = warp_excl64(p.agg + t0, cnt, p.excl + t0);
-    if (lane == 0) {
-      p.sum_scratch[g] = gt;
-      p.state->gcnt[g] = 0;
-      __threadfence();
-      const unsigned t = atomicAdd(&p.state->done, 1u);
-      stage_flag = (t == (unsigned)G - 1) ? 2 : 0;
-    }
-  }
-  __syncthreads();
-  if (stage_flag != 2) return;
-  // last group: exclusive scan of the group totals (64 per warp-pass, serial
-  // carry across passes), the total, the validation flags
-  __threadfence();
-  if (warp == 0) {
-    A carry = A(0);
-    for (int64_t g0 = 0; g0 < G; g0 += 64) {
-      const int cnt = (int)min((int64_t)64, G - g0);
-      A* out = group_prefix(p) + g0;
-      const A tot = warp_excl64(p.sum_scratch + g0, cnt, out);
-      __syncwarp();
-      if (g0) {  // shift by the carry of the previous passes
-        if (2 * lane < cnt) out[2 * lane] = add_rn(carry, out[2 * lane]);
-        if (2 * lane + 1 < cnt) out[2 * lane + 1] = add_rn(carry, out[2 * lane + 1]);
-      }
-      carry = g0 ? add_rn(carry, tot) : tot;
-      __syncwarp();
-    }
-    if (lane == 0) p.excl[p.tiles] = carry;  // the total
-  }
-  uint32_t fl = 0;
-  for (int64_t i = threadIdx.x; i < p.tiles; i += kTileThreads) fl |= __ldcg(tile_flags(p) + i);
-  fl = __reduce_or_sync(0xffffffffu, fl);
-  if (lane == 0 && fl) atomicOr(&cta_flags, fl);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    p.state->done = 0;
-    p.state->flags = 0;
-    status_or(p.status, cta_flags);
-  }
+  hier_tile_done(hier_of(p), b, &cta_flags, &stage, p.status);
+  if (stage == 2 && threadIdx.x == 0) p.state->flags = 0;  // pipeline flags of this delivery
 }
 
 // ---------------------------------------------------------------------------
@@ -386,12 +231,12 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
                                                int32_t (&o)[kTileItems], int32_t& o_prev) {
   const int64_t base = b * kTile;
   T x[kTileItems];
-  tile_load_direct<T>((const T*)p.w, p.n, base, x);
+  tile_load_any<T>((const T*)p.w, p.n, base, x);
   TileScan<A> s;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
   tile_scan<A>(s, warp_sums);
-  const A total = __ldcg(p.excl + p.tiles);
+  const A total = hier_of(p).total();
   const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
   const A ex = tile_excl(p, b);
   const A tex = s.thread_excl;
@@ -573,7 +418,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_dv_expand(DvArgs<A> p) {
     if (threadIdx.x == 0) atomicOr(&p.state->flags, kNeedsRepair);
     return;  // the rare-path kernel recomputes everything
   }
-  tile_expand(o, o_prev, b, p.n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), heads, warp_last);
+  if (p.expand) tile_expand(o, o_prev, b, p.n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), heads, warp_last);
 }
 
 // ---------------------------------------------------------------------------
@@ -804,9 +649,11 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_rare(DvArgs<A> p) {
       }
       const int32_t o_prev = b ? (int32_t)max(before_tiles, (int64_t)0) : 0;
       if (p.O_out) tile_store<int32_t>(p.O_out, n, b * kTile, stage, o, policy_evict_last());
-      tile_expand(o, o_prev, b, n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), heads, warp_last);
+      if (p.expand)
+        tile_expand(o, o_prev, b, n, p.words, p.bitmap, reinterpret_cast<uint32_t*>(stage), heads, warp_last);
     }
     grid.sync();
+    if (!p.expand) return;  // cumulative offspring only: done
     // D: in-place indices
     bool overflow = false;
     int longest = 0;
@@ -912,13 +759,13 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   if (e != cudaSuccess || stages < 2) return e;
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
   if (e != cudaSuccess || stages < 3) return e;
-  static int occ3 = -1;
-  if (occ3 < 0) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_dv_inplace, kIpThreads, 0);
-    if (e != cudaSuccess) return e;
-    if (occ3 < 1) occ3 = 1;
-  }
-  {
+  if (p.expand) {
+    static int occ3 = -1;
+    if (occ3 < 0) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_dv_inplace, kIpThreads, 0);
+      if (e != cudaSuccess) return e;
+      if (occ3 < 1) occ3 = 1;
+    }
     // >= 8 groups per warp: small problems spread over many warps (the chain
     // walks are latency bound), large ones fill the machine once (persistent)
     const int64_t warps_needed = (p.n + 32 * 8 - 1) / (32 * 8);
@@ -926,8 +773,8 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
         (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
     e = launch_pdl(k_dv_inplace, dim3(grid3), dim3(kIpThreads), s, false, (const uint32_t*)p.words,
                    (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
+    if (e != cudaSuccess || stages < 4) return e;
   }
-  if (e != cudaSuccess || stages < 4) return e;
   static int occ = -1;
   if (occ < 0) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dv_rare<T, A, UM>, kTileThreads, 0);
@@ -969,6 +816,7 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
   p.state = ws.dv;
   p.status = status;
   p.fx_S = fx_bits(n);
+  p.expand = c != nullptr;
   p.O = ws.O;
   p.tmax = reinterpret_cast<int64_t*>(ws.j1);  // tiles << n
   p.d = ws.O;  // O is dead once the words exist
@@ -980,6 +828,14 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
 }
 
 }  // namespace
+
+// systematic_/stratified_cumulative_offspring (resamplers.py:105-153): the
+// delivery's K1 + K2 with O stored and no expansion (rare path repairs O)
+cudaError_t launch_offspring(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
+                             const double* uniforms, const pfr_rng* rng, int32_t* O, uint32_t* status,
+                             const Workspace& ws, cudaStream_t s) {
+  return launch_deliver(w, n, dtype, accum, stratified, offset, uniforms, rng, nullptr, O, nullptr, status, ws, s);
+}
 
 cudaError_t launch_deliver(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
                            const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,

@@ -8,6 +8,7 @@
 // slot runs its own chain / proposal loop reading w through the read-only
 // path (ld.global.nc).  Random draws come from a counter-based generator so
 // they are a pure function of (stream, slot, step): no state in memory.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -78,7 +79,8 @@ __global__ void __launch_bounds__(256) k_metropolis_philox(const T* __restrict__
       philox4x32_10(i, (uint32_t)(b >> 1), kTagMetropolis, 0, k0, k1, o);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        j[c][h] = bounded_u32(o[2 * h], nn, threshold, i, (uint32_t)(b + h), kTagMetropolis, k0, k1);
+        j[c][h] = threshold == 0 ? __umulhi(o[2 * h], nn)  // power-of-two N: Lemire never rejects
+                                 : bounded_u32(o[2 * h], nn, threshold, i, (uint32_t)(b + h), kTagMetropolis, k0, k1);
         if constexpr (sizeof(T) == 4)
           u[c][h] = u32_to_unit_f(o[2 * h + 1]);
         else
@@ -195,7 +197,7 @@ struct RejArgs {
   double bound;
   double cap;  // > 0: capped variant, v = min(w, cap), bound = cap
   uint32_t k0, k1, threshold;
-  int64_t max_trips;
+  uint32_t max_trips;
   int32_t* a;
   int32_t* trips;
   T* out_w;
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
   int64_t chunk_next = 0, chunk_end = 0;  // warp-uniform local queue
   bool exhausted = false;                 // warp-uniform: no chunks left
   int64_t slot = -1;
-  int64_t trip = 0;
+  uint32_t trip = 0;
   uint32_t flags = 0;
   int iter = 0;
   while (true) {
@@ -257,34 +259,32 @@ __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
 #pragma unroll
       for (int q = 0; q < kRejBatch / 2; ++q) {
         uint32_t o[4];
-        philox4x32_10((uint32_t)slot, (uint32_t)((trip >> 1) + q), kTagRejection, 0, A.k0, A.k1, o);
+        philox4x32_10((uint32_t)slot, (trip >> 1) + q, kTagRejection, 0, A.k0, A.k1, o);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int64_t t = trip + 2 * q + h;
-          j[2 * q + h] = t == 0 ? (uint32_t)slot
-                                : bounded_u32(o[2 * h], nn, A.threshold, (uint32_t)slot, (uint32_t)t, kTagRejection,
-                                              A.k0, A.k1);
+          // power-of-two N (threshold 0): Lemire never rejects
+          j[2 * q + h] = A.threshold == 0 ? __umulhi(o[2 * h], nn)
+                                          : bounded_u32(o[2 * h], nn, A.threshold, (uint32_t)slot,
+                                                        trip + 2 * q + h, kTagRejection, A.k0, A.k1);
           if constexpr (sizeof(T) == 4)
             uu[2 * q + h] = u32_to_unit_f(o[2 * h + 1]);
           else
             uu[2 * q + h] = u32_to_unit_d(o[2 * h + 1]);
         }
       }
+      if (trip == 0) j[0] = (uint32_t)slot;  // trip 0 proposes the slot itself (resamplers.py:291-294)
 #pragma unroll
       for (int q = 0; q < kRejBatch; ++q) wj[q] = ldg(A.w + j[q]);
       int done = -1;  // batch position of the first accepting trip
-      bool stuck = false;
 #pragma unroll
-      for (int q = 0; q < kRejBatch; ++q) {
-        if (done < 0 && !stuck) {
-          const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
-          // beta <= v[j] / bound  <=>  beta * bound <= v[j]
-          if (uu[q] * bound <= vj)
-            done = q;
-          else if (trip + q + 1 >= A.max_trips)
-            stuck = true;
-        }
+      for (int q = kRejBatch - 1; q >= 0; --q) {
+        const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
+        // beta <= v[j] / bound  <=>  beta * bound <= v[j]
+        if (uu[q] * bound <= vj) done = q;
       }
+      // round cap: the trips past max_trips do not exist
+      const bool near_cap = trip + (uint32_t)kRejBatch >= A.max_trips;
+      if (near_cap && (done < 0 || trip + (uint32_t)done + 1 > A.max_trips)) done = -2;
       if (done >= 0) {
         T wd = wj[0];
         uint32_t jd = j[0];
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
           A.out_w[slot] = (vd == T(0)) ? T(1) : div_rn_t(wd, vd);
         }
         slot = -1;
-      } else if (stuck) {
+      } else if (done == -2) {
         flags |= PFR_ST_NOPROGRESS;
         A.a[slot] = (int32_t)slot;
         if (A.trips) A.trips[slot] = (int32_t)A.max_trips;
@@ -483,7 +483,7 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
   cudaError_t e = cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
   if (e != cudaSuccess) return e;
   const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
-  const int64_t max_trips = max_rounds + 1;
+  const uint32_t max_trips = (uint32_t)std::min<int64_t>(max_rounds + 1, 0x7FFFFFFF);
   // persistent: one resident wave fills the machine, chunks hand out the slots
   auto blocks_for = [](auto kernel) {
     int occ = 0;

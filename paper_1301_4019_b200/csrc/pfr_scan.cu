@@ -14,25 +14,19 @@
 //   k_scan        -- single-pass inclusive/exclusive scan with the same tree.
 #include <cmath>
 
+#include <algorithm>
+
+#include <cooperative_groups.h>
+
+#include "pfr_hier.cuh"
 #include "pfr_internal.h"
 #include "pfr_tile.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace pfr {
 
 namespace {
-
-constexpr unsigned kTicketPass1 = 0;
-constexpr unsigned kTicketPass2 = 1;
-constexpr unsigned kTicketScan = 2;
-
-template <typename T>
-__device__ __forceinline__ uint32_t weight_flags(T x) {
-  uint32_t f = 0;
-  if (!isfinite((double)x)) f |= PFR_ST_NONFINITE;
-  if (x < T(0)) f |= PFR_ST_NEGATIVE;
-  if (x > T(0)) f |= PFR_ST_POSITIVE;
-  return f;
-}
 
 template <typename A>
 __device__ __forceinline__ A mul_rn(A a, A b);
@@ -44,223 +38,88 @@ template <>
 __device__ __forceinline__ float mul_rn(float a, float b) {
   return __fmul_rn(a, b);
 }
-template <typename A>
-__device__ __forceinline__ A div_rn(A a, A b);
-template <>
-__device__ __forceinline__ double div_rn(double a, double b) {
-  return __ddiv_rn(a, b);
-}
-template <>
-__device__ __forceinline__ float div_rn(float a, float b) {
-  return __fdiv_rn(a, b);
-}
 
-__device__ __forceinline__ int64_t floor_to_i64(double x) { return (int64_t)floor(x); }
-__device__ __forceinline__ int64_t floor_to_i64(float x) { return (int64_t)floorf(x); }
+constexpr unsigned kScanRepair = 0x10u;  // DvState.flags: the scan output needs the running-max repair
+
+__device__ __forceinline__ void griddep_wait_scan() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
-// pass 1: tile sums + validation + normaliser
-template <typename T, typename A>
-__global__ void __launch_bounds__(kTileThreads) k_tile_sums(const T* __restrict__ w, int64_t n, Tree tree,
-                                                             WsHeader* hdr, uint32_t* status) {
-  __shared__ __align__(16) uint4 stage[kTile * sizeof(T) / 16];
+// Two-pass scan (inclusive_prefix_sum / exclusive_prefix_sum / vector_sum,
+// primitives.py:34-66; offspring_to_cumulative, ancestry.py:85-88).
+// S1: one CTA per tile, tile aggregate in the in-tile association of S2,
+//     validation flags, hierarchical tile prefixes (pfr_hier.cuh).
+// S2: one CTA per tile, re-reads its tile (L2), out = tile prefix + in-tile
+//     scan; flags ulp-level decreases (a parallel association is not the
+//     reference's serial fold) for the rare-path running-max repair S3.
+template <typename T, typename A, bool kFloat>
+__global__ void __launch_bounds__(kTileThreads) k_sc_reduce(const T* __restrict__ in, int64_t n, Hier<A> h,
+                                                             uint32_t* status) {
   __shared__ A warp_sums[kTileThreads / 32];
-  __shared__ int slot;
-  const int64_t b = acquire_tile(&hdr->ticket[kTicketPass1], &slot);
-  const int64_t base = b * kTile;
-  const uint64_t pol = policy_evict_last();  // keep w in L2 for pass 2
-  T x[kTileItems];
-  tile_load<T>(w, n, base, stage, pol, x);
-  TileScan<A> s;
-  uint32_t flags = 0;
+  __shared__ uint32_t cta_flags;
+  __shared__ int stage;
+  const int64_t b = blockIdx.x;
+  if (threadIdx.x == 0) cta_flags = 0;
+  {
+    T x[kTileItems];
+    tile_load_any<T>(in, n, b * kTile, x);
+    uint32_t f = 0;
+    TileScan<A> s;
+    if constexpr (kFloat) {
+      FlagAcc<T> acc;
 #pragma unroll
-  for (int j = 0; j < kTileItems; ++j) {
-    const bool valid = base + threadIdx.x * kTileItems + j < n;
-    if (valid) flags |= weight_flags(x[j]);
-    s.loc[j] = (A)x[j];
-  }
-  status_or_warp(status, flags);
-  tile_scan<A>(s, warp_sums);
-  if (threadIdx.x == 0) tree_publish<A, SumOp>(tree, b, s.tile_total);
-  // the tile holding w[N-1] computes the normaliser W[N-1]
-  if (b == tree.tiles - 1) {
-    A prefix = A(0);
-    __syncwarp();
-    if (threadIdx.x < 32) prefix = tree_prefix<A, SumOp>(tree, b, A(0));
-    if (threadIdx.x == 0) warp_sums[0] = prefix;
-    __syncthreads();
-    prefix = warp_sums[0];
-    const int64_t p = (n - 1) - base;
-    if (threadIdx.x == p / kTileItems) {
-      const A basev = add_rn(prefix, s.thread_excl);
-      A wl = s.loc[0];
+      for (int j = 0; j < kTileItems; ++j) acc.add(x[j]);
+      f = acc.flags() & PFR_ST_NONFINITE;
+    } else {
 #pragma unroll
       for (int j = 0; j < kTileItems; ++j)
-        if (j == p % kTileItems) wl = s.loc[j];
-      const A total = add_rn(basev, wl);
-      st_relaxed_u64(&hdr->cell[0], Cell<A>::encode(total));
+        if (x[j] < T(0)) f |= PFR_ST_NEGCOUNT;
     }
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
+    tile_scan<A>(s, warp_sums);
+    if (threadIdx.x == kTileThreads - 1) h.agg[b] = add_rn(s.thread_excl, s.loc[kTileItems - 1]);
+    f = __reduce_or_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && f) atomicOr(&cta_flags, f);
   }
+  hier_tile_done(h, b, &cta_flags, &stage, status);
+  if (stage == 2 && threadIdx.x == 0) h.state->flags = 0;
 }
 
-// ---------------------------------------------------------------------------
-// pass 2: cumulative offspring
-enum UMode { kUSystematic = 0, kUArray = 1, kUNumpy = 2, kUPhilox = 3 };
-
-template <typename T, typename A, int UM>
-__device__ __forceinline__ A stratum_offset(int64_t k0based, A u_sys, const double* __restrict__ uniforms,
-                                            Key2x64 key) {
-  if constexpr (UM == kUSystematic) {
-    return u_sys;
-  } else if constexpr (UM == kUArray) {
-    return (A)(T)uniforms[k0based];  // cast to the weight dtype (resamplers.py:124)
-  } else if constexpr (UM == kUNumpy) {
-    return (A)(T)u64_to_unit(numpy_raw64(key, (uint64_t)k0based));
-  } else {
-    uint32_t o[4];
-    philox4x32_10((uint32_t)(k0based >> 2), (uint32_t)(k0based >> 34), kTagStratified, 0, (uint32_t)key.k0,
-                  (uint32_t)(key.k0 >> 32), o);
-    const uint32_t r = o[k0based & 3];
-    return (A)(T)u32_to_unit_d(r);
-  }
-}
-
-template <typename T, typename A, int UM>
+template <typename T, typename A, typename U, bool kFloat>
 __global__ void __launch_bounds__(kTileThreads)
-    k_offspring(const T* __restrict__ w, int64_t n, Tree sum_tree, Tree max_tree, WsHeader* hdr, A u_sys,
-                const double* __restrict__ uniforms, Key2x64 key, int32_t* __restrict__ O, uint32_t* status) {
-  __shared__ __align__(16) uint4 stage[kTile * sizeof(T) / 16 > kTile * 4 / 16 ? kTile * sizeof(T) / 16
-                                                                                 : kTile * 4 / 16];
+    k_sc_apply(const T* in, U* out, int64_t n, Hier<A> h, int exclusive, int repair, void* total_out,
+               int64_t expect_total, uint32_t* status) {
+  constexpr size_t kStageOut = kTile * sizeof(U) / 16;
+  __shared__ __align__(16) uint4 stage[kStageOut];
   __shared__ A warp_sums[kTileThreads / 32];
-  __shared__ int64_t imax8[kTileThreads / 32];
-  __shared__ int slot;
-  __shared__ A sh_prefix;
-  __shared__ int64_t sh_pmax;
-  const int64_t b = acquire_tile(&hdr->ticket[kTicketPass2], &slot);
+  __shared__ A wlast[kTileThreads / 32];
+  griddep_wait_scan();
+  const int64_t b = blockIdx.x;
   const int64_t base = b * kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   T x[kTileItems];
-  tile_load<T>(w, n, base, stage, policy_evict_first(), x);
+  tile_load_any<T>(in, n, base, x);
   TileScan<A> s;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
   tile_scan<A>(s, warp_sums);
-  if (threadIdx.x < 32) {
-    const A p = tree_prefix<A, SumOp>(sum_tree, b, A(0));
-    if (threadIdx.x == 0) sh_prefix = p;
-  }
-  __syncthreads();
-  const A total = Cell<A>::decode(ld_relaxed_u64(&hdr->cell[0]));
-  const A nA = (A)n;
-  const A basev = add_rn(sh_prefix, s.thread_excl);
-  int32_t o[kTileItems];
-#pragma unroll
-  for (int j = 0; j < kTileItems; ++j) {
-    const A W = add_rn(basev, s.loc[j]);
-    const A r = div_rn(mul_rn(W, nA), total);
-    int64_t k = floor_to_i64(r) + 1;  // 1-based stratum
-    if (k > n) k = n;
-    if (k < 1) k = 1;
-    const A u = stratum_offset<T, A, UM>(k - 1, u_sys, uniforms, key);
-    int64_t ov = floor_to_i64(add_rn(r, u));
-    if (ov > n) ov = n;
-    if (ov < 0) ov = 0;
-    o[j] = (int32_t)ov;
-  }
-  // running-max repair (resamplers.py:150): exact, order independent
-  const int64_t my_max = o[kTileItems - 1];
-  int64_t tile_max;
-  const int64_t before = block_excl_max<int64_t>(my_max, INT64_MIN, imax8, tile_max);
-  if (threadIdx.x == 0) tree_publish<int64_t, MaxOp>(max_tree, b, tile_max);
-  __syncwarp();
-  if (threadIdx.x < 32) {
-    const int64_t pm = tree_prefix<int64_t, MaxOp>(max_tree, b, INT64_MIN);
-    if (threadIdx.x == 0) sh_pmax = pm;
-  }
-  __syncthreads();
-  const int64_t floor_v = MaxOp::combine(sh_pmax, before);
-  uint32_t repaired = 0;
-#pragma unroll
-  for (int j = 0; j < kTileItems; ++j) {
-    if (o[j] < floor_v) {
-      o[j] = (int32_t)floor_v;
-      repaired = PFR_ST_REPAIRED;
-    }
-    if (base + threadIdx.x * kTileItems + j == n - 1) o[j] = (int32_t)n;  // O[-1] = N
-  }
-  status_or_warp(status, repaired);
-  tile_store<int32_t>(O, n, base, stage, o, policy_evict_last());
-}
-
-// ---------------------------------------------------------------------------
-// single-pass scan (inclusive or exclusive) with monotone repair for floats
-template <typename T, typename A, typename U, bool kFloat>
-__global__ void __launch_bounds__(kTileThreads)
-    k_scan(const T* __restrict__ in, U* __restrict__ out, int64_t n, Tree sum_tree, Tree max_tree, WsHeader* hdr,
-           int exclusive, int repair, void* total_out, int64_t expect_total, uint32_t* status) {
-  constexpr size_t kStageIn = kTile * sizeof(T) / 16;
-  constexpr size_t kStageOut = kTile * sizeof(U) / 16;
-  __shared__ __align__(16) uint4 stage[kStageIn > kStageOut ? kStageIn : kStageOut];
-  __shared__ A warp_sums[kTileThreads / 32];
-  __shared__ A amax8[kTileThreads / 32];
-  __shared__ A wlast[kTileThreads / 32];
-  __shared__ int slot;
-  __shared__ A sh_prefix, sh_pmax;
-  const int64_t b = acquire_tile(&hdr->ticket[kTicketScan], &slot);
-  const int64_t base = b * kTile;
-  T x[kTileItems];
-  tile_load<T>(in, n, base, stage, policy_evict_first(), x);
-  TileScan<A> s;
-  uint32_t flags = 0;
-#pragma unroll
-  for (int j = 0; j < kTileItems; ++j) {
-    const bool valid = base + threadIdx.x * kTileItems + j < n;
-    if constexpr (kFloat) {
-      if (valid && !isfinite((double)x[j])) flags |= PFR_ST_NONFINITE;
-    } else {
-      if (valid && x[j] < T(0)) flags |= PFR_ST_NEGCOUNT;
-    }
-    s.loc[j] = (A)x[j];
-  }
-  status_or_warp(status, flags);
-  tile_scan<A>(s, warp_sums);
-  if (threadIdx.x == 0) tree_publish<A, SumOp>(sum_tree, b, s.tile_total);
-  __syncwarp();
-  if (threadIdx.x < 32) {
-    const A p = tree_prefix<A, SumOp>(sum_tree, b, A(0));
-    if (threadIdx.x == 0) sh_prefix = p;
-  }
-  __syncthreads();
-  const A basev = add_rn(sh_prefix, s.thread_excl);
+  const A ex = b ? h.tile_excl(b) : A(0);
+  const A prev_tile_end = b ? h.tile_end(b - 1) : A(0);
   A v[kTileItems];
 #pragma unroll
-  for (int j = 0; j < kTileItems; ++j) v[j] = add_rn(basev, s.loc[j]);
-  A prev_tile_last = A(0);  // W of the element before this tile
-  if (kFloat && !repair) {
-    // no repair: the exclusive shift needs the raw W at the end of tile b-1,
-    // published per tile (depends only on the sum tree: no serial chain)
-    if (threadIdx.x == kTileThreads - 1) st_relaxed_u64(&max_tree.cells[b], Cell<A>::encode(v[kTileItems - 1]));
-    if (exclusive && threadIdx.x == 0 && b > 0) sh_pmax = cell_wait<A>(&max_tree.cells[b - 1]);
-    __syncthreads();
-    prev_tile_last = b ? sh_pmax : A(0);
-  } else if constexpr (kFloat) {
-    // W_raw is monotone inside a thread; repair across threads and tiles with a
-    // running max (exact): W = max(prefix max of earlier tiles, earlier threads, own)
-    const A ident = -INFINITY;
-    A tile_max;
-    const A before = block_excl_max<A>(v[kTileItems - 1], ident, amax8, tile_max);
-    if (threadIdx.x == 0) tree_publish<A, MaxOp>(max_tree, b, tile_max);
-    __syncwarp();
-    if (threadIdx.x < 32) {
-      const A pm = tree_prefix<A, MaxOp>(max_tree, b, ident);
-      if (threadIdx.x == 0) sh_pmax = pm;
-    }
-    __syncthreads();
-    const A fl = MaxOp::combine(sh_pmax, before);
+  for (int j = 0; j < kTileItems; ++j) v[j] = add_rn(ex, add_rn(s.thread_excl, s.loc[j]));
+  // value before this thread's first element
+  A prev = __shfl_up_sync(0xffffffffu, v[kTileItems - 1], 1);
+  if (lane == 31) wlast[warp] = v[kTileItems - 1];
+  __syncthreads();
+  if (lane == 0) prev = warp ? wlast[warp - 1] : prev_tile_end;
+  const int e0 = threadIdx.x * kTileItems;
+  const int64_t len = min((int64_t)kTile, n - base);
+  if (kFloat && repair) {
+    bool bad = e0 < len && (b > 0 || e0 > 0) && v[0] < prev;
 #pragma unroll
-    for (int j = 0; j < kTileItems; ++j) v[j] = MaxOp::combine(fl, v[j]);
-    prev_tile_last = (b == 0) ? A(0) : sh_pmax;
-  } else {
-    prev_tile_last = sh_prefix;
+    for (int j = 1; j < kTileItems; ++j) bad |= e0 + j < len && v[j] < v[j - 1];
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&h.state->flags, kScanRepair);
   }
   // total = W[N-1]
   {
@@ -283,11 +142,6 @@ __global__ void __launch_bounds__(kTileThreads)
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) y[j] = (U)v[j];
   } else {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    A prev = __shfl_up_sync(0xffffffffu, v[kTileItems - 1], 1);
-    if (lane == 31) wlast[warp] = v[kTileItems - 1];
-    __syncthreads();
-    if (lane == 0) prev = (warp == 0) ? prev_tile_last : wlast[warp - 1];
 #pragma unroll
     for (int j = kTileItems - 1; j > 0; --j) y[j] = (U)v[j - 1];
     y[0] = (U)prev;
@@ -295,13 +149,89 @@ __global__ void __launch_bounds__(kTileThreads)
   tile_store<U>(out, n, base, stage, y, policy_evict_first());
 }
 
+// S3 (rare path, cooperative; returns at once unless S2 flagged a decrease):
+// out = running max of out (exact), status REPAIRED, total = max.
+template <typename U>
+__global__ void __launch_bounds__(kTileThreads) k_sc_repair(U* out, int64_t n, int64_t tiles, DvState* state,
+                                                             U* tmax, int exclusive, void* total_out,
+                                                             uint32_t* status) {
+  __shared__ U smax8[kTileThreads / 32];
+  griddep_wait_scan();
+  if (!(*(volatile unsigned*)&state->flags & kScanRepair)) return;
+  cg::grid_group grid = cg::this_grid();
+  // A: per-tile maxima
+  for (int64_t b = blockIdx.x; b < tiles; b += gridDim.x) {
+    U m = -INFINITY;
+    for (int64_t i = b * kTile + threadIdx.x; i < min(n, (b + 1) * kTile); i += kTileThreads) m = fmax(m, out[i]);
+    U bm;
+    block_excl_max<U>(m, (U)-INFINITY, smax8, bm);
+    if (threadIdx.x == 0) tmax[b] = bm;
+  }
+  grid.sync();
+  // B: exclusive max over tiles (serial: rare path)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    U run = -INFINITY;
+    for (int64_t b = 0; b < tiles; ++b) {
+      const U v = tmax[b];
+      tmax[b] = run;
+      run = fmax(run, v);
+    }
+    if (total_out) *reinterpret_cast<double*>(total_out) = fmax(*reinterpret_cast<double*>(total_out), (double)run);
+    status_or(status, PFR_ST_REPAIRED);
+  }
+  grid.sync();
+  // C: apply, one thread per tile segment of 16 (serial within, block max-scan across)
+  for (int64_t b = blockIdx.x; b < tiles; b += gridDim.x) {
+    const int64_t i0 = b * kTile + threadIdx.x * kTileItems;
+    U loc[kTileItems];
+    U m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      loc[j] = i0 + j < n ? out[i0 + j] : (U)-INFINITY;
+      m = fmax(m, loc[j]);
+    }
+    U bm;
+    const U before = block_excl_max<U>(m, (U)-INFINITY, smax8, bm);
+    U run = fmax(before, tmax[b]);
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      run = fmax(run, loc[j]);
+      if (i0 + j < n) out[i0 + j] = run;
+    }
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) state->flags &= ~kScanRepair;
+}
+
 // ---------------------------------------------------------------------------
+// check_weights (diagnostics.py:38-51): 16-byte vector loads, four in flight
+// per thread, flags from integer maxima of the bit patterns (FlagAcc)
 template <typename T>
-__global__ void k_check_weights(const T* __restrict__ w, int64_t n, uint32_t* status) {
-  uint32_t f = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    f |= weight_flags(w[i]);
-  status_or_warp(status, f);
+__global__ void __launch_bounds__(256) k_check_weights(const T* __restrict__ w, int64_t n, uint32_t* status) {
+  constexpr int kPer = 16 / sizeof(T);
+  FlagAcc<T> acc;
+  const int64_t nvec = ((reinterpret_cast<uintptr_t>(w) & 15) == 0) ? n / kPer : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; v + 3 * stride < nvec; v += 4 * stride) {
+    uint4 x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = __ldcs(reinterpret_cast<const uint4*>(w) + v + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const T* e = reinterpret_cast<const T*>(&x[k]);
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) acc.add(e[t]);
+    }
+  }
+  for (; v < nvec; v += stride) {
+    const uint4 x = __ldcs(reinterpret_cast<const uint4*>(w) + v);
+    const T* e = reinterpret_cast<const T*>(&x);
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) acc.add(e[t]);
+  }
+  for (int64_t i = nvec * kPer + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) acc.add(w[i]);
+  status_or_warp(status, acc.flags());
 }
 
 template <typename T, typename U, bool kCumulative>
@@ -382,62 +312,57 @@ Tree make_tree(uint64_t* cells, int64_t tiles) {
   return t;
 }
 
-template <typename T, typename A>
-cudaError_t offspring_typed(const T* w, int64_t n, int stratified, double offset, const double* uniforms,
-                            const pfr_rng* rng, int32_t* O, uint32_t* status, const Workspace& ws, cudaStream_t s) {
-  const int64_t tiles = num_tiles(n);
-  Tree sum_tree = make_tree(ws.sum_cells, tiles);
-  Tree max_tree = make_tree(ws.max_cells, tiles);
-  k_tile_sums<T, A><<<(unsigned)tiles, kTileThreads, 0, s>>>(w, n, sum_tree, ws.hdr, status);
-  note_launch();
-  Key2x64 key{rng ? rng->key0 : 0, rng ? rng->key1 : 0};
-  const A u_sys = (A)(T)offset;  // systematic: u cast to the weight dtype (resamplers.py:135)
-  if (!stratified) {
-    k_offspring<T, A, kUSystematic>
-        <<<(unsigned)tiles, kTileThreads, 0, s>>>(w, n, sum_tree, max_tree, ws.hdr, u_sys, nullptr, key, O, status);
-  } else if (uniforms) {
-    k_offspring<T, A, kUArray>
-        <<<(unsigned)tiles, kTileThreads, 0, s>>>(w, n, sum_tree, max_tree, ws.hdr, u_sys, uniforms, key, O, status);
-  } else if (rng && rng->mode == PFR_RNG_NUMPY) {
-    k_offspring<T, A, kUNumpy>
-        <<<(unsigned)tiles, kTileThreads, 0, s>>>(w, n, sum_tree, max_tree, ws.hdr, u_sys, nullptr, key, O, status);
-  } else {
-    k_offspring<T, A, kUPhilox>
-        <<<(unsigned)tiles, kTileThreads, 0, s>>>(w, n, sum_tree, max_tree, ws.hdr, u_sys, nullptr, key, O, status);
+template <typename K, typename... Args>
+cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, cudaStream_t s, bool pdl, bool cooperative, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
   }
+  if (cooperative) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
   note_launch();
-  return cudaGetLastError();
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 template <typename T, typename A, typename U, bool kFloat>
 cudaError_t scan_typed(const void* in, void* out, int64_t n, int exclusive, int repair, void* total,
                        int64_t expect_total, uint32_t* status, const Workspace& ws, cudaStream_t s) {
   const int64_t tiles = num_tiles(n);
-  Tree sum_tree = make_tree(ws.sum_cells, tiles);
-  Tree max_tree = make_tree(ws.max_cells, tiles);
-  k_scan<T, A, U, kFloat><<<(unsigned)tiles, kTileThreads, 0, s>>>(
-      (const T*)in, (U*)out, n, sum_tree, max_tree, ws.hdr, exclusive, repair, total, expect_total, status);
-  note_launch();
-  return cudaGetLastError();
+  A* agg = reinterpret_cast<A*>(ws.sum_cells);
+  Hier<A> h{agg, reinterpret_cast<A*>(ws.max_cells), agg + tiles + 8, ws.dv, tiles};
+  cudaError_t e = launch_ex(k_sc_reduce<T, A, kFloat>, dim3((unsigned)tiles), dim3(kTileThreads), s, false, false,
+                            (const T*)in, n, h, status);
+  if (e != cudaSuccess) return e;
+  e = launch_ex(k_sc_apply<T, A, U, kFloat>, dim3((unsigned)tiles), dim3(kTileThreads), s, true, false,
+                (const T*)in, (U*)out, n, h, exclusive, repair, total, expect_total, status);
+  if (e != cudaSuccess) return e;
+  if constexpr (kFloat) {
+    if (repair) {
+      // tile maxima scratch: the sum-tree region past the aggregates and group totals
+      U* tmax = reinterpret_cast<U*>(agg + tiles + 8 + (tiles + kGroupTiles - 1) / kGroupTiles + 8);
+      e = launch_ex(k_sc_repair<U>, dim3((unsigned)num_sms()), dim3(kTileThreads), s, true, true, (U*)out, n, tiles,
+                    ws.dv, tmax, exclusive, total, status);
+    }
+  }
+  return e;
 }
 
 }  // namespace
 
-cudaError_t launch_offspring(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
-                             const double* uniforms, const pfr_rng* rng, int32_t* O, uint32_t* status,
-                             const Workspace& ws, cudaStream_t s) {
-  cudaError_t e = workspace_reset(ws, s);
-  if (e != cudaSuccess) return e;
-  if (dtype == PFR_F64) return offspring_typed<double, double>((const double*)w, n, stratified, offset, uniforms, rng, O, status, ws, s);
-  if (accum == PFR_ACC_NATIVE)
-    return offspring_typed<float, float>((const float*)w, n, stratified, offset, uniforms, rng, O, status, ws, s);
-  return offspring_typed<float, double>((const float*)w, n, stratified, offset, uniforms, rng, O, status, ws, s);
-}
-
 cudaError_t launch_scan(const void* in, void* out, int64_t n, int dtype, int out_dtype, int accum, int exclusive,
                         void* total, int64_t expect_total, uint32_t* status, const Workspace& ws, cudaStream_t s) {
-  cudaError_t e = workspace_reset(ws, s);
-  if (e != cudaSuccess) return e;
   const int repair = (accum & PFR_SCAN_MONOTONE) ? 1 : 0;
   const bool native = (accum & 0xFF) == PFR_ACC_NATIVE;
 #define PFR_SCAN_ARGS in, out, n, exclusive, repair, total, expect_total, status, ws, s
@@ -460,7 +385,8 @@ cudaError_t launch_scan(const void* in, void* out, int64_t n, int dtype, int out
 }
 
 cudaError_t launch_check_weights(const void* w, int64_t n, int dtype, uint32_t* status, cudaStream_t s) {
-  const int g = grid_for(n, 256);
+  const int64_t vecs = n * (dtype == PFR_F64 ? 8 : 4) / 16;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((vecs + 1023) / 1024, (int64_t)num_sms() * 8));
   if (dtype == PFR_F64)
     k_check_weights<double><<<g, 256, 0, s>>>((const double*)w, n, status);
   else

@@ -178,6 +178,33 @@ __device__ __forceinline__ void tile_load(const T* __restrict__ in, int64_t n, i
   __syncthreads();
 }
 
+// Blocked direct loads: thread t gets elements [16t, 16t + 16) of the tile
+// through L1-allocating 16-byte loads (the 4-8 loads of a thread cover whole
+// lines), zero padded past n.  No shared memory, no barrier.
+template <typename T>
+__device__ __forceinline__ void tile_load_any(const T* __restrict__ in, int64_t n, int64_t base, T (&x)[kTileItems]) {
+  constexpr int kPerVec = 16 / sizeof(T);
+  const int64_t e0 = base + (int64_t)threadIdx.x * kTileItems;
+  if (e0 + kTileItems <= n && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    uint4 v[kTileItems / kPerVec];
+#pragma unroll
+    for (int q = 0; q < kTileItems / kPerVec; ++q) v[q] = __ldg(reinterpret_cast<const uint4*>(in + e0) + q);
+#pragma unroll
+    for (int q = 0; q < kTileItems / kPerVec; ++q) {
+      union {
+        uint4 u;
+        T e[kPerVec];
+      } tmp;
+      tmp.u = v[q];
+#pragma unroll
+      for (int e = 0; e < kPerVec; ++e) x[q * kPerVec + e] = tmp.e[e];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) x[j] = (e0 + j < n) ? in[e0 + j] : T(0);
+  }
+}
+
 // Store per-thread blocked registers y[16] of U to out[base ...] (clipped at n).
 template <typename U>
 __device__ __forceinline__ void tile_store(U* __restrict__ out, int64_t n, int64_t base, uint4* smem,
