@@ -207,27 +207,61 @@ struct RejArgs {
 
 constexpr int kRejChunk = 256;
 
-// Each lane evaluates kRejBatch consecutive trips of its slot per iteration:
+// Each lane evaluates kRejBatch (default 8) consecutive trips of its slot per iteration:
 // the trips' proposals do not depend on earlier outcomes, so their Philox
 // words and weight gathers are all issued before the first comparison (4
 // gathers in flight per lane instead of one dependent L2 round trip per trip).
 // The first accepting trip of the batch wins, so results, trip counts and the
 // stream mapping are exactly those of a one-trip-at-a-time loop; the few
 // trips evaluated past the acceptance are discarded.
+// draws of trips trip .. trip+B-1 of `slot` (trip even): Philox counters
+// (slot, trip/2 + q), words (2h, 2h+1) = (proposal, uniform); trip 0
+// proposes the slot itself (resamplers.py:291-294)
+template <typename T, int B>
+struct RejBatch {
+  uint32_t j[B];
+  T u[B];
+};
+
+template <typename T, int B>
+__device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, uint32_t trip, RejBatch<T, B>& d) {
+  const uint32_t nn = (uint32_t)A.n;
+#pragma unroll
+  for (int q = 0; q < B / 2; ++q) {
+    uint32_t o[4];
+    philox4x32_10(slot, (trip >> 1) + q, kTagRejection, 0, A.k0, A.k1, o);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      // power-of-two N (threshold 0): Lemire never rejects
+      d.j[2 * q + h] = A.threshold == 0 ? __umulhi(o[2 * h], nn)
+                                        : bounded_u32(o[2 * h], nn, A.threshold, slot, trip + 2 * q + h,
+                                                      kTagRejection, A.k0, A.k1);
+      if constexpr (sizeof(T) == 4)
+        d.u[2 * q + h] = u32_to_unit_f(o[2 * h + 1]);
+      else
+        d.u[2 * q + h] = u32_to_unit_d(o[2 * h + 1]);
+    }
+  }
+  if (trip == 0) d.j[0] = slot;
+}
+
+// Software pipelined: the gathers of batch k are issued, then the draws of
+// batch k+1 are computed while they are in flight, then batch k is resolved.
+// A lane whose slot finishes discards its precomputed batch (one per slot).
 template <typename T, bool kCapped, int kRejBatch>
 __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
   const int lane = threadIdx.x & 31;
   const T bound = (T)A.bound;
   const T capv = (T)A.cap;
-  const uint32_t nn = (uint32_t)A.n;
   int64_t chunk_next = 0, chunk_end = 0;  // warp-uniform local queue
   bool exhausted = false;                 // warp-uniform: no chunks left
   int64_t slot = -1;
   uint32_t trip = 0;
   uint32_t flags = 0;
   int iter = 0;
+  RejBatch<T, kRejBatch> cur;
   while (true) {
-    // refill idle lanes
+    // refill idle lanes (a new slot starts with its first batch of draws)
     unsigned idle = __ballot_sync(0xffffffffu, slot < 0);
     while (idle) {
       if (chunk_next >= chunk_end) {
@@ -247,52 +281,37 @@ __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
       if (slot < 0 && rank < take) {
         slot = chunk_next + rank;
         trip = 0;
+        rej_draws<T, kRejBatch>(A, (uint32_t)slot, 0u, cur);
       }
       chunk_next += take;
       idle = __ballot_sync(0xffffffffu, slot < 0);
     }
     if (__ballot_sync(0xffffffffu, slot >= 0) == 0) break;
     if (slot >= 0) {
-      // trips trip .. trip+kRejBatch-1 (trip is even): counters (slot, trip/2 + q)
-      uint32_t j[kRejBatch];
-      T uu[kRejBatch], wj[kRejBatch];
+      T wj[kRejBatch];
 #pragma unroll
-      for (int q = 0; q < kRejBatch / 2; ++q) {
-        uint32_t o[4];
-        philox4x32_10((uint32_t)slot, (trip >> 1) + q, kTagRejection, 0, A.k0, A.k1, o);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          // power-of-two N (threshold 0): Lemire never rejects
-          j[2 * q + h] = A.threshold == 0 ? __umulhi(o[2 * h], nn)
-                                          : bounded_u32(o[2 * h], nn, A.threshold, (uint32_t)slot,
-                                                        trip + 2 * q + h, kTagRejection, A.k0, A.k1);
-          if constexpr (sizeof(T) == 4)
-            uu[2 * q + h] = u32_to_unit_f(o[2 * h + 1]);
-          else
-            uu[2 * q + h] = u32_to_unit_d(o[2 * h + 1]);
-        }
-      }
-      if (trip == 0) j[0] = (uint32_t)slot;  // trip 0 proposes the slot itself (resamplers.py:291-294)
-#pragma unroll
-      for (int q = 0; q < kRejBatch; ++q) wj[q] = ldg(A.w + j[q]);
+      for (int q = 0; q < kRejBatch; ++q) wj[q] = ldg(A.w + cur.j[q]);
+      // next batch's draws overlap the gathers' latency
+      RejBatch<T, kRejBatch> nxt;
+      rej_draws<T, kRejBatch>(A, (uint32_t)slot, trip + kRejBatch, nxt);
       int done = -1;  // batch position of the first accepting trip
 #pragma unroll
       for (int q = kRejBatch - 1; q >= 0; --q) {
         const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
         // beta <= v[j] / bound  <=>  beta * bound <= v[j]
-        if (uu[q] * bound <= vj) done = q;
+        if (cur.u[q] * bound <= vj) done = q;
       }
       // round cap: the trips past max_trips do not exist
       const bool near_cap = trip + (uint32_t)kRejBatch >= A.max_trips;
       if (near_cap && (done < 0 || trip + (uint32_t)done + 1 > A.max_trips)) done = -2;
       if (done >= 0) {
         T wd = wj[0];
-        uint32_t jd = j[0];
+        uint32_t jd = cur.j[0];
 #pragma unroll
         for (int q = 1; q < kRejBatch; ++q)
           if (done == q) {
             wd = wj[q];
-            jd = j[q];
+            jd = cur.j[q];
           }
         A.a[slot] = (int32_t)jd;
         if (A.trips) A.trips[slot] = (int32_t)(trip + done + 1);
@@ -309,6 +328,7 @@ __global__ void __launch_bounds__(256) k_rejection_philox(RejArgs<T> A) {
         slot = -1;
       } else {
         trip += kRejBatch;
+        cur = nxt;
       }
     }
     if (((++iter) & 63) == 0) {
@@ -493,7 +513,7 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
   // trips evaluated per lane and iteration (PFR_REJ_BATCH: profiling aid)
   static const int batch = [] {
     const char* v = getenv("PFR_REJ_BATCH");
-    return v && atoi(v) == 8 ? 8 : (v && atoi(v) == 2 ? 2 : 4);
+    return v && atoi(v) == 4 ? 4 : (v && atoi(v) == 2 ? 2 : 8);
   }();
 #define PFR_REJ_LAUNCH(T, CAP, B) k_rejection_philox<T, CAP, B><<<blocks_for(k_rejection_philox<T, CAP, B>), 256, 0, s>>>(A)
 #define PFR_REJ_DISPATCH(T, CAP)     \
