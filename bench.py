@@ -392,7 +392,12 @@ def main():
     # ---------------- north-star targets: N = 2^24 float32 ----------------
     targets = None
     if not args.no_targets:
-        targets = north_star_targets(pf, torch, dev, stream, flush, hbm)
+        targets = north_star_targets(pf, torch, dev, stream, flush, hbm) if rank == 0 else {}
+        # config 4: ONE filter of N = 2^28 float32, weight-sharded over the ranks
+        try:
+            targets.update(c4_targets(pf, torch, dev, stream, flush, hbm, rank, world))
+        except Exception as exc:  # keep the bench line even if this optional leg fails
+            targets["c4_error"] = f"{type(exc).__name__}: {exc}"[:300]
 
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu = None
@@ -468,6 +473,77 @@ def north_star_targets(pf, torch, dev, stream, flush, hbm, reps=10):
     out["metropolis_B32_2^24_f32_delivery"] = {"us": t * 1e3, "particles_per_s": n / (t * 1e-3)}
     del w, c, a
     return out
+
+
+def c4_targets(pf, torch, dev, stream, flush, hbm, rank, world, n_log2=28, reps=3):
+    """BASELINE.json configs[3]: a single filter of N = 2^28 float32 log-normal
+    weights, systematic delivery weight-sharded over `world` GPUs
+    (paper_1301_4019_b200.sharded: shard totals all-gather + slot-word
+    all-to-all + walker rounds, NCCL) and Metropolis(B=32) with the chains
+    partitioned over the ranks.  At world == 1 this is the single-GPU path.
+    Device time per rank (CUDA events), max over ranks."""
+    import torch.distributed as dist
+
+    from paper_1301_4019_b200 import sharded
+
+    n = 1 << n_log2
+    n_loc = n // world
+    g = torch.Generator(device=dev)
+    g.manual_seed(2828 + rank)
+    lw = torch.randn(n_loc, device=dev, generator=g, dtype=torch.float32)
+    mx = lw.max()
+    if world > 1:
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    w = torch.exp(lw - mx)
+    del lw
+    out = {}
+    comm = sharded.DistComm() if world > 1 else None
+    ops = sharded.CudaShardOps() if world > 1 else None
+
+    def timed(fn):
+        ts = []
+        for r in range(reps + 1):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            torch.cuda._sleep(PREROLL_CYCLES)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn(r)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if r >= 1:
+                ts.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    cfg = pf.ResamplerConfig("systematic")
+    if world == 1:
+        c = torch.empty(n, dtype=torch.int32, device=dev)
+        t = timed(lambda r: pf.deliver(w, cfg, pf.RngStream(r), index_dtype=torch.int32, out=c))
+        del c
+    else:
+        t = timed(lambda r: sharded.deliver_sharded(w, cfg, pf.RngStream(r), comm=comm, ops=ops))
+    b = 8 * n
+    out[f"c4_systematic_delivery_2^{n_log2}_f32_{world}gpu"] = {
+        "ms": t, "particles_per_s": n / (t * 1e-3), "algorithmic_bytes": b,
+        "achieved_gbs_aggregate": b / (t * 1e-3) / 1e9, "frac_of_aggregate_hbm": b / (t * 1e-3) / 1e9 / (hbm * world),
+        "scaling": "strong (one filter, fixed N)", "sharding": "weight shards, NCCL" if world > 1 else "single GPU"}
+    if world == 1:
+        t = timed(lambda r: pf.metropolis_ancestors(w, B_STEPS, pf.RngStream(r), index_dtype=torch.int32))
+    else:
+        t = timed(lambda r: sharded.metropolis_sharded(w, B_STEPS, pf.RngStream(r), comm=comm, ops=ops))
+    b = (4 + 4 + B_STEPS * 4) * n
+    out[f"c4_metropolis_B32_2^{n_log2}_f32_{world}gpu"] = {
+        "ms": t, "particles_per_s": n / (t * 1e-3), "algorithmic_bytes": b,
+        "achieved_gbs_aggregate": b / (t * 1e-3) / 1e9, "frac_of_aggregate_hbm": b / (t * 1e-3) / 1e9 / (hbm * world),
+        "note": "gathers from a 1 GiB weight vector: HBM random-sector bound"}
+    del w
+    return out if rank == 0 else {}
 
 
 if __name__ == "__main__":
