@@ -398,6 +398,10 @@ def main():
             targets.update(c4_targets(pf, torch, dev, stream, flush, hbm, rank, world))
         except Exception as exc:  # keep the bench line even if this optional leg fails
             targets["c4_error"] = f"{type(exc).__name__}: {exc}"[:300]
+        try:
+            targets.update(c5_targets(pf, torch, dev, stream, rank, world))
+        except Exception as exc:
+            targets["c5_error"] = f"{type(exc).__name__}: {exc}"[:300]
 
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu = None
@@ -544,6 +548,43 @@ def c4_targets(pf, torch, dev, stream, flush, hbm, rank, world, n_log2=28, reps=
         "note": "gathers from a 1 GiB weight vector: HBM random-sector bound"}
     del w
     return out if rank == 0 else {}
+
+
+def c5_targets(pf, torch, dev, stream, rank, world, filters=4096, n_log2=16, steps=100):
+    """BASELINE.json configs[4]: 4096 independent bootstrap filters x N = 2^16
+    particles, T = 100, on the linear-Gaussian model; the filters are split
+    over the ranks with no communication (each rank runs filters / world).
+    Device time per rank, max over ranks."""
+    import torch.distributed as dist
+
+    from paper_1301_4019_b200.pf import LinearGaussianModel, simulate_observations
+
+    model = LinearGaussianModel(coeff=0.9, trans_std=1.0, obs_std=1.0)
+    mine = filters // world
+    ys = np.stack([simulate_observations(model, steps, 1000 + rank * mine + k) for k in range(mine)])
+    n = 1 << n_log2
+    pf.pf_run(model, ys[:, :3], n, seed=1)  # warm-up (allocations, module load)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = pf.pf_run(model, ys, n, "systematic", 0.5, seed=7)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    resamples = int(res.resampled.sum()) * world
+    return {f"c5_batched_pf_{filters}x2^{n_log2}_T{steps}_{world}gpu": {
+        "ms": ms, "particle_steps_per_s": filters * n * steps / (ms * 1e-3),
+        "particles_resampled_per_s": resamples * n / (ms * 1e-3), "resampling_events": resamples,
+        "filters_per_gpu": mine, "note": "includes host->device copy of the observations and device->host "
+                                         "copy of means/ESS/log-likelihood (the pf_run API call)",
+        "cpu_reference_note": "SURVEY.md 6: the reference pf_run takes 1.95 s per filter (N=2^16, T=100) on "
+                              "one core, i.e. ~2.2 core-hours for 4096 filters"}} if rank == 0 else {}
 
 
 if __name__ == "__main__":

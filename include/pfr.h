@@ -272,6 +272,40 @@ int pfr_shard_advance(const int32_t* walkers, int64_t count, const uint32_t* wor
 int pfr_shard_scatter(const int32_t* done, int64_t count, int64_t index_base, int64_t n_loc, int32_t* c,
                       uint32_t* status, void* stream);
 
+/* ---- batches of independent filters -----------
+ * No communication: one CTA per filter.  Arrays are [filters, n] row-major. */
+
+size_t pfr_batched_workspace_bytes(int64_t filters, int64_t n);
+
+/* systematic delivery of every filter: c[m] = permute_parallel(
+ * cumulative_offspring_to_ancestors(systematic_cumulative_offspring(w[m])))
+ * (resamplers.py:127-153, ancestry.py:69-76, 139-174) with local indices;
+ * offsets[m] (nullable) are the filters' u in [0,1), else own Philox draws. */
+int pfr_deliver_batched(const void* w, int64_t filters, int64_t n, int dtype, const double* offsets,
+                        const pfr_rng* rng, int32_t* c, int32_t* max_steps, uint32_t* status, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* the scalar linear-Gaussian model of pf.py:41-64 */
+typedef struct pfr_pf_model {
+  double coeff;
+  double trans_std;
+  double obs_std;
+  double initial_mean;
+  double initial_std;
+} pfr_pf_model;
+
+size_t pfr_pf_workspace_bytes(int64_t filters, int64_t n);
+
+/* pf_run (pf.py:111-204) for `filters` independent bootstrap filters of n
+ * particles over `steps` observations y[filters, steps] (device): ESS-
+ * triggered systematic resampling through the in-place ancestry, propagate,
+ * weight, normalise.  Outputs (device): means[filters, steps],
+ * loglik[filters], ess[filters, steps] (ESS at the start of each step),
+ * resampled[filters, steps].  Weight collapse sets PFR_ST_NOPROGRESS. */
+int pfr_pf_run(const pfr_pf_model* model, const double* y, int64_t filters, int64_t n, int64_t steps,
+               double ess_threshold, const pfr_rng* rng, double* means, double* loglik, double* ess,
+               uint8_t* resampled, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,6 +88,10 @@ _SIGNATURES = {
     "pfr_shard_resolve": ([_P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P], _INT),
     "pfr_shard_advance": ([_P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P], _INT),
     "pfr_shard_scatter": ([_P, _I64, _I64, _I64, _P, _P, _P], _INT),
+    "pfr_batched_workspace_bytes": ([_I64, _I64], _SZ),
+    "pfr_deliver_batched": ([_P, _I64, _I64, _INT, _P, _RNGP, _P, _P, _P, _P, _SZ, _P], _INT),
+    "pfr_pf_workspace_bytes": ([_I64, _I64], _SZ),
+    "pfr_pf_run": ([_P, _P, _I64, _I64, _I64, _DBL, _RNGP, _P, _P, _P, _P, _P, _P, _SZ, _P], _INT),
 }
 
 _lib = None

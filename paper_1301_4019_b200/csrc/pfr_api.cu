@@ -431,4 +431,43 @@ int pfr_shard_scatter(const int32_t* done, int64_t count, int64_t index_base, in
                    "pfr_shard_scatter");
   return PFR_OK;
 }
+
+/* ---- batches of independent filters (pfr_batch.cu) ----------------------- */
+
+size_t pfr_batched_workspace_bytes(int64_t filters, int64_t n) {
+  return batched_workspace_bytes(filters < 1 ? 1 : filters, n < 1 ? 1 : n);
+}
+
+int pfr_deliver_batched(const void* w, int64_t filters, int64_t n, int dtype, const double* offsets,
+                        const pfr_rng* rng, int32_t* c, int32_t* max_steps, uint32_t* status, void* ws,
+                        size_t ws_bytes, void* stream) {
+  (void)status;
+  PFR_REQUIRE(filters >= 1 && valid_n(n) && filters * n < 0x7F000000LL * 64, "bad sizes");
+  PFR_REQUIRE(w && c && ws, "null array");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(offsets || (rng && rng->mode == PFR_RNG_PHILOX), "need offsets or a PHILOX stream");
+  PFR_REQUIRE(ws_bytes >= batched_workspace_bytes(filters, n), "workspace too small (see pfr_batched_workspace_bytes)");
+  PFR_CHECK_LAUNCH(launch_deliver_batched(w, filters, n, dtype, offsets, rng, c, max_steps, ws, (cudaStream_t)stream),
+                   "pfr_deliver_batched");
+  return PFR_OK;
+}
+
+size_t pfr_pf_workspace_bytes(int64_t filters, int64_t n) {
+  return pf_workspace_bytes(filters < 1 ? 1 : filters, n < 1 ? 1 : n);
+}
+
+int pfr_pf_run(const pfr_pf_model* model, const double* y, int64_t filters, int64_t n, int64_t steps,
+               double ess_threshold, const pfr_rng* rng, double* means, double* loglik, double* ess,
+               uint8_t* resampled, uint32_t* status, void* ws, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(model && y && means && loglik && ess && resampled && status && ws && rng, "null argument");
+  PFR_REQUIRE(filters >= 1 && n >= 2 && valid_n(n) && steps >= 1, "need filters >= 1, n >= 2, steps >= 1");
+  PFR_REQUIRE(model->trans_std > 0 && model->obs_std > 0 && model->initial_std > 0,
+              "trans_std, obs_std and initial_std must be strictly positive");
+  PFR_REQUIRE(ess_threshold >= 0.0 && ess_threshold <= 1.0, "ess_threshold must lie in [0, 1]");
+  PFR_REQUIRE(ws_bytes >= pf_workspace_bytes(filters, n), "workspace too small (see pfr_pf_workspace_bytes)");
+  PFR_CHECK_LAUNCH(launch_pf_run(model, y, filters, n, steps, ess_threshold, rng, means, loglik, ess, resampled, status,
+                                 ws, (cudaStream_t)stream),
+                   "pfr_pf_run");
+  return PFR_OK;
+}
 }  // extern "C"

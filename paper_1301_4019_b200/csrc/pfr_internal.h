@@ -113,6 +113,15 @@ cudaError_t launch_shard_advance(const int32_t* walkers, int64_t count, const ui
 cudaError_t launch_shard_scatter(const int32_t* done, int64_t count, int64_t index_base, int64_t n_loc, int32_t* c,
                                  uint32_t* status, cudaStream_t s);
 
+// launchers (pfr_batch.cu): batches of independent filters
+size_t batched_workspace_bytes(int64_t M, int64_t N);
+size_t pf_workspace_bytes(int64_t M, int64_t N);
+cudaError_t launch_deliver_batched(const void* w, int64_t M, int64_t n, int dtype, const double* offsets,
+                                   const pfr_rng* rng, int32_t* c, int32_t* max_steps, void* ws, cudaStream_t s);
+cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M, int64_t N, int64_t T,
+                          double ess_threshold, const pfr_rng* rng, double* means, double* loglik, double* ess,
+                          uint8_t* resampled, uint32_t* status, void* ws, cudaStream_t s);
+
 int num_sms();
 
 }  // namespace pfr

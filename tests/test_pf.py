@@ -1,0 +1,110 @@
+"""Batched bootstrap particle filter (BASELINE config 5)
+and the batched systematic delivery.
+
+CPU: the closed-form Kalman oracle and the observation simulator.
+GPU: the batched delivery is bit-identical per filter to the oracle's
+delivery (integer weights: exact sums); the batched filter's log-likelihood
+and filtered means agree with the exact Kalman filter (the reference's own
+end-to-end check, test_pf.py / acceptance C10)."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import pfr_oracle as orc
+from paper_1301_4019_b200.pf import LinearGaussianModel, exact_filter, simulate_observations
+
+
+def test_exact_filter_one_step_closed_form():
+    m = LinearGaussianModel(coeff=0.5, trans_std=1.5, obs_std=0.7, initial_mean=0.3, initial_std=2.0)
+    y = 1.1
+    r = exact_filter(m, [y])
+    p_pred = 0.25 * 4.0 + 2.25
+    s = p_pred + 0.49
+    gain = p_pred / s
+    assert math.isclose(r.means[0], 0.15 + gain * (y - 0.15), rel_tol=1e-15)
+    assert math.isclose(r.variances[0], (1 - gain) * p_pred, rel_tol=1e-15)
+    assert math.isclose(r.log_likelihood, -0.5 * (math.log(2 * math.pi * s) + (y - 0.15) ** 2 / s), rel_tol=1e-15)
+
+
+def test_model_validation_and_simulation():
+    with pytest.raises(ValueError, match="obs_std"):
+        LinearGaussianModel(obs_std=0.0)
+    m = LinearGaussianModel(coeff=0.9)
+    y = simulate_observations(m, 50, 3)
+    assert y.shape == (50,) and np.all(np.isfinite(y))
+    np.testing.assert_array_equal(y, simulate_observations(m, 50, 3))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("n", [1000, 4096, 70000])
+def test_deliver_batched_matches_oracle(dtype, n):
+    import paper_1301_4019_b200 as pf
+
+    g = np.random.default_rng(n)
+    filters = 6
+    w = g.integers(0, 40, (filters, n)).astype(dtype)
+    w[:, 0] += 1
+    offsets = g.random(filters)
+    c = pf.deliver_batched(w, offsets=offsets).cpu().numpy()
+    for m in range(filters):
+        want = orc.permute(orc.expand_cumulative(orc.systematic(w[m].astype(np.float64), float(dtype(offsets[m])))))
+        np.testing.assert_array_equal(c[m], want)
+        assert orc.satisfies_predicate(c[m])
+
+
+@pytest.mark.gpu
+def test_deliver_batched_lognormal_properties():
+    import paper_1301_4019_b200 as pf
+
+    g = np.random.default_rng(1)
+    w = np.exp(g.normal(0, 1, (32, 1 << 16)))
+    c, steps = pf.deliver_batched(w, pf.RngStream(5), return_max_steps=True)
+    c = c.cpu().numpy()
+    for m in range(0, 32, 7):
+        o = np.bincount(c[m], minlength=w.shape[1])
+        assert np.all(np.abs(o - w.shape[1] * w[m] / w[m].sum()) < 1.0)
+        assert orc.satisfies_predicate(c[m])
+    assert steps > 0
+
+
+@pytest.mark.gpu
+def test_batched_filter_against_kalman():
+    import paper_1301_4019_b200 as pf
+
+    model = LinearGaussianModel(coeff=0.9, trans_std=1.0, obs_std=0.8)
+    y = simulate_observations(model, 60, 11)
+    exact = exact_filter(model, y)
+    filters, n = 128, 4096
+    res = pf.pf_run(model, y, n, "systematic", 0.5, seed=3, filters=filters)
+    assert res.filtered_means.shape == (filters, 60)
+    assert np.all(res.ess[:, 0] == n)
+    assert 0.05 < res.resampled.mean() < 0.95
+    ll = res.log_likelihood
+    se = ll.std(ddof=1) / math.sqrt(filters)
+    # log of an unbiased likelihood estimate: bias ~ -var/2, tiny at N = 4096
+    assert abs(ll.mean() - exact.log_likelihood) < 5 * se + 0.05, (ll.mean(), exact.log_likelihood, se)
+    err = np.abs(res.filtered_means.mean(axis=0) - exact.means)
+    assert err.max() < 0.02, err.max()
+    # one filter: the reference's squeezed result
+    one = pf.pf_run(model, y, 2048, seed=9)
+    assert one.filtered_means.shape == (60,) and isinstance(one.log_likelihood, float)
+    assert abs(one.log_likelihood - exact.log_likelihood) < 2.0
+
+
+@pytest.mark.gpu
+def test_batched_filter_independent_observations_and_threshold():
+    import paper_1301_4019_b200 as pf
+
+    model = LinearGaussianModel(coeff=0.5, trans_std=0.5, obs_std=0.3)
+    ys = np.stack([simulate_observations(model, 20, s) for s in range(8)])
+    res = pf.pf_run(model, ys, 1024, ess_threshold=0.0, seed=1)
+    assert not res.resampled.any()  # threshold 0: sequential importance sampling
+    res1 = pf.pf_run(model, ys, 1024, ess_threshold=1.0, seed=1)
+    assert res1.resampled[:, 1:].all()
+    for m in range(8):
+        assert abs(res1.log_likelihood[m] - exact_filter(model, ys[m]).log_likelihood) < 3.0
