@@ -4,7 +4,7 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.txt 2>&1 || { cat gpurun_out/build.txt; exit 1; }
-timeout ${TEST_TIMEOUT:-1200} python -m pytest tests/test_gpu_parity.py -m gpu -q --timeout 300 -rf --tb=short ${PYTEST_ARGS} > gpurun_out/gpu_tests.txt 2>&1
+timeout ${TEST_TIMEOUT:-1200} python -m pytest tests/ -m gpu -q --timeout 600 -rf --tb=short ${PYTEST_ARGS} > gpurun_out/gpu_tests.txt 2>&1
 echo "pytest rc=$?" >> gpurun_out/gpu_tests.txt
 tail -5 gpurun_out/gpu_tests.txt
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.txt
