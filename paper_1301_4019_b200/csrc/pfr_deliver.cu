@@ -245,7 +245,11 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
   for (int j = 0; j < kTileItems; ++j) {
     const A W = add_rn(ex, add_rn(tex, s.loc[j]));
     o[j] = offspring_of<T, A, UM>(W, total, fx, p.n, p);
-    if (e0 + j == last) o[j] = (int32_t)p.n;  // O[N-1] = N
+  }
+  if (last >= 0) {  // the final tile: O[N-1] = N, and padding past N stays at N
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j)
+      if (e0 + j >= last) o[j] = (int32_t)p.n;
   }
   o_prev = 0;
   if (b > 0) {
@@ -260,21 +264,23 @@ __device__ __forceinline__ bool tile_decreases(const int32_t (&o)[kTileItems], i
                                                int32_t* warp_last) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e0 = threadIdx.x * kTileItems;
+  (void)e0;
+  (void)len;  // padding past N holds O = N: it never decreases
   bool bad = false;
 #pragma unroll
-  for (int j = 1; j < kTileItems; ++j) bad |= (e0 + j < len) && o[j] < o[j - 1];
+  for (int j = 1; j < kTileItems; ++j) bad |= o[j] < o[j - 1];
   int prev = __shfl_up_sync(0xffffffffu, o[kTileItems - 1], 1);
   if (lane == 31) warp_last[warp] = o[kTileItems - 1];
   __syncthreads();
   if (lane == 0) prev = warp ? warp_last[warp - 1] : o_prev;
-  if (e0 < len) bad |= o[0] < prev;
+  bad |= o[0] < prev;
   return __syncthreads_or(bad);
 }
 
 // ---------------------------------------------------------------------------
 // K2
 template <typename T, typename A, int UM>
-__global__ void __launch_bounds__(kTileThreads, 3) k_dv_expand(DvArgs<A> p) {
+__global__ void __launch_bounds__(kTileThreads, 4) k_dv_expand(DvArgs<A> p) {
   __shared__ __align__(16) uint4 stage[kSlotCap * 4 / 16];  // word staging (32 KB)
   __shared__ uint32_t heads[kTileThreads];
   __shared__ A warp_sums[kTileThreads / 32];
@@ -309,7 +315,6 @@ constexpr int kIpThreads = 256;
 constexpr int kIpWarps = kIpThreads / 32;
 constexpr int kQ = 512;          // queue entries per warp
 constexpr int kStepPer = 4;      // chain loads per lane per step batch
-constexpr int kScanG = 4;        // 32-index groups scanned per iteration
 constexpr int kGroup = 32;
 
 struct IpQueue {
@@ -382,6 +387,9 @@ __device__ __forceinline__ void scan_group(IpQueue& Q, int warp, int lane, uint3
   qlen += __popc(m);
 }
 
+// kScanG: 32-index groups scanned per iteration; kThresh: queued chains that
+// trigger a step pass
+template <int kScanG, int kThresh>
 __global__ void __launch_bounds__(kIpThreads) k_dv_inplace(const uint32_t* __restrict__ words,
                                                           const uint32_t* __restrict__ bitmap, int64_t n,
                                                           int32_t* __restrict__ c, int32_t* max_steps,
@@ -401,7 +409,7 @@ __global__ void __launch_bounds__(kIpThreads) k_dv_inplace(const uint32_t* __res
   uint32_t g = g0;
   // steady state: whole iterations, no bounds checks
   for (; g + kScanG <= min(g1, gfull); g += kScanG) {
-    if (qlen >= 64) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
+    if (qlen >= kThresh) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
     while (qlen > kQ - 32 * kScanG) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
     uint32_t wd[kScanG], bw[kScanG];
 #pragma unroll
@@ -632,19 +640,31 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
   if (e != cudaSuccess || stages < 3) return e;
   if (p.expand) {
-    static int occ3 = -1;
-    if (occ3 < 0) {
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_dv_inplace, kIpThreads, 0);
-      if (e != cudaSuccess) return e;
+    // PFR_IP_VARIANT (profiling aid): scan width / step-pass threshold
+    static const int variant = [] {
+      const char* v = getenv("PFR_IP_VARIANT");
+      return v ? atoi(v) : 0;
+    }();
+    auto go = [&](auto kernel) {
+      int occ3 = 0;
+      cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, kernel, kIpThreads, 0);
+      if (e2 != cudaSuccess) return e2;
       if (occ3 < 1) occ3 = 1;
+      // >= 8 groups per warp: small problems spread over many warps (the chain
+      // walks are latency bound), large ones fill the machine once (persistent)
+      const int64_t warps_needed = (p.n + 32 * 8 - 1) / (32 * 8);
+      const unsigned grid3 =
+          (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
+      return launch_pdl(kernel, dim3(grid3), dim3(kIpThreads), s, false, (const uint32_t*)p.words,
+                        (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
+    };
+    switch (variant) {
+      case 1: e = go(k_dv_inplace<8, 64>); break;
+      case 2: e = go(k_dv_inplace<4, 32>); break;
+      case 3: e = go(k_dv_inplace<2, 64>); break;
+      case 4: e = go(k_dv_inplace<8, 128>); break;
+      default: e = go(k_dv_inplace<4, 64>); break;
     }
-    // >= 8 groups per warp: small problems spread over many warps (the chain
-    // walks are latency bound), large ones fill the machine once (persistent)
-    const int64_t warps_needed = (p.n + 32 * 8 - 1) / (32 * 8);
-    const unsigned grid3 =
-        (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
-    e = launch_pdl(k_dv_inplace, dim3(grid3), dim3(kIpThreads), s, false, (const uint32_t*)p.words,
-                   (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
     if (e != cudaSuccess || stages < 4) return e;
   }
   static int occ = -1;

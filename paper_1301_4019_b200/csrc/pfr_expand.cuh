@@ -49,7 +49,7 @@ static __device__ void tile_expand(const int32_t (&o)[kTileItems], int32_t o_pre
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
     const int pv = j ? o[j - 1] : prev;
-    if (e0 + j < len && o[j] > pv) bits |= 1u << j;
+    if (o[j] > pv) bits |= 1u << j;  // padding past N repeats O = N: never a parent
   }
   const uint32_t hi = __shfl_down_sync(0xffffffffu, bits, 1);
   if ((tid & 1) == 0 && e0 < len) bitmap[(base >> 5) + (tid >> 1)] = bits | (hi << 16);
