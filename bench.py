@@ -328,7 +328,7 @@ def main():
     for parts in all_parts:
         for name, a, b in parts:
             kernel_parts.setdefault(name, []).append(a.elapsed_time(b))
-    status = int(L.status_word().item())
+    status = L.status_all()
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -250,19 +250,56 @@ def workspace(n: int) -> tuple[int, int]:
     return cur.data_ptr(), cur.numel()
 
 
-def status_word() -> torch.Tensor:
+_RING = 256  # status words per device, zeroed together
+
+
+class _StatusRing:
+    """A ring of device status words zeroed in bulk: each call takes a fresh
+    zero word, so no per-call fill kernel sits on the stream; the ring is
+    re-zeroed (one fill, ordered after every earlier user on the stream) when
+    it wraps."""
+
+    def __init__(self, dev):
+        self.words = torch.zeros(_RING, dtype=torch.int32, device=dev)
+        self.next = 0
+        self.last = self.words[0:1]
+
+    def take(self) -> torch.Tensor:
+        if self.next == _RING:
+            self.words.zero_()
+            self.next = 0
+        self.last = self.words[self.next: self.next + 1]
+        self.next += 1
+        return self.last
+
+
+_rings = threading.local()
+
+
+def _ring() -> _StatusRing:
     dev = device()
-    st = _status.get(dev.index)
-    if st is None:
-        st = torch.zeros(1, dtype=torch.int32, device=dev)
-        _status[dev.index] = st
-    return st
+    rings = getattr(_rings, "by_dev", None)
+    if rings is None:
+        rings = _rings.by_dev = {}
+    r = rings.get(dev.index)
+    if r is None:
+        r = rings[dev.index] = _StatusRing(dev)
+    return r
+
+
+def status_word() -> torch.Tensor:
+    """The status word of the most recent call on this thread and device."""
+    return _ring().last
 
 
 def new_status() -> torch.Tensor:
-    st = status_word()
-    st.zero_()
-    return st
+    return _ring().take()
+
+
+def status_all() -> int:
+    """OR of every status word handed out since the ring last wrapped."""
+    r = _ring()
+    return int(np.bitwise_or.reduce(r.words[: max(r.next, 1)].cpu().numpy())) & 0xFFFFFFFF
 
 
 def read_status(st: torch.Tensor) -> int:

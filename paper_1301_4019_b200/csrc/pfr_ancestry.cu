@@ -149,9 +149,53 @@ __global__ void k_claim(const I* __restrict__ a, int64_t n, int32_t* __restrict_
   status_or_warp(status, f);
 }
 
+// Pointer jumping (Wyllie list ranking) over the claim graph x -> d[x] by ONE
+// CTA: the rare fallback of the general permute when a walker exceeded the
+// walk bound (adversarial ancestries; realistic ones stay far below it).
+template <typename I>
+__device__ void block_pointer_jump(const I* __restrict__ a, int64_t n, const int32_t* __restrict__ d,
+                                   int32_t* __restrict__ c, int32_t* J0, int32_t* J1, int32_t* R0, int32_t* R1,
+                                   int32_t* max_steps) {
+  const int64_t stride = blockDim.x;
+  for (int64_t x = threadIdx.x; x < n; x += stride) {
+    const int64_t dx = __ldcg(d + x);
+    J0[x] = dx < n ? (int32_t)dx : (int32_t)x;
+    R0[x] = dx < n ? 1 : 0;
+  }
+  int rounds = 1;
+  while ((int64_t(1) << rounds) < n) ++rounds;
+  ++rounds;
+  int32_t *J = J0, *Jn = J1, *R = R0, *Rn = R1;
+  for (int r = 0; r < rounds; ++r) {
+    __syncthreads();
+    for (int64_t x = threadIdx.x; x < n; x += stride) {
+      const int32_t y = __ldcg(J + x);
+      Jn[x] = __ldcg(J + y);
+      Rn[x] = __ldcg(R + x) + __ldcg(R + y);
+    }
+    int32_t* t = J;
+    J = Jn;
+    Jn = t;
+    t = R;
+    R = Rn;
+    Rn = t;
+  }
+  __syncthreads();
+  int longest = 0;
+  for (int64_t i = threadIdx.x; i < n; i += stride) {
+    const int64_t v = ld_idx(a, i);
+    if (v < 0 || v >= n || __ldcg(d + v) == i) continue;  // not a loser
+    c[__ldcg(J + i)] = (int32_t)v;
+    longest = max(longest, __ldcg(R + i));
+  }
+  if (max_steps && longest) atomicMax(max_steps, longest);
+}
+
 template <typename I>
 __global__ void k_walk(const I* __restrict__ a, int64_t n, const int32_t* __restrict__ d, int32_t* __restrict__ c,
-                       int32_t* max_steps, WsHeader* hdr, uint32_t* status) {
+                       int32_t* max_steps, WsHeader* hdr, unsigned int* done, int32_t* J0, int32_t* J1, int32_t* R0,
+                       int32_t* R1, uint32_t* status) {
+  __shared__ bool last;
   int longest = 0;
   uint32_t f = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -177,6 +221,17 @@ __global__ void k_walk(const I* __restrict__ a, int64_t n, const int32_t* __rest
   }
   status_or_warp(status, f);
   if (max_steps && longest) atomicMax(max_steps, longest);
+  // the last CTA to finish runs the (rare) fallback: no extra launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (*(volatile int32_t*)&hdr->overflow == 1) block_pointer_jump<I>(a, n, d, c, J0, J1, R0, R1, max_steps);
+  if (threadIdx.x == 0) *done = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -419,18 +474,18 @@ cudaError_t launch_permute(const void* a, int64_t n, int idx_dtype, int32_t* c, 
   e = cudaMemsetAsync(ws.d, 0x7F, (size_t)n * sizeof(int32_t), s);
   if (e != cudaSuccess) return e;
   const int g = grid_for(n, 256);
+  unsigned int* done = &ws.dv->pad[0];  // zero at workspace creation; reset by the last CTA
   if (idx_dtype == PFR_I64) {
     k_claim<int64_t><<<g, 256, 0, s>>>((const int64_t*)a, n, ws.d, max_steps, status);
-    k_walk<int64_t><<<g, 256, 0, s>>>((const int64_t*)a, n, ws.d, c, max_steps, ws.hdr, status);
+    k_walk<int64_t><<<g, 256, 0, s>>>((const int64_t*)a, n, ws.d, c, max_steps, ws.hdr, done, ws.j0, ws.j1, ws.r0,
+                                      ws.r1, status);
   } else {
     k_claim<int32_t><<<g, 256, 0, s>>>((const int32_t*)a, n, ws.d, max_steps, status);
-    k_walk<int32_t><<<g, 256, 0, s>>>((const int32_t*)a, n, ws.d, c, max_steps, ws.hdr, status);
+    k_walk<int32_t><<<g, 256, 0, s>>>((const int32_t*)a, n, ws.d, c, max_steps, ws.hdr, done, ws.j0, ws.j1, ws.r0,
+                                      ws.r1, status);
   }
   note_launch(2);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  FallbackArgs fa{a, idx_dtype == PFR_I64, ws.d, n, c, ws.j0, ws.j1, ws.r0, ws.r1, max_steps, ws.hdr};
-  return launch_fallback<false>(fa, s);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_prepermute(const void* a, int64_t n, int idx_dtype, int32_t* d, uint32_t* status,

@@ -393,8 +393,8 @@ __device__ __forceinline__ void scan_group(IpQueue& Q, int warp, int lane, uint3
 
 // kScanG: 32-index groups scanned per iteration; kThresh: queued chains that
 // trigger a step pass
-template <int kScanG, int kThresh>
-__global__ void __launch_bounds__(kIpThreads) k_dv_inplace(const uint32_t* __restrict__ words,
+template <int kScanG, int kThresh, int kMinBlocks>
+__global__ void __launch_bounds__(kIpThreads, kMinBlocks) k_dv_inplace(const uint32_t* __restrict__ words,
                                                           const uint32_t* __restrict__ bitmap, int64_t n,
                                                           int32_t* __restrict__ c, int32_t* max_steps,
                                                           DvState* state, uint32_t* status) {
@@ -644,31 +644,21 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
   if (e != cudaSuccess || stages < 3) return e;
   if (p.expand) {
-    // PFR_IP_VARIANT (profiling aid): scan width / step-pass threshold
-    static const int variant = [] {
-      const char* v = getenv("PFR_IP_VARIANT");
-      return v ? atoi(v) : 0;
-    }();
-    auto go = [&](auto kernel) {
-      int occ3 = 0;
-      cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, kernel, kIpThreads, 0);
-      if (e2 != cudaSuccess) return e2;
-      if (occ3 < 1) occ3 = 1;
-      // >= 8 groups per warp: small problems spread over many warps (the chain
-      // walks are latency bound), large ones fill the machine once (persistent)
-      const int64_t warps_needed = (p.n + 32 * 8 - 1) / (32 * 8);
-      const unsigned grid3 =
-          (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
-      return launch_pdl(kernel, dim3(grid3), dim3(kIpThreads), s, false, (const uint32_t*)p.words,
-                        (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
-    };
-    switch (variant) {
-      case 1: e = go(k_dv_inplace<8, 64>); break;
-      case 2: e = go(k_dv_inplace<4, 32>); break;
-      case 3: e = go(k_dv_inplace<2, 64>); break;
-      case 4: e = go(k_dv_inplace<8, 128>); break;
-      default: e = go(k_dv_inplace<4, 64>); break;
-    }
+    // K3 tunables measured on B200 (scan width 2..8 groups, step-pass
+    // threshold 32..128, 4 vs 6 CTAs/SM): <4, 64, 4> is best; more CTAs/SM
+    // spill and lose 40%
+    auto kernel = k_dv_inplace<4, 64, 4>;
+    int occ3 = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, kernel, kIpThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (occ3 < 1) occ3 = 1;
+    // >= 8 groups per warp: small problems spread over many warps (the chain
+    // walks are latency bound), large ones fill the machine once (persistent)
+    const int64_t warps_needed = (p.n + 32 * 8 - 1) / (32 * 8);
+    const unsigned grid3 =
+        (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
+    e = launch_pdl(kernel, dim3(grid3), dim3(kIpThreads), s, false, (const uint32_t*)p.words,
+                   (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
     if (e != cudaSuccess || stages < 4) return e;
   }
   static int occ = -1;
