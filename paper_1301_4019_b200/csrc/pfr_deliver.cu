@@ -198,32 +198,38 @@ __device__ __forceinline__ A tile_excl(const DvArgs<A>& p, int64_t b) {
   return hier_of(p).tile_excl(b);
 }
 
-template <typename T, typename A>
+template <typename T, typename A, int kTilesPerCta>
 __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ uint32_t cta_flags;
   __shared__ int stage;
-  // one tile per CTA: many small CTAs in flight per SM keep HBM busy (a
-  // persistent double-buffered variant measured slower: 48 vs 30 us at 2^24)
-  const int64_t b = blockIdx.x;
-  if (threadIdx.x == 0) cta_flags = 0;
-  {
-    T x[kTileItems];
-    tile_load_any<T>((const T*)p.w, p.n, b * kTile, x);
+  // kTilesPerCta consecutive tiles per CTA, every load issued before the
+  // first reduction (launched with 1: more tiles per CTA, or a persistent
+  // double-buffered variant, measured slower)
+  const int64_t b0 = (int64_t)blockIdx.x * kTilesPerCta;
+  T x[kTilesPerCta][kTileItems];
+#pragma unroll
+  for (int t = 0; t < kTilesPerCta; ++t)
+    if (b0 + t < p.tiles) tile_load_any<T>((const T*)p.w, p.n, (b0 + t) * kTile, x[t]);
+#pragma unroll
+  for (int t = 0; t < kTilesPerCta; ++t) {
+    const int64_t b = b0 + t;
+    if (b >= p.tiles) break;  // CTA-uniform
+    if (threadIdx.x == 0) cta_flags = 0;
     FlagAcc<T> facc;
     TileScan<A> s;
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) {
-      facc.add(x[j]);
-      s.loc[j] = (A)x[j];
+      facc.add(x[t][j]);
+      s.loc[j] = (A)x[t][j];
     }
     tile_scan<A>(s, warp_sums);
     if (threadIdx.x == kTileThreads - 1) p.agg[b] = add_rn(s.thread_excl, s.loc[kTileItems - 1]);
     const uint32_t flags = __reduce_or_sync(0xffffffffu, facc.flags());
     if ((threadIdx.x & 31) == 0 && flags) atomicOr(&cta_flags, flags);
+    hier_tile_done(hier_of(p), b, &cta_flags, &stage, p.status);
+    if (stage == 2 && threadIdx.x == 0) p.state->flags = 0;  // pipeline flags of this delivery
   }
-  hier_tile_done(hier_of(p), b, &cta_flags, &stage, p.status);
-  if (stage == 2 && threadIdx.x == 0) p.state->flags = 0;  // pipeline flags of this delivery
 }
 
 // ---------------------------------------------------------------------------
@@ -630,14 +636,9 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
     return v ? atoi(v) : 4;
   }();
   const unsigned tiles = (unsigned)p.tiles;
-  static int occ1 = -1;
-  if (occ1 < 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_dv_reduce<T, A>, kTileThreads, 0);
-    if (occ1 < 1) occ1 = 1;
-  }
-  const unsigned grid1 = (unsigned)p.tiles;
-  (void)occ1;
-  k_dv_reduce<T, A><<<grid1, kTileThreads, 0, s>>>(p);
+  // one tile per CTA (2 or 4 consecutive tiles per CTA measured 29 -> 37 / 43
+  // us at 2^24: the per-tile hierarchy step is serial inside a CTA)
+  k_dv_reduce<T, A, 1><<<(unsigned)p.tiles, kTileThreads, 0, s>>>(p);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || stages < 2) return e;
