@@ -397,6 +397,81 @@ __global__ void k_multinomial_sorted(const T* __restrict__ W, int64_t n, const d
   }
 }
 
+// Merge path of the sorted uniforms U[k] = S[k]/S[N] * W[N-1] against W:
+// a[k] = min(N-1, #{j : W[j] < U[k]}) (searchsorted left, float64 compare as
+// numpy promotes, primitives.py:91-106).  CTA c owns merge diagonals
+// [c*D, (c+1)*D) of the 2N-long merge of W and U (W first on ties only when
+// strictly smaller), stages its W and U runs in shared memory, and every
+// thread merges 16 consecutive positions: O(N) coalesced work instead of N
+// binary searches.
+constexpr int kMergeD = 4096;
+
+template <typename T>
+__device__ __forceinline__ double mm_u(const double* __restrict__ S, int64_t k, double norm, double total) {
+  return S[k] / norm * total;
+}
+
+// number of W elements among the first d merge positions
+template <typename T>
+__device__ int64_t mm_split(const T* __restrict__ W, const double* __restrict__ S, int64_t n, int64_t d, double norm,
+                            double total) {
+  int64_t lo = d > n ? d - n : 0, hi = d < n ? d : n;
+  while (lo < hi) {
+    const int64_t i = (lo + hi + 1) >> 1;  // try taking i W elements: needs W[i-1] < U[d-i]
+    const int64_t jj = d - i;
+    if (jj >= n || (double)W[i - 1] < mm_u<T>(S, jj, norm, total))
+      lo = i;
+    else
+      hi = i - 1;
+  }
+  return lo;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_multinomial_merge(const T* __restrict__ W, int64_t n,
+                                                           const double* __restrict__ S, int32_t* __restrict__ out) {
+  __shared__ double sbuf[kMergeD];  // the CTA's W run, then its U run (nw + nu = D)
+  __shared__ int64_t split[2];
+  const double total = (double)W[n - 1];
+  const double norm = S[n];
+  const int64_t d0 = (int64_t)blockIdx.x * kMergeD;
+  const int64_t d1 = min(d0 + kMergeD, 2 * n);
+  if (threadIdx.x < 2) split[threadIdx.x] = mm_split<T>(W, S, n, threadIdx.x ? d1 : d0, norm, total);
+  __syncthreads();
+  const int64_t i0 = split[0], i1 = split[1];
+  const int64_t j0 = d0 - i0, j1 = d1 - i1;
+  const int nw = (int)(i1 - i0), nu = (int)(j1 - j0);
+  double* sw = sbuf;
+  double* su = sbuf + nw;
+  for (int t = threadIdx.x; t < nw; t += blockDim.x) sw[t] = (double)W[i0 + t];
+  for (int t = threadIdx.x; t < nu; t += blockDim.x) su[t] = mm_u<T>(S, j0 + t, norm, total);
+  __syncthreads();
+  // per-thread split inside the CTA's run
+  const int per = kMergeD / 256;
+  const int td = threadIdx.x * per;
+  if (td >= nw + nu) return;
+  int lo = td > nu ? td - nu : 0, hi = td < nw ? td : nw;
+  while (lo < hi) {
+    const int i = (lo + hi + 1) >> 1;
+    const int jj = td - i;
+    if (jj >= nu || sw[i - 1] < su[jj])
+      lo = i;
+    else
+      hi = i - 1;
+  }
+  int i = lo, j = td - lo;
+  const int te = min(td + per, nw + nu);
+  for (int pos = td; pos < te; ++pos) {
+    if (j >= nu || (i < nw && sw[i] < su[j])) {
+      ++i;  // a W element: strictly below the next uniform
+    } else {
+      const int64_t a = i0 + i;
+      out[j0 + j] = (int32_t)(a < n ? a : n - 1);
+      ++j;
+    }
+  }
+}
+
 // Code 4 (multinomial_ancestors_serial) with numpy draws: L_p = ln(d_p)/(N-p)
 __global__ void k_serial_logs(int64_t n, Key2x64 key, double* __restrict__ L) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
@@ -591,10 +666,11 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
     e = launch_scan(ws.f0, ws.f0, n + 1, PFR_F64, PFR_F64, PFR_ACC_F64 | PFR_SCAN_MONOTONE, 0, nullptr, -1, status,
                     ws, s);
     if (e != cudaSuccess) return e;
+    const unsigned gm = (unsigned)((2 * n + kMergeD - 1) / kMergeD);
     if (dtype == PFR_F64)
-      k_multinomial_sorted<double><<<g, 256, 0, s>>>((const double*)W, n, ws.f0, a);
+      k_multinomial_merge<double><<<gm, 256, 0, s>>>((const double*)W, n, ws.f0, a);
     else
-      k_multinomial_sorted<float><<<g, 256, 0, s>>>((const float*)W, n, ws.f0, a);
+      k_multinomial_merge<float><<<gm, 256, 0, s>>>((const float*)W, n, ws.f0, a);
     note_launch();
   }
   return cudaGetLastError();
