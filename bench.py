@@ -355,28 +355,56 @@ def main():
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
 
     # ---------------- e2e: host buffers through the public API ----------------
+    # Every delivery's weights come from pinned host memory and its ancestry
+    # goes back to pinned host memory, inside the timed region.  The copies
+    # run on a second stream and are pipelined with the resampling kernels
+    # (delivery d+1's weights upload while delivery d computes; delivery d's
+    # result downloads while d+1 computes) -- the B200-native way to feed the
+    # API; the device-only number is `value`.
     host_w = {dt: weights[dt].cpu().pin_memory() for dt in DTYPES}
-    host_c = {dt: torch.empty(n, dtype=torch.int32).pin_memory() for dt in DTYPES}
-    dev_w = {dt: torch.empty_like(weights[dt]) for dt in DTYPES}
-    h2d = d2h = 0
+    jobs = [(i, alg, j, dt) for i, alg in enumerate(ALGS) for j, dt in enumerate(DTYPES)]
+    host_c = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in jobs]
+    dev_w = [torch.empty_like(weights[dt]) for (_, _, _, dt) in jobs]
+    dev_c = [torch.empty(n, dtype=torch.int32, device=dev) for _ in jobs]
+    copy_stream = torch.cuda.Stream(device=dev)
+    h2d = sum(host_w[dt].numel() * host_w[dt].element_size() for (_, _, _, dt) in jobs)
+    d2h = len(jobs) * n * 4
     e2e_ms = 0.0
+
+    def e2e_delivery(alg, dt, w, rs, out):
+        if alg in ("systematic", "stratified"):
+            return pf.deliver(w, cfgs[alg], rs, index_dtype=torch.int32, out=out)
+        if alg == "multinomial":
+            a = pf.multinomial_ancestors(w, rs, index_dtype=torch.int32)
+        elif alg == "metropolis":
+            a = pf.metropolis_ancestors(w, B_STEPS, rs, index_dtype=torch.int32)
+        else:
+            a = pf.rejection_ancestors(w, sup[dt], rs, index_dtype=torch.int32)
+        return pf.permute_parallel(a, index_dtype=torch.int32)
+
     for s in range(args.warmup + args.steps):
+        flush.zero_()
+        copy_stream.wait_stream(stream)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        flush.zero_()
-        e0.record(stream)
-        for i, alg in enumerate(ALGS):
-            for j, dt in enumerate(DTYPES):
-                dev_w[dt].copy_(host_w[dt], non_blocking=True)
-                w_saved = weights[dt]
-                weights[dt] = dev_w[dt]
-                c = delivery(alg, dt, pf.RngStream(50_000 + s, (rank, i, j)))
-                weights[dt] = w_saved
-                host_c[dt].copy_(c, non_blocking=True)
-                if s == args.warmup:
-                    h2d += dev_w[dt].numel() * dev_w[dt].element_size()
-                    d2h += c.numel() * c.element_size()
-        e1.record(stream)
+        e0.record(copy_stream)
+        up = []
+        for k, (i, alg, j, dt) in enumerate(jobs):
+            with torch.cuda.stream(copy_stream):
+                dev_w[k].copy_(host_w[dt], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_stream)
+            up.append(ev)
+        for k, (i, alg, j, dt) in enumerate(jobs):
+            stream.wait_event(up[k])
+            c = e2e_delivery(alg, dt, dev_w[k], pf.RngStream(50_000 + s, (rank, i, j)), dev_c[k])
+            done = torch.cuda.Event()
+            done.record(stream)
+            c.record_stream(copy_stream)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(done)
+                host_c[k].copy_(c, non_blocking=True)
+        e1.record(copy_stream)
         torch.cuda.synchronize()
         if s >= args.warmup:
             e2e_ms += e0.elapsed_time(e1)
