@@ -350,6 +350,14 @@ def main():
             if m > dom_ms:
                 dom_name, dom_ms = name, m
     alg, dt = dom_name.split("/")
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            tr = json.load(fh)
+        if n == N_DEFAULT and dom_name in tr:
+            traffic = float(tr[dom_name]["bytes"])
+    except Exception:
+        pass
     s_bytes = 4 if dt == "f32" else 8
     alg_bytes = algorithmic_bytes(alg, s_bytes, n, trips[dt])
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
@@ -451,8 +459,12 @@ def main():
             "data": "synthetic i.i.d. log-normal weights (sigma=1), resident in HBM",
             "config": workload_config(n, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "kernel": dom_name,
-                         "algorithmic_bytes": alg_bytes, "kernel_ms": dom_ms, "peak_source": peak_src},
+                         "frac": achieved / hbm, "traffic": traffic, "kernel": dom_name,
+                         "algorithmic_bytes": alg_bytes, "kernel_ms": dom_ms, "peak_source": peak_src,
+                         "traffic_source": "profiles/r01_traffic.json (ncu --set full, per launch)",
+                         "note": "algorithmic bytes count every proposal's weight gather (SURVEY 8(d)); the "
+                                 "gathers hit L2 (N=2^20 weights are L2 resident): the kernel is bound by the "
+                                 "L2 random-sector rate and Philox issue, not by HBM (DESIGN.md 3.3-3.4)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "particles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
