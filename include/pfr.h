@@ -272,6 +272,23 @@ int pfr_shard_advance(const int32_t* walkers, int64_t count, const uint32_t* wor
 int pfr_shard_scatter(const int32_t* done, int64_t count, int64_t index_base, int64_t n_loc, int32_t* c,
                       uint32_t* status, void* stream);
 
+/* ---- remaining reference functions around the step ----------------------- */
+
+/* permute_serial (ancestry.py:104-122, PAPER Code 11): the serial pairwise
+ * swaps, run by one device thread (inherently sequential; API parity). */
+int pfr_permute_serial(const void* a, int64_t n, int idx_dtype, int32_t* c, uint32_t* status, void* stream);
+
+/* stable_sum (primitives.py:69-88): balanced pairwise tree over the
+ * zero-padded power-of-two vector, bit-identical to the reference;
+ * *result (device double). */
+int pfr_stable_sum(const void* w, int64_t n, int dtype, double* result, void* ws, size_t ws_bytes, void* stream);
+
+/* ess (diagnostics.py:54-63) and resampling_mse (diagnostics.py:66-80) in one
+ * deterministic pass: out[4] (device) = {sum w, sum w^2, ESS, MSE}; MSE = 0
+ * when o (offspring counts) is NULL. */
+int pfr_weight_stats(const void* w, int64_t n, int dtype, const void* o, int idx_dtype, double* out, void* ws,
+                     size_t ws_bytes, void* stream);
+
 /* ---- batches of independent filters -----------
  * No communication: one CTA per filter.  Arrays are [filters, n] row-major. */
 

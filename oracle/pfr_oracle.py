@@ -156,6 +156,34 @@ def exclusive_scan(w) -> np.ndarray:
     return out
 
 
+def stable_sum(w):
+    """Balanced pairwise tree over the zero-padded power-of-two vector
+    (primitives.py:69-88)."""
+    w = np.asarray(w)
+    n = w.size
+    size = 1 << (n - 1).bit_length()
+    v = np.zeros(size, dtype=w.dtype)
+    v[:n] = w
+    while v.size > 1:
+        v = v[0::2] + v[1::2]
+    return v[0]
+
+
+def ess(w) -> float:
+    """(sum w)^2 / (w . w) (diagnostics.py:54-63)."""
+    w = as_weights(w)
+    total = w.sum(dtype=w.dtype)
+    return float(total * total / np.dot(w, w))
+
+
+def resampling_mse(o, w) -> float:
+    """(1/N) sum (o/N - w/sum w)^2 in float64 (diagnostics.py:66-80)."""
+    o = np.asarray(o, dtype=np.float64)
+    w = as_weights(w).astype(np.float64)
+    diff = o / w.size - w / w.sum()
+    return float(np.mean(diff * diff))
+
+
 def adjacent_difference(W) -> np.ndarray:
     """primitives.py:54-57."""
     W = np.asarray(W)

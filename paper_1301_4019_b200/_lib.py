@@ -92,6 +92,9 @@ _SIGNATURES = {
     "pfr_deliver_batched": ([_P, _I64, _I64, _INT, _P, _RNGP, _P, _P, _P, _P, _SZ, _P], _INT),
     "pfr_pf_workspace_bytes": ([_I64, _I64], _SZ),
     "pfr_pf_run": ([_P, _P, _I64, _I64, _I64, _DBL, _RNGP, _P, _P, _P, _P, _P, _P, _SZ, _P], _INT),
+    "pfr_permute_serial": ([_P, _I64, _INT, _P, _P, _P], _INT),
+    "pfr_stable_sum": ([_P, _I64, _INT, _P, _P, _SZ, _P], _INT),
+    "pfr_weight_stats": ([_P, _I64, _INT, _P, _INT, _P, _P, _SZ, _P], _INT),
 }
 
 _lib = None

@@ -22,6 +22,7 @@ __all__ = [
     "prepermute",
     "permute_parallel",
     "permute_cumulative",
+    "permute_serial",
     "satisfies_inplace_predicate",
     "copy_particles",
 ]
@@ -148,6 +149,20 @@ def permute_cumulative(O, return_max_steps: bool = False, *, index_dtype=None):
     if return_max_steps:
         return c, int(steps.item())
     return c
+
+
+def permute_serial(a, *, index_dtype=None) -> torch.Tensor:
+    """Serial pairwise-swap permutation (ancestry.py:104-122, PAPER Code 11)
+    satisfying the in-place predicate; run by one device thread (the
+    algorithm is inherently sequential -- permute_parallel is the
+    production permutation; the two may differ element-wise)."""
+    a = _idx(a, "ancestry vector")
+    n = a.numel()
+    c = torch.empty(n, dtype=torch.int32, device=a.device)
+    st = L.new_status()
+    L.call("pfr_permute_serial", a.data_ptr(), n, L.dtype_code(a), c.data_ptr(), st.data_ptr(), L.stream_handle())
+    _finish_index(st, n)
+    return L.to_index_dtype(c, index_dtype)
 
 
 def copy_particles(x: torch.Tensor, c) -> torch.Tensor:

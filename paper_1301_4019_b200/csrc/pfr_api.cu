@@ -470,4 +470,32 @@ int pfr_pf_run(const pfr_pf_model* model, const double* y, int64_t filters, int6
                    "pfr_pf_run");
   return PFR_OK;
 }
+
+/* ---- remaining reference functions (pfr_misc.cu) ------------------------- */
+
+int pfr_permute_serial(const void* a, int64_t n, int idx_dtype, int32_t* c, uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n) && a && c, "bad arguments");
+  PFR_REQUIRE(is_index(idx_dtype), "ancestry must be int32 or int64");
+  PFR_CHECK_LAUNCH(launch_permute_serial(a, n, idx_dtype, c, status, (cudaStream_t)stream), "pfr_permute_serial");
+  return PFR_OK;
+}
+
+int pfr_stable_sum(const void* w, int64_t n, int dtype, double* result, void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && result, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "stable_sum needs float32 or float64");
+  PFR_WS(PFR_OP_ANY);
+  PFR_CHECK_LAUNCH(launch_stable_sum(w, n, dtype, result, ws.f0, (cudaStream_t)stream), "pfr_stable_sum");
+  return PFR_OK;
+}
+
+int pfr_weight_stats(const void* w, int64_t n, int dtype, const void* o, int idx_dtype, double* out, void* ws_ptr,
+                     size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && out, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(!o || is_index(idx_dtype), "offspring must be int32 or int64");
+  PFR_WS(PFR_OP_ANY);
+  PFR_CHECK_LAUNCH(launch_weight_stats(w, n, dtype, o, idx_dtype, out, ws.f0, (cudaStream_t)stream),
+                   "pfr_weight_stats");
+  return PFR_OK;
+}
 }  // extern "C"

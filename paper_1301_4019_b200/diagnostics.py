@@ -13,7 +13,7 @@ import torch
 
 from . import _lib as L
 
-__all__ = ["check_weights", "logweights_to_weights", "ess"]
+__all__ = ["check_weights", "logweights_to_weights", "ess", "resampling_mse"]
 
 
 def check_weights(w, require_positive_total: bool = True, name: str = "w") -> torch.Tensor:
@@ -43,8 +43,26 @@ def logweights_to_weights(lw) -> torch.Tensor:
     return w
 
 
+def _weight_stats(w, o=None):
+    out = torch.empty(4, dtype=torch.float64, device=w.device)
+    ws, wsb = L.workspace(w.numel())
+    L.call("pfr_weight_stats", w.data_ptr(), w.numel(), L.dtype_code(w), L.ptr(o),
+           L.dtype_code(o) if o is not None else L.I32, out.data_ptr(), ws, wsb, L.stream_handle())
+    return out.cpu().numpy()
+
+
 def ess(w) -> float:
-    """Effective sample size (sum w)^2 / (w . w) (diagnostics.py:54-63)."""
+    """Effective sample size (sum w)^2 / (w . w) (diagnostics.py:54-63): one
+    deterministic device pass (pfr_weight_stats)."""
     w = check_weights(w)
-    total = w.sum()
-    return float(total * total / torch.dot(w, w))
+    return float(_weight_stats(w)[2])
+
+
+def resampling_mse(o, w) -> float:
+    """(1/N) sum_i (o[i]/N - w[i]/sum w)^2 in float64 (diagnostics.py:66-80),
+    fused with the weight sums in one device pass."""
+    w = check_weights(w)
+    o = L.as_index(o, "offspring vector")
+    if o.numel() != w.numel():
+        raise ValueError(f"offspring and weight vectors differ in length: ({o.numel()},) vs ({w.numel()},)")
+    return float(_weight_stats(w, o)[3])

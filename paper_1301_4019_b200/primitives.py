@@ -9,11 +9,13 @@ every run and every launch geometry returns the same bits.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _lib as L
 
 __all__ = [
+    "stable_sum",
     "inclusive_prefix_sum",
     "exclusive_prefix_sum",
     "adjacent_difference",
@@ -85,3 +87,19 @@ def lower_bound(W, u, *, index_dtype=None):
            L.stream_handle())
     out = L.to_index_dtype(out, index_dtype)
     return out[0] if scalar else out
+
+
+def stable_sum(w):
+    """Balanced pairwise-tree sum of the zero-padded power-of-two vector
+    (primitives.py:69-88), bit-identical to the reference; returns a numpy
+    scalar of the input dtype."""
+    w = L.as_weights(w, "vector")
+    out = torch.empty(1, dtype=torch.float64, device=w.device)
+    ws, wsb = L.workspace(w.numel())
+    st = L.new_status()
+    L.call("pfr_check_weights", w.data_ptr(), w.numel(), L.dtype_code(w), st.data_ptr(), L.stream_handle())
+    L.call("pfr_stable_sum", w.data_ptr(), w.numel(), L.dtype_code(w), out.data_ptr(), ws, wsb, L.stream_handle())
+    if L.read_status(st) & L.ST_NONFINITE:
+        raise ValueError("vector must be finite (no NaN or infinity)")
+    t = np.float32 if w.dtype == torch.float32 else np.float64
+    return t(float(out.item()))

@@ -58,6 +58,16 @@ WEIGHT_CASES = [
 
 ANCESTRY_CASES = [(1, 21), (2, 22), (3, 23), (7, 24), (100, 25), (257, 26), (4096, 27)]
 
+# (n, dtype) of the stable_sum fixtures; vectors regenerated from their index
+STABLE_CASES = [(1, np.float64), (5, np.float32), (4096, np.float64), (4097, np.float32), (100000, np.float64),
+                (1 << 20, np.float32)]
+
+
+def stable_vector(k: int) -> np.ndarray:
+    n, dt = STABLE_CASES[k]
+    g = np.random.default_rng(600 + k)
+    return (g.random(n) * np.exp(g.normal(0, 4, n))).astype(dt)
+
 
 def main():
     sys.path.insert(0, REF_SRC)
@@ -136,6 +146,20 @@ def main():
     out["stream/u2"] = gen.random(8)
     out["stream/derive"] = np.array([pf.derive_seed(4242, 0, 1, 2, 3), pf.derive_seed(4242, 1, 1, 2, 3),
                                      pf.derive_seed(0), pf.derive_seed(2**64 - 1, 5)], dtype=np.uint64)
+
+    # stable_sum (pairwise tree), ESS and resampling MSE (diagnostics.py:54-80)
+    for k, (n, dt) in enumerate(STABLE_CASES):
+        v = stable_vector(k)
+        out[f"stable/{k}/checksum"] = np.float64(v.astype(np.float64).sum())
+        out[f"stable/{k}/sum"] = np.asarray(pf.stable_sum(v))
+    for k, n in enumerate((16, 1000, 4097)):
+        g = np.random.default_rng(700 + k)
+        w = np.exp(g.normal(0, 1, n))
+        o = np.bincount(g.integers(0, n, n), minlength=n)
+        out[f"wstats/{k}/w"] = w
+        out[f"wstats/{k}/o"] = o.astype(np.int64)
+        out[f"wstats/{k}/ess"] = np.float64(pf.ess(w))
+        out[f"wstats/{k}/mse"] = np.float64(pf.resampling_mse(o, w))
 
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
