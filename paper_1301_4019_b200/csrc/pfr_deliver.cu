@@ -44,7 +44,7 @@ namespace pfr {
 
 namespace {
 
-constexpr int kBackBound = 64;
+constexpr int kBackBound = 255;  // chain steps walked by K3 before the pointer-jumping fallback (fits the queue's uint8)
 
 constexpr uint32_t kNeedsRepair = 1u;
 constexpr uint32_t kOverflow = 2u;
