@@ -172,6 +172,8 @@ struct PfArgs {
   uint32_t* bitmap;     // [M, bitmap_stride]
   int64_t bitmap_stride;
   uint8_t* need;        // [M] resample at the next step
+  double* part;         // [M, kPfSlices, 4] slice partials
+  unsigned int* slice_done;  // [M] slices finished (reset by the last)
   double* means;        // [M, T]
   double* loglik;       // [M]
   double* ess;          // [M, T]
@@ -225,10 +227,15 @@ __global__ void __launch_bounds__(kTileThreads) k_pf_resample(PfArgs a, int64_t 
 }
 
 // propagate (through the ancestry when resampled) + weight + per-filter
-// reductions; one CTA per filter, deterministic reduction order
+// reductions.  Grid (slices, M): kPfSlices CTAs per filter each reduce their
+// contiguous slice; the last slice to finish (per-filter counter) folds the
+// slice partials in slice order (deterministic) and finishes the filter.
+constexpr int kPfSlices = 8;
+
 __global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
   __shared__ double red[4][8];
-  const int64_t m = blockIdx.x;
+  __shared__ bool last;
+  const int64_t m = blockIdx.y;
   const int64_t n = a.N;
   const bool res = a.need[m] != 0;
   const double* src = ((t & 1) ? a.x1 : a.x0) + m * n;
@@ -238,9 +245,13 @@ __global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
   const double y = a.y[m * a.T + t];
   const double inv_obs = 1.0 / a.obs_std;
   const double dens_norm = inv_obs * 0.3989422804014327;  // 1 / (obs_std sqrt(2 pi))
+  // this slice: pairs [p0, p1) of the filter
+  const int64_t pairs = (n + 1) / 2;
+  const int64_t p0 = pairs * blockIdx.x / gridDim.x, p1 = pairs * (blockIdx.x + 1) / gridDim.x;
   double su = 0.0, sux = 0.0, suu = 0.0, sw = 0.0;
-  for (int64_t i = 2 * threadIdx.x; i < n; i += 2 * blockDim.x) {
-    const float2 z = normal2((uint32_t)(i >> 1), (uint32_t)m, (uint32_t)t, kTagPfProp, a.k0, a.k1);
+  for (int64_t pp = p0 + threadIdx.x; pp < p1; pp += blockDim.x) {
+    const int64_t i = 2 * pp;
+    const float2 z = normal2((uint32_t)pp, (uint32_t)m, (uint32_t)t, kTagPfProp, a.k0, a.k1);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int64_t k = i + h;
@@ -269,20 +280,32 @@ __global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
     for (int q = 0; q < 4; ++q) red[q][threadIdx.x >> 5] = v[q];
   __syncthreads();
   if (threadIdx.x == 0) {
-    double r[4] = {0, 0, 0, 0};
-    for (int q = 0; q < 4; ++q)
-      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r[q] += red[q][k];
-    const double total = r[0] / r[3];  // sum of normalised weights x density
-    if (!(total > 0.0) || !isfinite(total)) {
-      status_or(a.status, PFR_ST_NOPROGRESS);  // weight collapse (pf.py:193-198)
-    } else {
-      a.loglik[m] += log(total);
+    double* part = a.part + (m * kPfSlices + blockIdx.x) * 4;
+    for (int q = 0; q < 4; ++q) {
+      double r = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r += red[q][k];
+      part[q] = r;
     }
-    a.means[m * a.T + t] = r[1] / r[0];
-    const double ess_next = r[0] * r[0] / r[2];
-    if (t + 1 < a.T) a.ess[m * a.T + t + 1] = ess_next;
-    a.need[m] = (ess_next / (double)n < a.ess_threshold) ? 1 : 0;
+    __threadfence();
+    last = atomicAdd(&a.slice_done[m], 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double r[4] = {0, 0, 0, 0};
+  for (int sl = 0; sl < (int)gridDim.x; ++sl)
+    for (int q = 0; q < 4; ++q) r[q] += __ldcg(a.part + (m * kPfSlices + sl) * 4 + q);
+  a.slice_done[m] = 0;
+  const double total = r[0] / r[3];  // sum of normalised weights x density
+  if (!(total > 0.0) || !isfinite(total)) {
+    status_or(a.status, PFR_ST_NOPROGRESS);  // weight collapse (pf.py:193-198)
+  } else {
+    a.loglik[m] += log(total);
+  }
+  a.means[m * a.T + t] = r[1] / r[0];
+  const double ess_next = r[0] * r[0] / r[2];
+  if (t + 1 < a.T) a.ess[m * a.T + t + 1] = ess_next;
+  a.need[m] = (ess_next / (double)n < a.ess_threshold) ? 1 : 0;
 }
 
 }  // namespace
@@ -299,6 +322,8 @@ size_t pf_workspace_bytes(int64_t M, int64_t N) {
   add(mn * 4 + 16);     // words
   add(M * bstride * 4); // bitmap
   add(M);               // need
+  add(M * 8 * 4 * 8);   // slice partials
+  add(M * 4);           // slice counters
   return b;
 }
 
@@ -362,6 +387,8 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   a.bitmap_stride = (N + 31) / 32 + 4;
   a.bitmap = reinterpret_cast<uint32_t*>(take(M * a.bitmap_stride * 4));
   a.need = reinterpret_cast<uint8_t*>(take(M));
+  a.part = reinterpret_cast<double*>(take(M * 8 * 4 * 8));
+  a.slice_done = reinterpret_cast<unsigned int*>(take(M * 4));
   a.means = means;
   a.loglik = loglik;
   a.ess = ess;
@@ -371,6 +398,8 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   a.status = status;
   // ESS at t = 0: uniform weights
   cudaError_t e = cudaMemsetAsync(ess, 0, sizeof(double) * M * T, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(a.slice_done, 0, sizeof(unsigned int) * M, s);
   if (e != cudaSuccess) return e;
   const unsigned g0 = (unsigned)std::min<int64_t>((mn / 2 + 255) / 256 + 1, (int64_t)num_sms() * 16);
   k_pf_init<<<g0, 256, 0, s>>>(a);
@@ -384,7 +413,7 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
       e = cudaMemsetAsync(resampled, 0, M * T, s);
       if (e != cudaSuccess) return e;
     }
-    k_pf_step<<<(unsigned)M, 256, 0, s>>>(a, t);
+    k_pf_step<<<dim3(kPfSlices, (unsigned)M), 256, 0, s>>>(a, t);
     note_launch();
   }
   return cudaGetLastError();
