@@ -20,6 +20,7 @@
 // words (pfr_expand.cuh); pass 3 resolves the in-place ancestry by walking
 // the loser chains backwards (as k_dv_inplace).  Words live in a per-filter
 // global scratch (L2-resident for N <= 2^16).
+#include <cstdlib>
 #include <algorithm>
 
 #include "pfr_expand.cuh"
@@ -54,9 +55,9 @@ __device__ __forceinline__ double philox_unit53(uint32_t c0, uint32_t c1, uint32
 // Systematic delivery of one filter of n particles (all threads of the CTA).
 // u: the shared offset (already cast to the weight dtype).  Returns the
 // longest chain walk in `longest` (per thread).
-template <typename T>
+template <typename T, bool kResolve = true>
 __device__ void segment_deliver(const T* __restrict__ w, int64_t n, double u, uint32_t* words, uint32_t* bitmap,
-                                int32_t* __restrict__ c, int& longest, SegSmem& S) {
+                                int32_t* __restrict__ c, int& longest, SegSmem& S, uint32_t pidx_offset = 0) {
   const int64_t tiles = num_tiles(n);
   // pass 1: total W_N = serial fold of the tile aggregates
   double total = 0.0;
@@ -108,7 +109,8 @@ __device__ void segment_deliver(const T* __restrict__ w, int64_t n, double u, ui
       rr = max(rr, (int64_t)o[j]);
       o[j] = (int32_t)rr;  // maximum.accumulate (resamplers.py:150)
     }
-    tile_expand(o, o_prev, b, n, words, bitmap, reinterpret_cast<uint32_t*>(S.stage), S.heads, S.warp_last);
+    tile_expand(o, o_prev, b, n, words, bitmap, reinterpret_cast<uint32_t*>(S.stage), S.heads, S.warp_last,
+                pidx_offset);
     if (threadIdx.x == kTileThreads - 1) {
       S.bcast = __dadd_rn(s.thread_excl, s.loc[kTileItems - 1]);
       S.bcast_i = o[kTileItems - 1];
@@ -120,6 +122,7 @@ __device__ void segment_deliver(const T* __restrict__ w, int64_t n, double u, ui
     __syncthreads();
   }
   __syncthreads();
+  if constexpr (!kResolve) return;  // the caller runs the in-place pass
   // pass 3: in-place ancestry (backward chain walks)
   for (int64_t i = threadIdx.x; i < n; i += kTileThreads) {
     const bool has = (__ldcg(bitmap + (i >> 5)) >> (i & 31)) & 1u;
@@ -172,6 +175,8 @@ struct PfArgs {
   uint32_t* bitmap;     // [M, bitmap_stride]
   int64_t bitmap_stride;
   uint8_t* need;        // [M] resample at the next step
+  DvState* dv;          // K3 state (overflow flag)
+  int c_global;          // c holds global particle numbers (global in-place pass)
   double* part;         // [M, kPfSlices, 4] slice partials
   unsigned int* slice_done;  // [M] slices finished (reset by the last)
   double* means;        // [M, T]
@@ -211,18 +216,51 @@ __global__ void __launch_bounds__(256) k_pf_init(PfArgs a) {
   }
 }
 
-// resampling of the filters whose ESS fell below the threshold
+// resampling of the filters whose ESS fell below the threshold: passes 1-2
+// of the delivery per filter CTA (slot words with GLOBAL parent numbers into a
+// contiguous bitmap: N % 32 == 0), then one global in-place pass (K3 of the
+// fused delivery, launch_dv_inplace) resolves every filter's chains at once
+// (chains never leave a filter: its slots only name its own parents).  Other
+// N: the per-CTA pass 3.  c holds global particle numbers.
+template <bool kGlobal>
 __global__ void __launch_bounds__(kTileThreads) k_pf_resample(PfArgs a, int64_t t) {
   __shared__ SegSmem S;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.dv->flags = 0;  // K3 overflow flag of the previous step
   for (int64_t m = blockIdx.x; m < a.M; m += gridDim.x) {
     const bool go = a.need[m] != 0;
     if (threadIdx.x == 0) a.resampled[m * a.T + t] = go ? 1 : 0;
     if (!go) continue;
     const double u = philox_unit53((uint32_t)m, (uint32_t)t, kTagPfSys, a.k0, a.k1);
     int longest = 0;
-    segment_deliver<double>(a.w + m * a.N, a.N, u, a.words + m * a.N, a.bitmap + m * a.bitmap_stride,
-                            a.c + m * a.N, longest, S);
+    if constexpr (kGlobal) {
+      segment_deliver<double, false>(a.w + m * a.N, a.N, u, a.words + m * a.N, a.bitmap + m * (a.N / 32), nullptr,
+                                     longest, S, (uint32_t)(m * a.N));
+    } else {
+      segment_deliver<double, true>(a.w + m * a.N, a.N, u, a.words + m * a.N, a.bitmap + m * a.bitmap_stride,
+                                    a.c + m * a.N, longest, S);
+    }
     __syncthreads();
+  }
+}
+
+// rare: a chain longer than K3's walk bound -- redo the in-place pass of the
+// resampled filters with unbounded per-thread walks (global numbers)
+__global__ void __launch_bounds__(kTileThreads) k_pf_fixup(PfArgs a, int force) {
+  if (!force && !(*(volatile unsigned*)&a.dv->flags & 2u)) return;
+  for (int64_t m = blockIdx.x; m < a.M; m += gridDim.x) {
+    if (!a.need[m]) continue;
+    const uint32_t* bitmap = a.bitmap + m * (a.N / 32);
+    const int64_t base = m * a.N;
+    for (int64_t i = threadIdx.x; i < a.N; i += blockDim.x) {
+      if ((__ldcg(bitmap + (i >> 5)) >> (i & 31)) & 1u) {
+        a.c[base + i] = (int32_t)(base + i);
+        continue;
+      }
+      uint32_t wd = __ldcg(a.words + base + i);
+      int64_t st = 0;
+      while ((wd & kFirst) && st++ <= a.N) wd = __ldcg(a.words + (wd & kParentMask));
+      a.c[base + i] = (int32_t)(wd & kParentMask);
+    }
   }
 }
 
@@ -242,6 +280,7 @@ __global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
   double* dst = ((t & 1) ? a.x0 : a.x1) + m * n;
   double* w = a.w + m * n;
   const int32_t* cm = a.c + m * n;
+  const int64_t c_base = a.c_global ? m * n : 0;
   const double y = a.y[m * a.T + t];
   const double inv_obs = 1.0 / a.obs_std;
   const double dens_norm = inv_obs * 0.3989422804014327;  // 1 / (obs_std sqrt(2 pi))
@@ -256,7 +295,7 @@ __global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
     for (int h = 0; h < 2; ++h) {
       const int64_t k = i + h;
       if (k >= n) break;
-      const double xo = res ? src[cm[k]] : src[k];
+      const double xo = res ? src[cm[k] - c_base] : src[k];
       const double wp = (res || t == 0) ? 1.0 : w[k];
       const double xn = a.coeff * xo + a.trans_std * (double)(h ? z.y : z.x);
       const double e = (y - xn) * inv_obs;
@@ -324,6 +363,7 @@ size_t pf_workspace_bytes(int64_t M, int64_t N) {
   add(M);               // need
   add(M * 8 * 4 * 8);   // slice partials
   add(M * 4);           // slice counters
+  add(sizeof(DvState)); // K3 state
   return b;
 }
 
@@ -389,6 +429,7 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   a.need = reinterpret_cast<uint8_t*>(take(M));
   a.part = reinterpret_cast<double*>(take(M * 8 * 4 * 8));
   a.slice_done = reinterpret_cast<unsigned int*>(take(M * 4));
+  a.dv = reinterpret_cast<DvState*>(take(sizeof(DvState)));
   a.means = means;
   a.loglik = loglik;
   a.ess = ess;
@@ -401,14 +442,37 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(a.slice_done, 0, sizeof(unsigned int) * M, s);
   if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(a.dv, 0, sizeof(DvState), s);
+  if (e != cudaSuccess) return e;
+  // stale slot words of filters that did not resample stay valid particle
+  // numbers for the global in-place pass
+  e = cudaMemsetAsync(a.words, 0, (size_t)mn * 4, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(a.bitmap, 0, (size_t)M * a.bitmap_stride * 4, s);
+  if (e != cudaSuccess) return e;
+  // PFR_PF_PATH (test knob): 0 global in-place pass (default), 1 per-filter
+  // pass 3, 2 global pass followed by the unbounded fixup pass
+  int path = 0;
+  if (const char* v = getenv("PFR_PF_PATH")) path = atoi(v);
+  const bool global_pass = (N % 32) == 0 && path != 1;
+  a.c_global = global_pass ? 1 : 0;
   const unsigned g0 = (unsigned)std::min<int64_t>((mn / 2 + 255) / 256 + 1, (int64_t)num_sms() * 16);
   k_pf_init<<<g0, 256, 0, s>>>(a);
   note_launch();
   const unsigned gr = (unsigned)std::min<int64_t>(M, (int64_t)num_sms() * 8);
   for (int64_t t = 0; t < T; ++t) {
     if (t > 0) {
-      k_pf_resample<<<gr, kTileThreads, 0, s>>>(a, t);
-      note_launch();
+      if (global_pass) {
+        k_pf_resample<true><<<gr, kTileThreads, 0, s>>>(a, t);
+        note_launch();
+        e = launch_dv_inplace(a.words, a.bitmap, mn, a.c, a.dv, status, s);
+        if (e != cudaSuccess) return e;
+        k_pf_fixup<<<gr, kTileThreads, 0, s>>>(a, path == 2);
+        note_launch();
+      } else {
+        k_pf_resample<false><<<gr, kTileThreads, 0, s>>>(a, t);
+        note_launch();
+      }
     } else {
       e = cudaMemsetAsync(resampled, 0, M * T, s);
       if (e != cudaSuccess) return e;

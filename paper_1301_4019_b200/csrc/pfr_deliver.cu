@@ -716,6 +716,24 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
 
 }  // namespace
 
+// K3 on its own, for callers that wrote slot words and the has-offspring
+// bitmap themselves (the batched filter: global parent numbers, so one pass
+// serves every filter).  Sets kOverflow in state->flags when a chain exceeds
+// the walk bound (the caller owns the fallback).
+cudaError_t launch_dv_inplace(const uint32_t* words, const uint32_t* bitmap, int64_t n, int32_t* c, DvState* state,
+                              uint32_t* status, cudaStream_t s) {
+  auto kernel = k_dv_inplace<4, 64, 4>;
+  int occ3 = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, kernel, kIpThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (occ3 < 1) occ3 = 1;
+  const int64_t warps_needed = (n + 32 * 8 - 1) / (32 * 8);
+  const unsigned grid3 =
+      (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
+  return launch_pdl(kernel, dim3(grid3), dim3(kIpThreads), s, false, words, bitmap, n, c, (int32_t*)nullptr, state,
+                    status);
+}
+
 // systematic_/stratified_cumulative_offspring (resamplers.py:105-153): the
 // delivery's K1 + K2 with O stored and no expansion (rare path repairs O)
 cudaError_t launch_offspring(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,

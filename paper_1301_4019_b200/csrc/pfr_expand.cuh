@@ -32,14 +32,16 @@ constexpr int kSlotsPerThread = kSlotCap / kTileThreads;  // 32
 // slot) and a running carry across chunks.  The chunk is written out with
 // coalesced 16-byte stores (positions are shifted so that global vectors are
 // aligned; partial edge vectors are written element-wise).
+// `pidx_offset` is added to every parent index written (a batched filter
+// writes global parent numbers so one in-place pass can serve the batch).
 static __device__ void tile_expand(const int32_t (&o)[kTileItems], int32_t o_prev, int64_t b, int64_t n, uint32_t* words,
                             uint32_t* bitmap, uint32_t* sbuf /* kSlotCap words */, uint32_t* heads /* 256 */,
-                            int32_t* warp_last /* 8 */) {
+                            int32_t* warp_last /* 8 */, uint32_t pidx_offset = 0) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t base = b * kTile;
   const int len = (int)min((int64_t)kTile, n - base);
   const int e0 = tid * kTileItems;
-  const uint32_t pbase = (uint32_t)base + (uint32_t)e0;
+  const uint32_t pbase = (uint32_t)base + (uint32_t)e0 + pidx_offset;
   // O of the element before this thread's first parent
   int prev = __shfl_up_sync(0xffffffffu, o[kTileItems - 1], 1);
   if (lane == 31) warp_last[warp] = o[kTileItems - 1];

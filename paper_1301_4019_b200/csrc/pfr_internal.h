@@ -113,6 +113,9 @@ cudaError_t launch_shard_advance(const int32_t* walkers, int64_t count, const ui
 cudaError_t launch_shard_scatter(const int32_t* done, int64_t count, int64_t index_base, int64_t n_loc, int32_t* c,
                                  uint32_t* status, cudaStream_t s);
 
+cudaError_t launch_dv_inplace(const uint32_t* words, const uint32_t* bitmap, int64_t n, int32_t* c, DvState* state,
+                              uint32_t* status, cudaStream_t s);
+
 // launchers (pfr_batch.cu): batches of independent filters
 size_t batched_workspace_bytes(int64_t M, int64_t N);
 size_t pf_workspace_bytes(int64_t M, int64_t N);

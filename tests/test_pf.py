@@ -108,3 +108,25 @@ def test_batched_filter_independent_observations_and_threshold():
     assert res1.resampled[:, 1:].all()
     for m in range(8):
         assert abs(res1.log_likelihood[m] - exact_filter(model, ys[m]).log_likelihood) < 3.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("obs_std", [0.8, 0.02])
+def test_batched_filter_inplace_paths_agree(monkeypatch, obs_std):
+    """The global in-place pass, its unbounded fixup and the per-filter pass 3
+    resolve the same ancestry, so the filters agree bit for bit (obs_std 0.02:
+    degenerate weights, long chains)."""
+    import paper_1301_4019_b200 as pf
+
+    model = LinearGaussianModel(coeff=0.9, trans_std=1.0, obs_std=obs_std)
+    ys = np.stack([simulate_observations(model, 12, s) for s in range(24)])
+    out = []
+    for path in ("0", "1", "2"):
+        monkeypatch.setenv("PFR_PF_PATH", path)
+        r = pf.pf_run(model, ys, 8192, ess_threshold=0.7, seed=5)
+        out.append(r)
+    assert out[0].resampled[:, 1:].any()
+    for r in out[1:]:
+        np.testing.assert_array_equal(r.filtered_means, out[0].filtered_means)
+        np.testing.assert_array_equal(r.log_likelihood, out[0].log_likelihood)
+        np.testing.assert_array_equal(r.ess, out[0].ess)
