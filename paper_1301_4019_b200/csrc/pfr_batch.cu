@@ -177,8 +177,12 @@ struct PfArgs {
   uint8_t* need;        // [M] resample at the next step
   DvState* dv;          // K3 state (overflow flag)
   int c_global;          // c holds global particle numbers (global in-place pass)
-  double* part;         // [M, kPfSlices, 4] slice partials
-  unsigned int* slice_done;  // [M] slices finished (reset by the last)
+  int64_t tiles;         // tiles per filter
+  double* agg;          // [M, tiles] tile aggregates of w
+  double* excl;         // [M, tiles + 1] exclusive tile prefixes, total
+  uint8_t* repair;      // [M] filter needs the running-max repair
+  double* part;         // [M, tiles, 4] tile partials
+  unsigned int* slice_done;  // [M] tiles finished (reset by the last)
   double* means;        // [M, T]
   double* loglik;       // [M]
   double* ess;          // [M, T]
@@ -216,29 +220,84 @@ __global__ void __launch_bounds__(256) k_pf_init(PfArgs a) {
   }
 }
 
-// resampling of the filters whose ESS fell below the threshold: passes 1-2
-// of the delivery per filter CTA (slot words with GLOBAL parent numbers into a
-// contiguous bitmap: N % 32 == 0), then one global in-place pass (K3 of the
-// fused delivery, launch_dv_inplace) resolves every filter's chains at once
-// (chains never leave a filter: its slots only name its own parents).  Other
-// N: the per-CTA pass 3.  c holds global particle numbers.
-template <bool kGlobal>
-__global__ void __launch_bounds__(kTileThreads) k_pf_resample(PfArgs a, int64_t t) {
+// Resampling of the filters whose ESS fell below the threshold (the step
+// before left their tile aggregates, exclusive tile prefixes and totals; see
+// k_pf_step).  Global in-place path (N % 32 == 0): one CTA per (tile,
+// filter) -- offspring of the tile from its prefix (the same association and
+// IEEE sequence as segment_deliver), then the slot words with GLOBAL parent
+// numbers into a contiguous bitmap; one global in-place pass (K3 of the fused
+// delivery, launch_dv_inplace) then resolves every filter's chains at once
+// (chains never leave a filter: its slots only name its own parents).  A tile
+// whose O decreases (rounding; never observed) flags its filter for
+// k_pf_repair, which redoes the filter with segment_deliver's running max.
+__global__ void __launch_bounds__(kTileThreads) k_pf_expand(PfArgs a, int64_t t) {
   __shared__ SegSmem S;
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.dv->flags = 0;  // K3 overflow flag of the previous step
+  const int64_t m = blockIdx.y, b = blockIdx.x, n = a.N;
+  if (b == 0 && m == 0 && threadIdx.x == 0) a.dv->flags = 0;  // K3 overflow flag of the previous step
+  const bool go = a.need[m] != 0;
+  if (b == 0 && threadIdx.x == 0) a.resampled[m * a.T + t] = go ? 1 : 0;
+  if (!go) return;
+  const double u = philox_unit53((uint32_t)m, (uint32_t)t, kTagPfSys, a.k0, a.k1);
+  const int64_t base = b * kTile;
+  double x[kTileItems];
+  tile_load_any<double>(a.w + m * n, n, base, x);
+  TileScan<double> s;
+#pragma unroll
+  for (int j = 0; j < kTileItems; ++j) s.loc[j] = x[j];
+  tile_scan<double>(s, S.warp_sums);
+  const double* ex = a.excl + m * (a.tiles + 1);
+  const double carry = __ldcg(ex + b), total = __ldcg(ex + a.tiles);
+  const double nd = (double)n;
+  auto off = [&](double W) {
+    const double r = __ddiv_rn(__dmul_rn(W, nd), total);
+    int64_t ov = (int64_t)floor(__dadd_rn(r, u));
+    return ov > n ? n : (ov < 0 ? (int64_t)0 : ov);
+  };
+  int32_t o[kTileItems];
+  const int64_t e0 = base + threadIdx.x * kTileItems;
+#pragma unroll
+  for (int j = 0; j < kTileItems; ++j) {
+    int64_t ov = off(__dadd_rn(carry, __dadd_rn(s.thread_excl, s.loc[j])));
+    if (e0 + j >= n - 1) ov = n;  // O[N-1] = N; padding past the filter
+    o[j] = (int32_t)ov;
+  }
+  const int32_t o_prev = b > 0 ? (int32_t)off(carry) : 0;
+  const int len = (int)min((int64_t)kTile, n - base);
+  if (tile_decreases(o, o_prev, len, S.warp_last)) {
+    if (threadIdx.x == 0) a.repair[m] = 1;
+    return;
+  }
+  tile_expand(o, o_prev, b, n, a.words + m * n, a.bitmap + m * (n / 32), reinterpret_cast<uint32_t*>(S.stage),
+              S.heads, S.warp_last, (uint32_t)(m * n));
+}
+
+// rare: a filter whose O decreased somewhere -- the whole filter again with
+// the running max (segment_deliver passes 1-2)
+__global__ void __launch_bounds__(kTileThreads) k_pf_repair(PfArgs a, int64_t t) {
+  __shared__ SegSmem S;
+  for (int64_t m = blockIdx.x; m < a.M; m += gridDim.x) {
+    if (!*(volatile uint8_t*)(a.repair + m)) continue;
+    const double u = philox_unit53((uint32_t)m, (uint32_t)t, kTagPfSys, a.k0, a.k1);
+    int longest = 0;
+    segment_deliver<double, false>(a.w + m * a.N, a.N, u, a.words + m * a.N, a.bitmap + m * (a.N / 32), nullptr,
+                                   longest, S, (uint32_t)(m * a.N));
+    __syncthreads();
+    if (threadIdx.x == 0) a.repair[m] = 0;
+  }
+}
+
+// Other N (or the PFR_PF_PATH=1 knob): one CTA per filter, segment_deliver
+// with its own pass 3 (c local to the filter).
+__global__ void __launch_bounds__(kTileThreads) k_pf_resample_local(PfArgs a, int64_t t) {
+  __shared__ SegSmem S;
   for (int64_t m = blockIdx.x; m < a.M; m += gridDim.x) {
     const bool go = a.need[m] != 0;
     if (threadIdx.x == 0) a.resampled[m * a.T + t] = go ? 1 : 0;
     if (!go) continue;
     const double u = philox_unit53((uint32_t)m, (uint32_t)t, kTagPfSys, a.k0, a.k1);
     int longest = 0;
-    if constexpr (kGlobal) {
-      segment_deliver<double, false>(a.w + m * a.N, a.N, u, a.words + m * a.N, a.bitmap + m * (a.N / 32), nullptr,
-                                     longest, S, (uint32_t)(m * a.N));
-    } else {
-      segment_deliver<double, true>(a.w + m * a.N, a.N, u, a.words + m * a.N, a.bitmap + m * a.bitmap_stride,
-                                    a.c + m * a.N, longest, S);
-    }
+    segment_deliver<double, true>(a.w + m * a.N, a.N, u, a.words + m * a.N, a.bitmap + m * a.bitmap_stride,
+                                  a.c + m * a.N, longest, S);
     __syncthreads();
   }
 }
@@ -264,16 +323,24 @@ __global__ void __launch_bounds__(kTileThreads) k_pf_fixup(PfArgs a, int force) 
   }
 }
 
-// propagate (through the ancestry when resampled) + weight + per-filter
-// reductions.  Grid (slices, M): kPfSlices CTAs per filter each reduce their
-// contiguous slice; the last slice to finish (per-filter counter) folds the
-// slice partials in slice order (deterministic) and finishes the filter.
-constexpr int kPfSlices = 8;
-
-__global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
-  __shared__ double red[4][8];
+// Propagate (through the ancestry when resampled) + weight + per-filter
+// reductions, one CTA per (tile, filter).  Compute runs striped (in round r
+// thread t owns the 4 particles at (256 r + t) * 4: coalesced 16-byte
+// accesses when N % 4 == 0); the new weights are restaged through shared
+// memory so that thread t then owns the tile's particles [16t, 16t + 16) and
+// each tile publishes the aggregate of its new weights in the association of
+// tile_scan (exactly segment_deliver's pass-1 value).  The last tile of a
+// filter to finish (per-filter counter) folds the tile partials in tile order
+// (deterministic), finishes the filter's step and, when it must resample
+// next, the exclusive tile prefixes and the total (serial folds, as
+// segment_deliver's pass 1/2 carries).
+template <bool kVec>
+__global__ void __launch_bounds__(kTileThreads, 4) k_pf_step(PfArgs a, int64_t t) {
+  __shared__ double red[4][kTileThreads / 32];
+  __shared__ double warp_sums[kTileThreads / 32];
+  __shared__ __align__(16) double2 ubuf[kTile / 2];
   __shared__ bool last;
-  const int64_t m = blockIdx.y;
+  const int64_t m = blockIdx.y, b = blockIdx.x;
   const int64_t n = a.N;
   const bool res = a.need[m] != 0;
   const double* src = ((t & 1) ? a.x1 : a.x0) + m * n;
@@ -284,30 +351,93 @@ __global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
   const double y = a.y[m * a.T + t];
   const double inv_obs = 1.0 / a.obs_std;
   const double dens_norm = inv_obs * 0.3989422804014327;  // 1 / (obs_std sqrt(2 pi))
-  // this slice: pairs [p0, p1) of the filter
-  const int64_t pairs = (n + 1) / 2;
-  const int64_t p0 = pairs * blockIdx.x / gridDim.x, p1 = pairs * (blockIdx.x + 1) / gridDim.x;
+  const int64_t base = b * kTile;
   double su = 0.0, sux = 0.0, suu = 0.0, sw = 0.0;
-  for (int64_t pp = p0 + threadIdx.x; pp < p1; pp += blockDim.x) {
-    const int64_t i = 2 * pp;
-    const float2 z = normal2((uint32_t)pp, (uint32_t)m, (uint32_t)t, kTagPfProp, a.k0, a.k1);
+  constexpr int kRounds = kTile / (4 * kTileThreads);
+#pragma unroll 2
+  for (int r = 0; r < kRounds; ++r) {
+    const int l0 = (r * kTileThreads + threadIdx.x) * 4;  // tile-local index of my first particle
+    const int64_t e0 = base + l0;
+    const bool full = kVec && e0 + 4 <= n;
+    double xo[4], wp[4];
+    if (full) {
+      if (res) {
+        const int4 ci = __ldcs(reinterpret_cast<const int4*>(cm + e0));
+        xo[0] = __ldg(src + (ci.x - c_base));
+        xo[1] = __ldg(src + (ci.y - c_base));
+        xo[2] = __ldg(src + (ci.z - c_base));
+        xo[3] = __ldg(src + (ci.w - c_base));
+      } else {
+        const double2 v0 = __ldcs(reinterpret_cast<const double2*>(src + e0));
+        const double2 v1 = __ldcs(reinterpret_cast<const double2*>(src + e0) + 1);
+        xo[0] = v0.x, xo[1] = v0.y, xo[2] = v1.x, xo[3] = v1.y;
+      }
+      if (res || t == 0) {
+        wp[0] = wp[1] = wp[2] = wp[3] = 1.0;
+      } else {
+        const double2 v0 = __ldcs(reinterpret_cast<const double2*>(w + e0));
+        const double2 v1 = __ldcs(reinterpret_cast<const double2*>(w + e0) + 1);
+        wp[0] = v0.x, wp[1] = v0.y, wp[2] = v1.x, wp[3] = v1.y;
+      }
+    } else {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t k = i + h;
-      if (k >= n) break;
-      const double xo = res ? src[cm[k] - c_base] : src[k];
-      const double wp = (res || t == 0) ? 1.0 : w[k];
-      const double xn = a.coeff * xo + a.trans_std * (double)(h ? z.y : z.x);
-      const double e = (y - xn) * inv_obs;
-      const double u = wp * (dens_norm * exp(-0.5 * e * e));
-      dst[k] = xn;
-      w[k] = u;
-      su += u;
-      sux += u * xn;
-      suu += u * u;
-      sw += wp;
+      for (int j = 0; j < 4; ++j) {
+        const int64_t k = e0 + j;
+        xo[j] = 0.0;
+        wp[j] = 0.0;
+        if (k < n) {
+          xo[j] = res ? src[cm[k] - c_base] : src[k];
+          wp[j] = (res || t == 0) ? 1.0 : w[k];
+        }
+      }
     }
+    double un[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      // the normals of pair (e0 + 2q) / 2 of the filter
+      const float2 z = normal2((uint32_t)((e0 >> 1) + q), (uint32_t)m, (uint32_t)t, kTagPfProp, a.k0, a.k1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 2 * q + h;
+        const double xn = a.coeff * xo[j] + a.trans_std * (double)(h ? z.y : z.x);
+        const double e = (y - xn) * inv_obs;
+        sw += wp[j];
+        double u = wp[j] * (dens_norm * exp(-0.5 * e * e));
+        if (!full && e0 + j >= n) u = 0.0;
+        xo[j] = xn;
+        un[j] = u;
+        su += u;
+        sux += u * xn;
+        suu += u * u;
+      }
+    }
+    if (full) {
+      __stcs(reinterpret_cast<double2*>(dst + e0), make_double2(xo[0], xo[1]));
+      __stcs(reinterpret_cast<double2*>(dst + e0) + 1, make_double2(xo[2], xo[3]));
+      __stcg(reinterpret_cast<double2*>(w + e0), make_double2(un[0], un[1]));
+      __stcg(reinterpret_cast<double2*>(w + e0) + 1, make_double2(un[2], un[3]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (e0 + j < n) {
+          dst[e0 + j] = xo[j];
+          w[e0 + j] = un[j];
+        }
+    }
+    ubuf[swz(l0 / 2)] = make_double2(un[0], un[1]);
+    ubuf[swz(l0 / 2 + 1)] = make_double2(un[2], un[3]);
   }
+  __syncthreads();
+  TileScan<double> s;
+#pragma unroll
+  for (int k = 0; k < kTileItems / 2; ++k) {
+    const double2 v = ubuf[swz(threadIdx.x * (kTileItems / 2) + k)];
+    s.loc[2 * k] = v.x;
+    s.loc[2 * k + 1] = v.y;
+  }
+  // tile aggregate of the new weights (segment_deliver's association)
+  tile_scan<double>(s, warp_sums);
+  if (threadIdx.x == kTileThreads - 1) a.agg[m * a.tiles + b] = __dadd_rn(s.thread_excl, s.loc[kTileItems - 1]);
   // block reduction: warp butterfly, then the 8 warps in order
   double v[4] = {su, sux, suu, sw};
 #pragma unroll
@@ -319,10 +449,10 @@ __global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
     for (int q = 0; q < 4; ++q) red[q][threadIdx.x >> 5] = v[q];
   __syncthreads();
   if (threadIdx.x == 0) {
-    double* part = a.part + (m * kPfSlices + blockIdx.x) * 4;
+    double* part = a.part + (m * a.tiles + b) * 4;
     for (int q = 0; q < 4; ++q) {
       double r = 0;
-      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r += red[q][k];
+      for (int k = 0; k < kTileThreads / 32; ++k) r += red[q][k];
       part[q] = r;
     }
     __threadfence();
@@ -332,8 +462,8 @@ __global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
   if (!last || threadIdx.x != 0) return;
   __threadfence();
   double r[4] = {0, 0, 0, 0};
-  for (int sl = 0; sl < (int)gridDim.x; ++sl)
-    for (int q = 0; q < 4; ++q) r[q] += __ldcg(a.part + (m * kPfSlices + sl) * 4 + q);
+  for (int64_t sl = 0; sl < a.tiles; ++sl)
+    for (int q = 0; q < 4; ++q) r[q] += __ldcg(a.part + (m * a.tiles + sl) * 4 + q);
   a.slice_done[m] = 0;
   const double total = r[0] / r[3];  // sum of normalised weights x density
   if (!(total > 0.0) || !isfinite(total)) {
@@ -344,7 +474,17 @@ __global__ void __launch_bounds__(256) k_pf_step(PfArgs a, int64_t t) {
   a.means[m * a.T + t] = r[1] / r[0];
   const double ess_next = r[0] * r[0] / r[2];
   if (t + 1 < a.T) a.ess[m * a.T + t + 1] = ess_next;
-  a.need[m] = (ess_next / (double)n < a.ess_threshold) ? 1 : 0;
+  const bool need = (ess_next / (double)n < a.ess_threshold);
+  a.need[m] = need ? 1 : 0;
+  if (need && t + 1 < a.T) {
+    double* ex = a.excl + m * (a.tiles + 1);
+    double carry = 0.0;
+    for (int64_t sl = 0; sl < a.tiles; ++sl) {
+      ex[sl] = carry;
+      carry = __dadd_rn(carry, __ldcg(a.agg + m * a.tiles + sl));
+    }
+    ex[a.tiles] = carry;
+  }
 }
 
 }  // namespace
@@ -361,8 +501,12 @@ size_t pf_workspace_bytes(int64_t M, int64_t N) {
   add(mn * 4 + 16);     // words
   add(M * bstride * 4); // bitmap
   add(M);               // need
-  add(M * 8 * 4 * 8);   // slice partials
-  add(M * 4);           // slice counters
+  const int64_t tiles = num_tiles(N);
+  add(M * tiles * 8);        // tile aggregates
+  add(M * (tiles + 1) * 8);  // tile prefixes
+  add(M);                    // repair flags
+  add(M * tiles * 4 * 8);    // tile partials
+  add(M * 4);                // tile counters
   add(sizeof(DvState)); // K3 state
   return b;
 }
@@ -427,7 +571,11 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   a.bitmap_stride = (N + 31) / 32 + 4;
   a.bitmap = reinterpret_cast<uint32_t*>(take(M * a.bitmap_stride * 4));
   a.need = reinterpret_cast<uint8_t*>(take(M));
-  a.part = reinterpret_cast<double*>(take(M * 8 * 4 * 8));
+  a.tiles = num_tiles(N);
+  a.agg = reinterpret_cast<double*>(take(M * a.tiles * 8));
+  a.excl = reinterpret_cast<double*>(take(M * (a.tiles + 1) * 8));
+  a.repair = reinterpret_cast<uint8_t*>(take(M));
+  a.part = reinterpret_cast<double*>(take(M * a.tiles * 4 * 8));
   a.slice_done = reinterpret_cast<unsigned int*>(take(M * 4));
   a.dv = reinterpret_cast<DvState*>(take(sizeof(DvState)));
   a.means = means;
@@ -443,6 +591,8 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   e = cudaMemsetAsync(a.slice_done, 0, sizeof(unsigned int) * M, s);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(a.dv, 0, sizeof(DvState), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(a.repair, 0, M, s);
   if (e != cudaSuccess) return e;
   // stale slot words of filters that did not resample stay valid particle
   // numbers for the global in-place pass
@@ -463,21 +613,26 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   for (int64_t t = 0; t < T; ++t) {
     if (t > 0) {
       if (global_pass) {
-        k_pf_resample<true><<<gr, kTileThreads, 0, s>>>(a, t);
+        k_pf_expand<<<dim3((unsigned)a.tiles, (unsigned)M), kTileThreads, 0, s>>>(a, t);
+        note_launch();
+        k_pf_repair<<<gr, kTileThreads, 0, s>>>(a, t);
         note_launch();
         e = launch_dv_inplace(a.words, a.bitmap, mn, a.c, a.dv, status, s);
         if (e != cudaSuccess) return e;
         k_pf_fixup<<<gr, kTileThreads, 0, s>>>(a, path == 2);
         note_launch();
       } else {
-        k_pf_resample<false><<<gr, kTileThreads, 0, s>>>(a, t);
+        k_pf_resample_local<<<gr, kTileThreads, 0, s>>>(a, t);
         note_launch();
       }
     } else {
       e = cudaMemsetAsync(resampled, 0, M * T, s);
       if (e != cudaSuccess) return e;
     }
-    k_pf_step<<<dim3(kPfSlices, (unsigned)M), 256, 0, s>>>(a, t);
+    if (N % 4 == 0)
+      k_pf_step<true><<<dim3((unsigned)a.tiles, (unsigned)M), kTileThreads, 0, s>>>(a, t);
+    else
+      k_pf_step<false><<<dim3((unsigned)a.tiles, (unsigned)M), kTileThreads, 0, s>>>(a, t);
     note_launch();
   }
   return cudaGetLastError();

@@ -268,25 +268,6 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
   }
 }
 
-// true when o decreases anywhere inside the tile or against the previous
-// tile's last O (the caller then defers to the repair path)
-__device__ __forceinline__ bool tile_decreases(const int32_t (&o)[kTileItems], int32_t o_prev, int len,
-                                               int32_t* warp_last) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int e0 = threadIdx.x * kTileItems;
-  (void)e0;
-  (void)len;  // padding past N holds O = N: it never decreases
-  bool bad = false;
-#pragma unroll
-  for (int j = 1; j < kTileItems; ++j) bad |= o[j] < o[j - 1];
-  int prev = __shfl_up_sync(0xffffffffu, o[kTileItems - 1], 1);
-  if (lane == 31) warp_last[warp] = o[kTileItems - 1];
-  __syncthreads();
-  if (lane == 0) prev = warp ? warp_last[warp - 1] : o_prev;
-  bad |= o[0] < prev;
-  return __syncthreads_or(bad);
-}
-
 // ---------------------------------------------------------------------------
 // K2
 template <typename T, typename A, int UM>
