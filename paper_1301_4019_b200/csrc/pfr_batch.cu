@@ -181,6 +181,8 @@ struct PfArgs {
   double* agg;          // [M, tiles] tile aggregates of w
   double* excl;         // [M, tiles + 1] exclusive tile prefixes, total
   uint8_t* repair;      // [M] filter needs the running-max repair
+  uint32_t* rlist;      // [2, M] filters to resample at the next step (double buffered by step parity)
+  uint32_t* rcount;     // [2]
   double* part;         // [M, tiles, 4] tile partials
   unsigned int* slice_done;  // [M] tiles finished (reset by the last)
   double* means;        // [M, T]
@@ -304,7 +306,10 @@ __global__ void __launch_bounds__(kTileThreads) k_pf_resample_local(PfArgs a, in
 
 // rare: a chain longer than K3's walk bound -- redo the in-place pass of the
 // resampled filters with unbounded per-thread walks (global numbers)
-__global__ void __launch_bounds__(kTileThreads) k_pf_fixup(PfArgs a, int force) {
+__global__ void __launch_bounds__(kTileThreads) k_pf_fixup(PfArgs a, int64_t t, int force) {
+  // the list the next step fills (its previous reader, the in-place pass of
+  // step t - 1, has finished)
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.rcount[(t + 1) & 1] = 0;
   if (!force && !(*(volatile unsigned*)&a.dv->flags & 2u)) return;
   for (int64_t m = blockIdx.x; m < a.M; m += gridDim.x) {
     if (!a.need[m]) continue;
@@ -477,6 +482,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_pf_step(PfArgs a, int64_t t
   const bool need = (ess_next / (double)n < a.ess_threshold);
   a.need[m] = need ? 1 : 0;
   if (need && t + 1 < a.T) {
+    const int nb = (int)((t + 1) & 1);
+    if (a.c_global) a.rlist[nb * a.M + atomicAdd(a.rcount + nb, 1u)] = (uint32_t)m;
     double* ex = a.excl + m * (a.tiles + 1);
     double carry = 0.0;
     for (int64_t sl = 0; sl < a.tiles; ++sl) {
@@ -505,6 +512,7 @@ size_t pf_workspace_bytes(int64_t M, int64_t N) {
   add(M * tiles * 8);        // tile aggregates
   add(M * (tiles + 1) * 8);  // tile prefixes
   add(M);                    // repair flags
+  add(2 * M * 4 + 8);        // resample lists + counts
   add(M * tiles * 4 * 8);    // tile partials
   add(M * 4);                // tile counters
   add(sizeof(DvState)); // K3 state
@@ -575,6 +583,8 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   a.agg = reinterpret_cast<double*>(take(M * a.tiles * 8));
   a.excl = reinterpret_cast<double*>(take(M * (a.tiles + 1) * 8));
   a.repair = reinterpret_cast<uint8_t*>(take(M));
+  a.rlist = reinterpret_cast<uint32_t*>(take(2 * M * 4 + 8));
+  a.rcount = a.rlist + 2 * M;
   a.part = reinterpret_cast<double*>(take(M * a.tiles * 4 * 8));
   a.slice_done = reinterpret_cast<unsigned int*>(take(M * 4));
   a.dv = reinterpret_cast<DvState*>(take(sizeof(DvState)));
@@ -593,6 +603,8 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   e = cudaMemsetAsync(a.dv, 0, sizeof(DvState), s);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(a.repair, 0, M, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(a.rcount, 0, 8, s);
   if (e != cudaSuccess) return e;
   // stale slot words of filters that did not resample stay valid particle
   // numbers for the global in-place pass
@@ -617,9 +629,10 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
         note_launch();
         k_pf_repair<<<gr, kTileThreads, 0, s>>>(a, t);
         note_launch();
-        e = launch_dv_inplace(a.words, a.bitmap, mn, a.c, a.dv, status, s);
+        e = launch_dv_inplace(a.words, a.bitmap, mn, a.c, a.dv, status, s, a.rlist + (t & 1) * M,
+                              a.rcount + (t & 1), N);
         if (e != cudaSuccess) return e;
-        k_pf_fixup<<<gr, kTileThreads, 0, s>>>(a, path == 2);
+        k_pf_fixup<<<gr, kTileThreads, 0, s>>>(a, t, path == 2);
         note_launch();
       } else {
         k_pf_resample_local<<<gr, kTileThreads, 0, s>>>(a, t);

@@ -308,6 +308,14 @@ constexpr int kQ = 512;          // queue entries per warp
 constexpr int kStepPer = 4;      // chain loads per lane per step batch
 constexpr int kGroup = 32;
 
+// optional segment list for K3: only the listed segments of `groups` 32-index
+// groups each (the batched filter's resampled filters)
+struct IpSegments {
+  const uint32_t* list;   // segment numbers (null: the whole index range)
+  const uint32_t* count;  // number of listed segments (device)
+  uint32_t groups;        // groups per segment
+};
+
 struct IpQueue {
   uint32_t x[kIpWarps][kQ];
   uint32_t z[kIpWarps][kQ];
@@ -384,16 +392,20 @@ template <int kScanG, int kThresh, int kMinBlocks>
 __global__ void __launch_bounds__(kIpThreads, kMinBlocks) k_dv_inplace(const uint32_t* __restrict__ words,
                                                           const uint32_t* __restrict__ bitmap, int64_t n,
                                                           int32_t* __restrict__ c, int32_t* max_steps,
-                                                          DvState* state, uint32_t* status) {
+                                                          DvState* state, uint32_t* status, IpSegments segs) {
   __shared__ IpQueue Q;
   griddep_wait();
   if (state->flags & kNeedsRepair) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t nn = (uint32_t)n;
-  const uint32_t groups = (nn + kGroup - 1) / kGroup;
+  // segment mode: the index space is the listed segments, back to back
+  const uint32_t groups = segs.list ? *segs.count * segs.groups : (nn + kGroup - 1) / kGroup;
+  auto pg = [&](uint32_t g) -> uint32_t {
+    return segs.list ? __ldg(segs.list + g / segs.groups) * segs.groups + g % segs.groups : g;
+  };
   const uint32_t gw = blockIdx.x * kIpWarps + warp, nw = gridDim.x * kIpWarps;
   const uint32_t g0 = (uint32_t)((uint64_t)groups * gw / nw), g1 = (uint32_t)((uint64_t)groups * (gw + 1) / nw);
-  const uint32_t gfull = nn / kGroup;  // groups entirely below n
+  const uint32_t gfull = segs.list ? groups : nn / kGroup;  // groups entirely below n
   int qlen = 0;
   int longest = 0;
   bool overflow = false;
@@ -405,20 +417,22 @@ __global__ void __launch_bounds__(kIpThreads, kMinBlocks) k_dv_inplace(const uin
     uint32_t wd[kScanG], bw[kScanG];
 #pragma unroll
     for (int q = 0; q < kScanG; ++q) {
-      wd[q] = __ldcs(words + (g + q) * kGroup + lane);
-      bw[q] = __ldg(bitmap + g + q);
+      const uint32_t gp = pg(g + q);
+      wd[q] = __ldcs(words + gp * kGroup + lane);
+      bw[q] = __ldg(bitmap + gp);
     }
 #pragma unroll
-    for (int q = 0; q < kScanG; ++q) scan_group(Q, warp, lane, (g + q) * kGroup + lane, true, wd[q], bw[q], qlen, c);
+    for (int q = 0; q < kScanG; ++q) scan_group(Q, warp, lane, pg(g + q) * kGroup + lane, true, wd[q], bw[q], qlen, c);
     __syncwarp();
   }
   // tail groups
   for (; g < g1; ++g) {
     if (qlen > kQ - 32) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
-    const uint32_t x = g * kGroup + lane;
-    const bool in = x < nn;
+    const uint32_t gp = pg(g);
+    const uint32_t x = gp * kGroup + lane;
+    const bool in = segs.list || x < nn;
     const uint32_t wd = in ? __ldcs(words + x) : 0u;
-    scan_group(Q, warp, lane, x, in, wd, __ldg(bitmap + g), qlen, c);
+    scan_group(Q, warp, lane, x, in, wd, __ldg(bitmap + gp), qlen, c);
     __syncwarp();
   }
   while (qlen) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
@@ -640,7 +654,7 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
     const unsigned grid3 =
         (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
     e = launch_pdl(kernel, dim3(grid3), dim3(kIpThreads), s, false, (const uint32_t*)p.words,
-                   (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status);
+                   (const uint32_t*)p.bitmap, p.n, p.c, p.max_steps, p.state, p.status, IpSegments{nullptr, nullptr, 0});
     if (e != cudaSuccess || stages < 4) return e;
   }
   static int occ = -1;
@@ -702,7 +716,8 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
 // serves every filter).  Sets kOverflow in state->flags when a chain exceeds
 // the walk bound (the caller owns the fallback).
 cudaError_t launch_dv_inplace(const uint32_t* words, const uint32_t* bitmap, int64_t n, int32_t* c, DvState* state,
-                              uint32_t* status, cudaStream_t s) {
+                              uint32_t* status, cudaStream_t s, const uint32_t* seg_list, const uint32_t* seg_count,
+                              int64_t seg_len) {
   auto kernel = k_dv_inplace<4, 64, 4>;
   int occ3 = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, kernel, kIpThreads, 0);
@@ -712,7 +727,7 @@ cudaError_t launch_dv_inplace(const uint32_t* words, const uint32_t* bitmap, int
   const unsigned grid3 =
       (unsigned)max((int64_t)1, min((int64_t)num_sms() * occ3, (warps_needed + kIpWarps - 1) / kIpWarps));
   return launch_pdl(kernel, dim3(grid3), dim3(kIpThreads), s, false, words, bitmap, n, c, (int32_t*)nullptr, state,
-                    status);
+                    status, IpSegments{seg_list, seg_count, (uint32_t)(seg_len / 32)});
 }
 
 // systematic_/stratified_cumulative_offspring (resamplers.py:105-153): the

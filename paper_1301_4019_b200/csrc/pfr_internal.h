@@ -114,7 +114,8 @@ cudaError_t launch_shard_scatter(const int32_t* done, int64_t count, int64_t ind
                                  uint32_t* status, cudaStream_t s);
 
 cudaError_t launch_dv_inplace(const uint32_t* words, const uint32_t* bitmap, int64_t n, int32_t* c, DvState* state,
-                              uint32_t* status, cudaStream_t s);
+                              uint32_t* status, cudaStream_t s, const uint32_t* seg_list = nullptr,
+                              const uint32_t* seg_count = nullptr, int64_t seg_len = 0);
 
 // launchers (pfr_batch.cu): batches of independent filters
 size_t batched_workspace_bytes(int64_t M, int64_t N);
