@@ -24,6 +24,7 @@
 #include <algorithm>
 
 #include "pfr_expand.cuh"
+#include "pfr_fx.cuh"
 #include "pfr_internal.h"
 #include "pfr_tile.cuh"
 
@@ -178,6 +179,7 @@ struct PfArgs {
   DvState* dv;          // K3 state (overflow flag)
   int c_global;          // c holds global particle numbers (global in-place pass)
   int64_t tiles;         // tiles per filter
+  int fx_S;              // fixed-point bits of the offspring fast path
   double* agg;          // [M, tiles] tile aggregates of w
   double* excl;         // [M, tiles + 1] exclusive tile prefixes, total
   uint8_t* repair;      // [M] filter needs the running-max repair
@@ -193,17 +195,18 @@ struct PfArgs {
   uint32_t* status;
 };
 
-// two standard normals from one Philox call (Box-Muller in float: the
-// transition noise of the model, pf.py:188-189)
+// two standard normals from one Philox call (Box-Muller in float with the
+// SFU log/sin/cos, abs. error ~1e-6: the transition noise of the model,
+// pf.py:188-189)
 __device__ __forceinline__ float2 normal2(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t tag, uint32_t k0,
                                           uint32_t k1) {
   uint32_t o[4];
   philox4x32_10(c0, c1, c2, tag, k0, k1, o);
   const float u1 = ((float)(o[0] >> 8) + 1.0f) * (1.0f / 16777216.0f);  // (0, 1]
   const float u2 = (float)(o[1] >> 8) * (1.0f / 16777216.0f);
-  const float rad = sqrtf(-2.0f * logf(u1));
+  const float rad = sqrtf(-2.0f * __logf(u1));
   float sn, cs;
-  sincospif(2.0f * u2, &sn, &cs);
+  __sincosf(6.283185307179586f * u2, &sn, &cs);
   return make_float2(rad * cs, rad * sn);
 }
 
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(256) k_pf_init(PfArgs a) {
 // (chains never leave a filter: its slots only name its own parents).  A tile
 // whose O decreases (rounding; never observed) flags its filter for
 // k_pf_repair, which redoes the filter with segment_deliver's running max.
-__global__ void __launch_bounds__(kTileThreads) k_pf_expand(PfArgs a, int64_t t) {
+__global__ void __launch_bounds__(kTileThreads, 4) k_pf_expand(PfArgs a, int64_t t) {
   __shared__ SegSmem S;
   const int64_t m = blockIdx.y, b = blockIdx.x, n = a.N;
   if (b == 0 && m == 0 && threadIdx.x == 0) a.dv->flags = 0;  // K3 overflow flag of the previous step
@@ -250,9 +253,14 @@ __global__ void __launch_bounds__(kTileThreads) k_pf_expand(PfArgs a, int64_t t)
   const double* ex = a.excl + m * (a.tiles + 1);
   const double carry = __ldcg(ex + b), total = __ldcg(ex + a.tiles);
   const double nd = (double)n;
-  auto off = [&](double W) {
-    const double r = __ddiv_rn(__dmul_rn(W, nd), total);
-    int64_t ov = (int64_t)floor(__dadd_rn(r, u));
+  // fixed-point fast path (pfr_fx.cuh), the exact sequence when fragile
+  const FxParams fx = fx_params<double>(n, total, u, a.fx_S);
+  auto off = [&](double W) -> int64_t {
+    const long long r = fx_round(W, fx.sfx);
+    const long long tt = r + fx.ufx;
+    if (fx_safe(r, fx.mask) & fx_safe(tt, fx.mask)) return min((int64_t)(tt >> fx.S), n);
+    const double rr = __ddiv_rn(__dmul_rn(W, nd), total);
+    int64_t ov = (int64_t)floor(__dadd_rn(rr, u));
     return ov > n ? n : (ov < 0 ? (int64_t)0 : ov);
   };
   int32_t o[kTileItems];
@@ -580,6 +588,7 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
   a.bitmap = reinterpret_cast<uint32_t*>(take(M * a.bitmap_stride * 4));
   a.need = reinterpret_cast<uint8_t*>(take(M));
   a.tiles = num_tiles(N);
+  a.fx_S = fx_bits(N);
   a.agg = reinterpret_cast<double*>(take(M * a.tiles * 8));
   a.excl = reinterpret_cast<double*>(take(M * (a.tiles + 1) * 8));
   a.repair = reinterpret_cast<uint8_t*>(take(M));
