@@ -427,8 +427,14 @@ def main():
 
     # ---------------- north-star targets: N = 2^24 float32 ----------------
     targets = None
+    probes = None
+    if rank == 0:
+        try:
+            probes = gather_probes(torch, dev, stream)
+        except Exception as exc:  # optional measurement leg
+            probes = {"error": f"{type(exc).__name__}: {exc}"[:200]}
     if not args.no_targets:
-        targets = north_star_targets(pf, torch, dev, stream, flush, hbm) if rank == 0 else {}
+        targets = north_star_targets(pf, torch, dev, stream, flush, hbm, probes=probes) if rank == 0 else {}
         # config 4: ONE filter of N = 2^28 float32, weight-sharded over the ranks
         try:
             targets.update(c4_targets(pf, torch, dev, stream, flush, hbm, rank, world))
@@ -465,6 +471,7 @@ def main():
                          "note": "algorithmic bytes count every proposal's weight gather (SURVEY 8(d)); the "
                                  "gathers hit L2 (N=2^20 weights are L2 resident): the kernel is bound by the "
                                  "L2 random-sector rate and Philox issue, not by HBM (DESIGN.md 3.3-3.4)"},
+            "gather_probes": probes,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "particles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
@@ -473,13 +480,56 @@ def main():
             "status_bits": status,
             "targets": targets,
         }
+        key = f"{dt}_2^{n.bit_length() - 1}"
+        if alg in ("rejection", "metropolis") and probes and key in probes:
+            gathers = (trips[dt] if alg == "rejection" else B_STEPS) * n
+            g = gathers / (dom_ms * 1e-3) / 1e9
+            peak = probes[key]["ggather_per_s"]
+            line["roofline"]["gather_floor"] = {
+                "achieved_ggather_per_s": g, "peak_ggather_per_s": peak, "frac": g / peak,
+                "gathers_per_launch": gathers,
+                "peak_source": f"pfr_probe_gather on the same-size ({key}) L2-resident vector, this run"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def north_star_targets(pf, torch, dev, stream, flush, hbm, reps=10):
+def gather_probes(torch, dev, stream, reps=5):
+    """Measured random-gather floor of the memory system (pfr_probe_gather:
+    8 independent LCG streams per thread, 2 integer ops per gather): G
+    gathers/s for L2-resident weight vectors (the N=2^20 headline and the
+    2^24 north star) and for a 1 GiB vector (HBM random sectors, config 4)."""
+    from paper_1301_4019_b200 import _lib as L
+
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    threads = sms * 8 * 256
+    out = {}
+    for name, log2n, eb in (("f32_2^20", 20, 4), ("f64_2^20", 20, 8), ("f32_2^24", 24, 4), ("f32_2^28", 28, 4)):
+        n = 1 << log2n
+        iters = max(1, (1 << 29) // (threads * 8))
+        gathers = threads * 8 * iters
+        buf = torch.randint(0, 2 ** 31 - 1, (n * eb // 4,), dtype=torch.int32, device=dev)
+        sink = torch.zeros(1, dtype=torch.int64, device=dev)
+        call = lambda: L.call("pfr_probe_gather", buf.data_ptr(), n, eb, gathers, sink.data_ptr(), stream.cuda_stream)
+        call()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            call()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        t = statistics.median(ts)
+        out[name] = {"ggather_per_s": gathers / (t * 1e-3) / 1e9, "bytes": n * eb}
+        del buf, sink
+    return out
+
+
+def north_star_targets(pf, torch, dev, stream, flush, hbm, reps=10, probes=None):
     n = 1 << 24
     w = torch.from_numpy(log_normal_weights(n, 424242, np.float32)).to(dev)
     c = torch.empty(n, dtype=torch.int32, device=dev)
@@ -512,6 +562,12 @@ def north_star_targets(pf, torch, dev, stream, flush, hbm, reps=10):
     out["metropolis_B32_2^24_f32_kernel"] = {"us": t * 1e3, "particles_per_s": n / (t * 1e-3),
                                              "algorithmic_bytes": b, "achieved_gbs": b / (t * 1e-3) / 1e9,
                                              "frac": b / (t * 1e-3) / 1e9 / hbm, "target_frac": 0.70}
+    if probes and "f32_2^24" in probes:
+        g = B_STEPS * n / (t * 1e-3) / 1e9
+        peak = probes["f32_2^24"]["ggather_per_s"]
+        out["metropolis_B32_2^24_f32_kernel"]["gather_floor"] = {
+            "achieved_ggather_per_s": g, "peak_ggather_per_s": peak, "frac": g / peak,
+            "peak_source": "pfr_probe_gather on a 64 MiB (L2-resident) vector, this run"}
     cfgm = pf.ResamplerConfig("metropolis", b=B_STEPS)
     t = timeit(lambda r: pf.deliver(w, cfgm, pf.RngStream(r), index_dtype=torch.int32))
     out["metropolis_B32_2^24_f32_delivery"] = {"us": t * 1e3, "particles_per_s": n / (t * 1e-3)}

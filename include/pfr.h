@@ -289,6 +289,14 @@ int pfr_stable_sum(const void* w, int64_t n, int dtype, double* result, void* ws
 int pfr_weight_stats(const void* w, int64_t n, int dtype, const void* o, int idx_dtype, double* out, void* ws,
                      size_t ws_bytes, void* stream);
 
+/* Measurement helper (not a reference interface): `gathers` random loads of
+ * elem_bytes (4 or 8) words from buf[n] (n a power of two), indices from
+ * per-thread LCGs -- the memory system's random-gather rate that bounds the
+ * Metropolis and rejection kernels (bench.py times it with CUDA events).
+ * *sink (device) only keeps the loads live. */
+int pfr_probe_gather(const void* buf, int64_t n, int elem_bytes, int64_t gathers, unsigned long long* sink,
+                     void* stream);
+
 /* ---- batches of independent filters -----------
  * No communication: one CTA per filter.  Arrays are [filters, n] row-major. */
 

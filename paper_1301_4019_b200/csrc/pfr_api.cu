@@ -488,6 +488,15 @@ int pfr_stable_sum(const void* w, int64_t n, int dtype, double* result, void* ws
   return PFR_OK;
 }
 
+int pfr_probe_gather(const void* buf, int64_t n, int elem_bytes, int64_t gathers, unsigned long long* sink,
+                     void* stream) {
+  PFR_REQUIRE(buf && sink && n >= 1 && n <= (int64_t(1) << 32) && (n & (n - 1)) == 0 && gathers > 0,
+              "bad arguments (n must be a power of two <= 2^32)");
+  PFR_REQUIRE(elem_bytes == 4 || elem_bytes == 8, "elem_bytes must be 4 or 8");
+  PFR_CHECK_LAUNCH(launch_probe_gather(buf, n, elem_bytes, gathers, sink, (cudaStream_t)stream), "pfr_probe_gather");
+  return PFR_OK;
+}
+
 int pfr_weight_stats(const void* w, int64_t n, int dtype, const void* o, int idx_dtype, double* out, void* ws_ptr,
                      size_t ws_bytes, void* stream) {
   PFR_REQUIRE(valid_n(n) && w && out, "bad arguments");

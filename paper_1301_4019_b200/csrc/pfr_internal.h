@@ -130,6 +130,8 @@ cudaError_t launch_pf_run(const pfr_pf_model* model, const double* y, int64_t M,
 cudaError_t launch_permute_serial(const void* a, int64_t n, int idx_dtype, int32_t* c, uint32_t* status,
                                   cudaStream_t s);
 cudaError_t launch_stable_sum(const void* w, int64_t n, int dtype, void* result, void* scratch, cudaStream_t s);
+cudaError_t launch_probe_gather(const void* buf, int64_t n, int elem_bytes, int64_t gathers, unsigned long long* sink,
+                                cudaStream_t s);
 cudaError_t launch_weight_stats(const void* w, int64_t n, int dtype, const void* o, int idx_dtype, double* out,
                                 void* scratch, cudaStream_t s);
 

@@ -220,4 +220,46 @@ cudaError_t launch_weight_stats(const void* w, int64_t n, int dtype, const void*
   return cudaGetLastError();
 }
 
+// Random-gather probe (measurement only): every thread walks 8 independent
+// LCG streams and gathers buf[index] for each (the top log2 n bits of the
+// state: uniform over a power-of-two n), XOR-folding the loaded words so the
+// loads stay live.  Two integer ops per gather: bound by the memory system
+// (L2 sectors when buf is L2 resident, HBM sectors otherwise) -- the floor
+// the Metropolis and rejection gathers are compared with.
+template <typename U>
+__global__ void __launch_bounds__(256) k_probe_gather(const U* __restrict__ buf, int shift, int iters,
+                                                      unsigned long long* sink) {
+  uint32_t st[8];
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) st[q] = (tid * 8u + q) * 0x9E3779B9u ^ 0x85EBCA6Bu;
+  U acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    U v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      st[q] = st[q] * 1664525u + 1013904223u;
+      v[q] = __ldg(buf + (shift >= 32 ? 0u : (st[q] >> shift)));
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc ^= v[q];
+  }
+  if (acc == (U)0x5EED5EEDu) atomicAdd(sink, 1ull);
+}
+
+cudaError_t launch_probe_gather(const void* buf, int64_t n, int elem_bytes, int64_t gathers, unsigned long long* sink,
+                                cudaStream_t s) {
+  int L = 0;
+  while ((int64_t(1) << L) < n) ++L;
+  const unsigned grid = (unsigned)num_sms() * 8;
+  const int64_t threads = (int64_t)grid * 256;
+  const int iters = (int)std::max<int64_t>(1, gathers / (threads * 8));
+  if (elem_bytes == 8)
+    k_probe_gather<unsigned long long><<<grid, 256, 0, s>>>((const unsigned long long*)buf, 32 - L, iters, sink);
+  else
+    k_probe_gather<uint32_t><<<grid, 256, 0, s>>>((const uint32_t*)buf, 32 - L, iters, sink);
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace pfr

@@ -114,7 +114,13 @@ __host__ __device__ __forceinline__ float u32_to_unit_f(uint32_t x) {
   return (float)(x >> 8) * (1.0f / 16777216.0f);  // 24-bit, [0,1)
 }
 __host__ __device__ __forceinline__ double u32_to_unit_d(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  // x * 2^-32 exactly, without the quarter-rate I2F.F64: the double with
+  // high word 2^20 and low word x is 2^20 + x * 2^-32; subtracting 2^20 is exact
+  return __hiloint2double(0x41300000, (int)x) - 1048576.0;
+#else
   return (double)x * (1.0 / 4294967296.0);  // [0,1)
+#endif
 }
 
 // Lemire bounded integer in [0, n): exact (rejection on the biased sliver;

@@ -24,6 +24,10 @@ for r in range(reps):
         pf.permute_parallel(a, index_dtype=torch.int32)
     if which in ("all", "rejection"):
         a = pf.rejection_ancestors(w, float(w.max()), pf.RngStream(r), index_dtype=torch.int32)
+    if which in ("all", "multinomial"):
+        pf.deliver(w, pf.ResamplerConfig("multinomial"), pf.RngStream(r), index_dtype=torch.int32, out=c)
+    if which in ("all", "metropolis-delivery"):
+        pf.deliver(w, pf.ResamplerConfig("metropolis", b=32), pf.RngStream(r), index_dtype=torch.int32, out=c)
     if which in ("all", "stratified"):
         pf.deliver(w, pf.ResamplerConfig("stratified"), pf.RngStream(r), index_dtype=torch.int32, out=c)
 torch.cuda.synchronize()
