@@ -365,10 +365,12 @@ def main():
     # ---------------- e2e: host buffers through the public API ----------------
     # Every delivery's weights come from pinned host memory and its ancestry
     # goes back to pinned host memory, inside the timed region.  The copies
-    # run on a second stream and are pipelined with the resampling kernels
-    # (delivery d+1's weights upload while delivery d computes; delivery d's
-    # result downloads while d+1 computes) -- the B200-native way to feed the
-    # API; the device-only number is `value`.
+    # run on a copy stream pipelined with the resampling kernels (later
+    # deliveries' weights upload while earlier ones compute; results download
+    # while later deliveries compute) -- the B200-native way to feed the API;
+    # the device-only number is `value`.  The host link is the floor here:
+    # the same uploads and downloads with no compute take ~2.0 ms per step
+    # (H2D and D2H share the link; reported as `link_only_ms`).
     host_w = {dt: weights[dt].cpu().pin_memory() for dt in DTYPES}
     jobs = [(i, alg, j, dt) for i, alg in enumerate(ALGS) for j, dt in enumerate(DTYPES)]
     host_c = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in jobs]
@@ -414,8 +416,33 @@ def main():
                 host_c[k].copy_(c, non_blocking=True)
         e1.record(copy_stream)
         torch.cuda.synchronize()
+        if os.environ.get("PFR_BENCH_DEBUG"):
+            print(f"e2e step {s}: {e0.elapsed_time(e1):.3f} ms", file=sys.stderr, flush=True)
         if s >= args.warmup:
             e2e_ms += e0.elapsed_time(e1)
+    # the link floor: the step's copies alone (uploads and downloads issued
+    # together on two streams, no compute)
+    link_ms = []
+    down_only = torch.cuda.Stream(device=dev)
+    for s in range(4):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record(copy_stream)
+        down_only.wait_event(e0)
+        with torch.cuda.stream(copy_stream):
+            for k, (i, alg, j, dt) in enumerate(jobs):
+                dev_w[k].copy_(host_w[dt], non_blocking=True)
+        with torch.cuda.stream(down_only):
+            for k in range(len(jobs)):
+                host_c[k].copy_(dev_c[k], non_blocking=True)
+        e1.record(copy_stream)
+        e2.record(down_only)
+        torch.cuda.synchronize()
+        if s:
+            link_ms.append(max(e0.elapsed_time(e1), e0.elapsed_time(e2)))
+    link_only_ms = statistics.median(link_ms)
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -473,7 +500,10 @@ def main():
                                  "L2 random-sector rate and Philox issue, not by HBM (DESIGN.md 3.3-3.4)"},
             "gather_probes": probes,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "particles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_value, "unit": "particles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms / args.steps, "link_only_ms": link_only_ms,
+                    "note": "pinned host buffers; copies pipelined with the deliveries on a copy stream; "
+                            "link_only_ms = the same copies with no compute (the host-link floor)"},
             "gpu_launches": launches,
             "clocks": clocks,
             "per_delivery_ms": {k: sum(v) / len(v) for k, v in per_delivery.items()},
