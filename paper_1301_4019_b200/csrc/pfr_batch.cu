@@ -210,6 +210,26 @@ __device__ __forceinline__ float2 normal2(uint32_t c0, uint32_t c1, uint32_t c2,
   return make_float2(rad * cs, rad * sn);
 }
 
+// four standard normals from one Philox call (all four words: two Box-Muller
+// pairs) -- the transition noise of particles 4q .. 4q+3 of a filter
+__device__ __forceinline__ float4 normal4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t tag, uint32_t k0,
+                                          uint32_t k1) {
+  uint32_t o[4];
+  philox4x32_10(c0, c1, c2, tag, k0, k1, o);
+  float z[4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float u1 = ((float)(o[2 * h] >> 8) + 1.0f) * (1.0f / 16777216.0f);  // (0, 1]
+    const float u2 = (float)(o[2 * h + 1] >> 8) * (1.0f / 16777216.0f);
+    const float rad = sqrtf(-2.0f * __logf(u1));
+    float sn, cs;
+    __sincosf(6.283185307179586f * u2, &sn, &cs);
+    z[2 * h] = rad * cs;
+    z[2 * h + 1] = rad * sn;
+  }
+  return make_float4(z[0], z[1], z[2], z[3]);
+}
+
 __global__ void __launch_bounds__(256) k_pf_init(PfArgs a) {
   const int64_t total = a.M * a.N;
   for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 2; p < total;
@@ -405,14 +425,15 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_pf_step(PfArgs a, int64_t t
       }
     }
     double un[4];
+    // the normals of particles e0 .. e0+3 (e0 % 4 == 0) of the filter
+    const float4 z4 = normal4((uint32_t)(e0 >> 2), (uint32_t)m, (uint32_t)t, kTagPfProp, a.k0, a.k1);
+    const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      // the normals of pair (e0 + 2q) / 2 of the filter
-      const float2 z = normal2((uint32_t)((e0 >> 1) + q), (uint32_t)m, (uint32_t)t, kTagPfProp, a.k0, a.k1);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int j = 2 * q + h;
-        const double xn = a.coeff * xo[j] + a.trans_std * (double)(h ? z.y : z.x);
+        const double xn = a.coeff * xo[j] + a.trans_std * (double)zz[j];
         const double e = (y - xn) * inv_obs;
         sw += wp[j];
         double u = wp[j] * (dens_norm * exp(-0.5 * e * e));
