@@ -198,25 +198,51 @@ __global__ void k_walk(const I* __restrict__ a, int64_t n, const int32_t* __rest
   __shared__ bool last;
   int longest = 0;
   uint32_t f = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t di = d[i];
-    if (di < n) c[i] = (int32_t)i;  // i has offspring: it keeps its slot
-    const int64_t ai = ld_idx(a, i);
-    if (ai < 0 || ai >= n) continue;
-    if (__ldg(d + ai) == i) continue;  // claim won
-    int64_t x = i, nx = di;
-    int steps = 0;
-    while (nx < n && steps <= kWalkBound) {
-      x = nx;
-      nx = __ldg(d + x);
-      ++steps;
-    }
-    if (nx < n) {
-      f |= PFR_ST_OVERFLOW;
-      hdr->overflow = 1;
+  // 4 consecutive indices per thread per iteration: their claim checks (one
+  // random d[a[i]] load each) are issued together
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i0 < n; i0 += stride) {
+    int64_t ai[4], di[4];
+    if (sizeof(I) == 4 && i0 + 4 <= n && (reinterpret_cast<uintptr_t>(a) & 15) == 0) {
+      const int4 av = __ldcs(reinterpret_cast<const int4*>(a + i0));
+      const int4 dv = __ldcs(reinterpret_cast<const int4*>(d + i0));
+      ai[0] = av.x, ai[1] = av.y, ai[2] = av.z, ai[3] = av.w;
+      di[0] = dv.x, di[1] = dv.y, di[2] = dv.z, di[3] = dv.w;
     } else {
-      c[x] = (int32_t)ai;
-      longest = max(longest, steps);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool in = i0 + j < n;
+        ai[j] = in ? ld_idx(a, i0 + j) : -1;
+        di[j] = in ? (int64_t)d[i0 + j] : n;
+      }
+    }
+    int64_t won[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool ok = ai[j] >= 0 && ai[j] < n;
+      won[j] = ok ? (int64_t)__ldg(d + ai[j]) : i0 + j;  // out of range or padding: nothing to walk
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t i = i0 + j;
+      if (i >= n) break;
+      if (di[j] < n) c[i] = (int32_t)i;  // i has offspring: it keeps its slot
+      if (ai[j] < 0 || ai[j] >= n) continue;
+      if (won[j] == i) continue;  // claim won
+      int64_t x = i, nx = di[j];
+      int steps = 0;
+      while (nx < n && steps <= kWalkBound) {
+        x = nx;
+        nx = __ldg(d + x);
+        ++steps;
+      }
+      if (nx < n) {
+        f |= PFR_ST_OVERFLOW;
+        hdr->overflow = 1;
+      } else {
+        c[x] = (int32_t)ai[j];
+        longest = max(longest, steps);
+      }
     }
   }
   status_or_warp(status, f);
@@ -474,14 +500,15 @@ cudaError_t launch_permute(const void* a, int64_t n, int idx_dtype, int32_t* c, 
   e = cudaMemsetAsync(ws.d, 0x7F, (size_t)n * sizeof(int32_t), s);
   if (e != cudaSuccess) return e;
   const int g = grid_for(n, 256);
+  const int gw = grid_for((n + 3) / 4, 256);  // k_walk: 4 indices per thread
   unsigned int* done = &ws.dv->pad[0];  // zero at workspace creation; reset by the last CTA
   if (idx_dtype == PFR_I64) {
     k_claim<int64_t><<<g, 256, 0, s>>>((const int64_t*)a, n, ws.d, max_steps, status);
-    k_walk<int64_t><<<g, 256, 0, s>>>((const int64_t*)a, n, ws.d, c, max_steps, ws.hdr, done, ws.j0, ws.j1, ws.r0,
+    k_walk<int64_t><<<gw, 256, 0, s>>>((const int64_t*)a, n, ws.d, c, max_steps, ws.hdr, done, ws.j0, ws.j1, ws.r0,
                                       ws.r1, status);
   } else {
     k_claim<int32_t><<<g, 256, 0, s>>>((const int32_t*)a, n, ws.d, max_steps, status);
-    k_walk<int32_t><<<g, 256, 0, s>>>((const int32_t*)a, n, ws.d, c, max_steps, ws.hdr, done, ws.j0, ws.j1, ws.r0,
+    k_walk<int32_t><<<gw, 256, 0, s>>>((const int32_t*)a, n, ws.d, c, max_steps, ws.hdr, done, ws.j0, ws.j1, ws.r0,
                                       ws.r1, status);
   }
   note_launch(2);
