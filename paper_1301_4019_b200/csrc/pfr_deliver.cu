@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_dv_expand(DvArgs<A> p) {
 // are L2 reads of the words written by K2.
 // kScanG: 32-index groups scanned per iteration; kThresh: queued chains that
 // trigger a step pass
-template <int kScanG, int kThresh, int kMinBlocks>
+template <int kScanG, int kThresh, int kMinBlocks, bool kSegs = false>
 __global__ void __launch_bounds__(kIpThreads, kMinBlocks) k_dv_inplace(const uint32_t* __restrict__ words,
                                                           const uint32_t* __restrict__ bitmap, int64_t n,
                                                           int32_t* __restrict__ c, int32_t* max_steps,
@@ -271,13 +271,14 @@ __global__ void __launch_bounds__(kIpThreads, kMinBlocks) k_dv_inplace(const uin
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t nn = (uint32_t)n;
   // segment mode: the index space is the listed segments, back to back
-  const uint32_t groups = segs.list ? *segs.count * segs.groups : (nn + kGroup - 1) / kGroup;
+  const uint32_t groups = kSegs ? *segs.count * segs.groups : (nn + kGroup - 1) / kGroup;
   auto pg = [&](uint32_t g) -> uint32_t {
-    return segs.list ? __ldg(segs.list + g / segs.groups) * segs.groups + g % segs.groups : g;
+    if constexpr (kSegs) return __ldg(segs.list + g / segs.groups) * segs.groups + g % segs.groups;
+    return g;
   };
   const uint32_t gw = blockIdx.x * kIpWarps + warp, nw = gridDim.x * kIpWarps;
   const uint32_t g0 = (uint32_t)((uint64_t)groups * gw / nw), g1 = (uint32_t)((uint64_t)groups * (gw + 1) / nw);
-  const uint32_t gfull = segs.list ? groups : nn / kGroup;  // groups entirely below n
+  const uint32_t gfull = kSegs ? groups : nn / kGroup;  // groups entirely below n
   int qlen = 0;
   int longest = 0;
   bool overflow = false;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(kIpThreads, kMinBlocks) k_dv_inplace(const uin
     if (qlen > kQ - 32) qlen = step_pass(Q, warp, lane, qlen, words, c, longest, overflow);
     const uint32_t gp = pg(g);
     const uint32_t x = gp * kGroup + lane;
-    const bool in = segs.list || x < nn;
+    const bool in = kSegs || x < nn;
     const uint32_t wd = in ? __ldcs(words + x) : 0u;
     scan_group(Q, warp, lane, x, in, wd, __ldg(bitmap + gp), qlen, c);
     __syncwarp();
@@ -590,7 +591,7 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
 cudaError_t launch_dv_inplace(const uint32_t* words, const uint32_t* bitmap, int64_t n, int32_t* c, DvState* state,
                               uint32_t* status, cudaStream_t s, const uint32_t* seg_list, const uint32_t* seg_count,
                               int64_t seg_len) {
-  auto kernel = k_dv_inplace<4, 64, 4>;
+  auto kernel = seg_list ? k_dv_inplace<4, 64, 4, true> : k_dv_inplace<4, 64, 4, false>;
   int occ3 = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, kernel, kIpThreads, 0);
   if (e != cudaSuccess) return e;

@@ -13,7 +13,7 @@ import paper_1301_4019_b200 as pf
 pf.config.check = False
 n = int(os.environ.get("N", 1 << 24))
 dt = np.float64 if os.environ.get("DT") == "f64" else np.float32
-g = np.random.default_rng(1); lw = g.normal(0, 1, n)
+g = np.random.default_rng(int(os.environ.get("SEED", 1))); lw = g.normal(0, 1, n)
 w = torch.from_numpy(np.exp(lw - lw.max()).astype(dt)).cuda()
 c = torch.empty(n, dtype=torch.int32, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
