@@ -17,9 +17,12 @@ g = np.random.default_rng(int(os.environ.get("SEED", 1))); lw = g.normal(0, 1, n
 w = torch.from_numpy(np.exp(lw - lw.max()).astype(dt)).cuda()
 c = torch.empty(n, dtype=torch.int32, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush2 = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
 ts = []
 for r in range(15):
     flush.zero_()
+    if os.environ.get("FLUSH") == "clean":  # evict the dirty flush lines too (read pass)
+        flush2.sum()
     torch.cuda._sleep(400_000)  # ~200 us: the host enqueues the work while the GPU spins
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(); pf.deliver(w, pf.ResamplerConfig("systematic"), pf.RngStream(r), index_dtype=torch.int32, out=c); e1.record()
