@@ -298,7 +298,7 @@ int pfr_probe_gather(const void* buf, int64_t n, int elem_bytes, int64_t gathers
                      void* stream);
 
 /* ---- batches of independent filters -----------
- * No communication: one CTA per filter.  Arrays are [filters, n] row-major. */
+ * No communication between filters.  Arrays are [filters, n] row-major. */
 
 size_t pfr_batched_workspace_bytes(int64_t filters, int64_t n);
 

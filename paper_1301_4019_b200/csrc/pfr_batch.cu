@@ -1,25 +1,30 @@
 // Batches of independent filters (SURVEY.md 8(e) "batched independent
-// filters", 8(f) N1, BASELINE config 5): no communication, one CTA per filter.
+// filters", 8(f) N1, BASELINE config 5): no communication between filters.
 //
-//   k_deliver_batched  systematic delivery of M filters of N particles:
-//                      permute_parallel(cumulative_offspring_to_ancestors(
+//   k_deliver_batched  systematic delivery of M filters of N particles, one
+//                      CTA per filter: permute_parallel(
+//                      cumulative_offspring_to_ancestors(
 //                      systematic_cumulative_offspring(w_m))) per filter
 //                      (resamplers.py:127-153, ancestry.py:69-76, 139-174)
-//   k_pf_init / k_pf_step / k_pf_resample
-//                      the bootstrap particle filter of pf.py:111-204 on the
+//   pfr_pf_run         the bootstrap particle filter of pf.py:111-204 on the
 //                      linear-Gaussian model, M filters at once: ESS-triggered
 //                      systematic resampling, the copy step fused with the
 //                      propagation (out-of-place gather x'[i] = x[c[i]], which
 //                      Eq. 2 makes equivalent to pf_copy_step, pf.py:86-97),
 //                      weighting, normalisation, log-likelihood, filtered mean.
+//                      Per step (N % 32 == 0): k_pf_expand (one CTA per tile
+//                      and filter) -> k_pf_repair (rare) -> K3 of the fused
+//                      delivery over the resampled filters -> k_pf_fixup
+//                      (rare) -> k_pf_step (one CTA per tile and filter);
+//                      other N: k_pf_resample_local -> k_pf_step (DESIGN 3.6).
 //
-// The per-filter delivery runs inside one CTA: pass 1 folds the tile
-// aggregates (tile association of pfr_tile.cuh, serial across tiles), pass 2
-// recomputes W per element, O = min(N, floor((W*N)/W_N + u)) with the exact
-// IEEE sequence, the running max (resamplers.py:150), and expands the slot
-// words (pfr_expand.cuh); pass 3 resolves the in-place ancestry by walking
-// the loser chains backwards (as k_dv_inplace).  Words live in a per-filter
-// global scratch (L2-resident for N <= 2^16).
+// segment_deliver (one CTA, one filter): pass 1 folds the tile aggregates
+// (tile association of pfr_tile.cuh, serial across tiles), pass 2 recomputes
+// W per element, O = min(N, floor((W*N)/W_N + u)) with the exact IEEE
+// sequence, the running max (resamplers.py:150), and expands the slot words
+// (pfr_expand.cuh); pass 3 resolves the in-place ancestry by walking the
+// loser chains backwards (as k_dv_inplace).  The tile-parallel PF path uses
+// the same associations, so every path gives identical results.
 #include <cstdlib>
 #include <algorithm>
 

@@ -5,8 +5,9 @@ Mirrors pfresample.pf (pf.py:41-229): the same model, the same per-step
 logic -- resample when ESS/N falls below ``ess_threshold`` through an
 in-place-valid ancestry, propagate through the transition prior, weight by
 the observation density, accumulate the log of the mean weighted density --
-for ``filters`` independent filters at once (one CTA per filter, no
-communication; independent filters split across GPUs by the caller).  The
+for ``filters`` independent filters at once (tile-parallel kernels over all
+filters, no communication between filters; independent filters split across
+GPUs by the caller).  The
 propagation noise comes from the GPU's own Philox stream, so trajectories
 are not the reference's draw for draw; ``exact_filter`` (the closed-form
 Kalman recursion, pf.py:207-229) is the end-to-end oracle, as in the
