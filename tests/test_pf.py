@@ -130,3 +130,38 @@ def test_batched_filter_inplace_paths_agree(monkeypatch, obs_std):
         np.testing.assert_array_equal(r.filtered_means, out[0].filtered_means)
         np.testing.assert_array_equal(r.log_likelihood, out[0].log_likelihood)
         np.testing.assert_array_equal(r.ess, out[0].ess)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [4096 + 32, 3 * 4096 + 64])
+def test_batched_filter_ragged_tiles_paths_agree(monkeypatch, n):
+    """A ragged last tile (N % 4096 != 0, N % 32 == 0): the tile-parallel
+    resample + global in-place pass equals the per-filter path bit for bit."""
+    import paper_1301_4019_b200 as pf
+
+    model = LinearGaussianModel(coeff=0.8, trans_std=0.7, obs_std=0.3)
+    ys = np.stack([simulate_observations(model, 10, s) for s in range(5)])
+    out = []
+    for path in ("0", "1"):
+        monkeypatch.setenv("PFR_PF_PATH", path)
+        out.append(pf.pf_run(model, ys, n, ess_threshold=1.0, seed=2))
+    assert out[0].resampled[:, 1:].all()
+    np.testing.assert_array_equal(out[0].filtered_means, out[1].filtered_means)
+    np.testing.assert_array_equal(out[0].log_likelihood, out[1].log_likelihood)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1000, 999])
+def test_batched_filter_unaligned_sizes_track_kalman(n):
+    """N % 32 != 0 (per-filter in-place pass) and odd N (scalar step path)."""
+    import paper_1301_4019_b200 as pf
+
+    model = LinearGaussianModel(coeff=0.9, trans_std=1.0, obs_std=0.8)
+    y = simulate_observations(model, 30, 5)
+    exact = exact_filter(model, y)
+    res = pf.pf_run(model, y, n, "systematic", 0.5, seed=4, filters=64)
+    assert res.resampled.any()
+    ll = res.log_likelihood
+    se = ll.std(ddof=1) / math.sqrt(len(ll))
+    assert abs(ll.mean() - exact.log_likelihood) < 5 * se + 0.2, (ll.mean(), exact.log_likelihood, se)
+    assert np.abs(res.filtered_means.mean(axis=0) - exact.means).max() < 0.1
