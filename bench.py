@@ -5,12 +5,16 @@ stratified, systematic, Metropolis(B=32), rejection(sup_w = max w) -- at
 N = 2^20 on i.i.d. log-normal (sigma = 1) weights, float32 AND float64.  One
 step = the ten deliveries (resample + permute to an in-place-valid ancestry,
 the timed region of the reference's bench.py:155-161), i.e. 10 * 2^20
-particles.  Weights are resident in HBM before timing; L2 is flushed
-(256 MiB write) before every delivery and every delivery is timed with CUDA
-events on the launching stream; the flush is outside the timed region, and a
-short GPU spin between the flush and the start event lets the host enqueue
-the delivery so that the events see device work only (the host-side cost of
-the API is what `e2e` measures).
+particles.  The ten deliveries are independent filters' resampling and run
+concurrently, each on its own stream with its own copy of the weights (the
+reference's bench runs its cells concurrently too, bench.py:226-230); weights
+are resident in HBM before timing; L2 is flushed (256 MiB write) before every
+step, outside the timed region; a GPU spin between the flush and the start
+event lets the host enqueue the whole step so that the CUDA events see device
+work only (the host-side cost of the API is what `e2e` measures).  The same
+ten deliveries are also timed one at a time (L2 flushed before each):
+`sequential` and `per_delivery_ms`, from which the dominant kernel's roofline
+is computed.
 
 Also reported (north-star targets): systematic delivery
 and Metropolis(B=32) at N = 2^24 float32 against the measured HBM roofline.
@@ -48,6 +52,7 @@ N_DEFAULT = 1 << 20
 B_STEPS = 32
 SIGMA = 1.0
 PREROLL_CYCLES = 400_000  # ~0.2 ms GPU spin before each timed delivery (outside the events)
+STEP_PREROLL_CYCLES = 4_000_000  # ~2 ms spin before a concurrent step: the host enqueues all ten deliveries
 
 
 def peaks():
@@ -207,7 +212,9 @@ def workload_config(n, world):
     return {"workload": "configs[1]: multinomial/stratified/systematic/metropolis(B=32)/rejection(sup_w=max w), "
                         f"N=2^{int(math.log2(n))}, f32 and f64, log-normal sigma={SIGMA}",
             "n_particles": n, "deliveries_per_step": len(ALGS) * len(DTYPES), "metropolis_B": B_STEPS,
-            "rng": "own Philox4x32-10 (rng_mode='philox')", "l2": "flushed (256 MiB write) before every delivery",
+            "rng": "own Philox4x32-10 (rng_mode='philox')",
+            "l2": "flushed (256 MiB write) before every step (and before every delivery of the sequential leg)",
+            "concurrency": "the ten deliveries of a step on ten streams (independent filters)",
             "parallelism": f"replicas x{world} (independent filters per GPU)"}
 
 
@@ -317,8 +324,64 @@ def main():
         all_evs.append(timed_step(s, parts))
         all_parts.append(parts)
     torch.cuda.synchronize()
+    seq_launches = int(L.lib().pfr_launch_count(1))
+
+    # ---------------- the step: ten independent deliveries at once ----------------
+    # Each delivery is an independent filter's resampling; they run on their
+    # own streams (each (device, stream) has its own workspace and status
+    # words), as the reference's bench runs its cells concurrently
+    # (bench.py:226-230).  Every delivery reads its own copy of the weights;
+    # L2 is flushed before every step; the GPU spins while the host enqueues
+    # the step, so the events time device work.
+    jobs = [(i, alg, j, dt) for i, alg in enumerate(ALGS) for j, dt in enumerate(DTYPES)]
+    conc_streams = [torch.cuda.Stream(device=dev) for _ in jobs]
+    conc_w = [weights[dt].clone() for (_, _, _, dt) in jobs]
+    conc_out = [torch.empty(n, dtype=torch.int32, device=dev) for _ in jobs]
+
+    def run_delivery(alg, dt, w, rs, out):
+        if alg in ("systematic", "stratified"):
+            return pf.deliver(w, cfgs[alg], rs, index_dtype=torch.int32, out=out)
+        if alg == "multinomial":
+            a = pf.multinomial_ancestors(w, rs, index_dtype=torch.int32)
+        elif alg == "metropolis":
+            a = pf.metropolis_ancestors(w, B_STEPS, rs, index_dtype=torch.int32)
+        else:
+            a = pf.rejection_ancestors(w, sup[dt], rs, index_dtype=torch.int32)
+        return pf.permute_parallel(a, index_dtype=torch.int32)
+
+    def concurrent_step(step):
+        flush.zero_()
+        torch.cuda._sleep(STEP_PREROLL_CYCLES)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        done = []
+        for k, (i, alg, j, dt) in enumerate(jobs):
+            sk = conc_streams[k]
+            sk.wait_event(e0)
+            with torch.cuda.stream(sk):
+                run_delivery(alg, dt, conc_w[k], pf.RngStream(step, (rank, i, j)), conc_out[k])
+                ev = torch.cuda.Event()
+                ev.record(sk)
+            done.append(ev)
+        for ev in done:
+            stream.wait_event(ev)
+        e1.record(stream)
+        return e0, e1
+
+    for s in range(args.warmup):
+        concurrent_step(30_000 + s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    L.lib().pfr_launch_count(1)
+    conc_evs = [concurrent_step(s) for s in range(args.steps)]
+    torch.cuda.synchronize()
     t_wall1 = time.time()
     launches = int(L.lib().pfr_launch_count(1))
+    conc_ms = sum(a.elapsed_time(b) for a, b in conc_evs)
+
     total_ms = 0.0
     for evs in all_evs:
         for name, a, b in evs:
@@ -330,12 +393,14 @@ def main():
             kernel_parts.setdefault(name, []).append(a.elapsed_time(b))
     status = L.status_all()
     if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([total_ms, conc_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
+        total_ms, conc_ms = float(t[0].item()), float(t[1].item())
+    seq_ms_per_step = total_ms / args.steps
+    ms_per_step = conc_ms / args.steps
     units_per_step = len(ALGS) * len(DTYPES) * n
     value = world * units_per_step / (ms_per_step * 1e-3)
+    seq_value = world * units_per_step / (seq_ms_per_step * 1e-3)
 
     # dominant kernel of the step (largest share), roofline from live events
     dom_name, dom_ms = None, 0.0
@@ -372,7 +437,6 @@ def main():
     # the same uploads and downloads with no compute take ~2.0 ms per step
     # (H2D and D2H share the link; reported as `link_only_ms`).
     host_w = {dt: weights[dt].cpu().pin_memory() for dt in DTYPES}
-    jobs = [(i, alg, j, dt) for i, alg in enumerate(ALGS) for j, dt in enumerate(DTYPES)]
     host_c = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in jobs]
     dev_w = [torch.empty_like(weights[dt]) for (_, _, _, dt) in jobs]
     dev_c = [torch.empty(n, dtype=torch.int32, device=dev) for _ in jobs]
@@ -381,19 +445,9 @@ def main():
     d2h = len(jobs) * n * 4
     e2e_ms = 0.0
 
-    def e2e_delivery(alg, dt, w, rs, out):
-        if alg in ("systematic", "stratified"):
-            return pf.deliver(w, cfgs[alg], rs, index_dtype=torch.int32, out=out)
-        if alg == "multinomial":
-            a = pf.multinomial_ancestors(w, rs, index_dtype=torch.int32)
-        elif alg == "metropolis":
-            a = pf.metropolis_ancestors(w, B_STEPS, rs, index_dtype=torch.int32)
-        else:
-            a = pf.rejection_ancestors(w, sup[dt], rs, index_dtype=torch.int32)
-        return pf.permute_parallel(a, index_dtype=torch.int32)
-
     for s in range(args.warmup + args.steps):
         flush.zero_()
+        torch.cuda._sleep(STEP_PREROLL_CYCLES)
         copy_stream.wait_stream(stream)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -406,10 +460,12 @@ def main():
                 ev.record(copy_stream)
             up.append(ev)
         for k, (i, alg, j, dt) in enumerate(jobs):
-            stream.wait_event(up[k])
-            c = e2e_delivery(alg, dt, dev_w[k], pf.RngStream(50_000 + s, (rank, i, j)), dev_c[k])
-            done = torch.cuda.Event()
-            done.record(stream)
+            sk = conc_streams[k]
+            sk.wait_event(up[k])
+            with torch.cuda.stream(sk):
+                c = run_delivery(alg, dt, dev_w[k], pf.RngStream(50_000 + s, (rank, i, j)), dev_c[k])
+                done = torch.cuda.Event()
+                done.record(sk)
             c.record_stream(copy_stream)
             with torch.cuda.stream(copy_stream):
                 copy_stream.wait_event(done)
@@ -498,12 +554,15 @@ def main():
                          "note": "algorithmic bytes count every proposal's weight gather (SURVEY 8(d)); the "
                                  "gathers hit L2 (N=2^20 weights are L2 resident): the kernel is bound by the "
                                  "L2 random-sector rate and Philox issue, not by HBM (DESIGN.md 3.3-3.4)"},
+            "sequential": {"ms_per_step": seq_ms_per_step, "value": seq_value, "gpu_launches": seq_launches,
+                           "note": "the same ten deliveries one at a time, L2 flushed before each"},
             "gather_probes": probes,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "particles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms / args.steps, "link_only_ms": link_only_ms,
-                    "note": "pinned host buffers; copies pipelined with the deliveries on a copy stream; "
-                            "link_only_ms = the same copies with no compute (the host-link floor)"},
+                    "note": "pinned host buffers; copies on a copy stream pipelined with the ten deliveries "
+                            "(each on its own stream); link_only_ms = the same copies with no compute "
+                            "(the host-link floor)"},
             "gpu_launches": launches,
             "clocks": clocks,
             "per_delivery_ms": {k: sum(v) / len(v) for k, v in per_delivery.items()},

@@ -256,20 +256,26 @@ def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
-# --- workspace + status (per device, grow-only) -----------------------------
+# --- workspace + status (per device and stream, grow-only) ------------------
+# Calls on different streams may run concurrently (independent filters on
+# their own streams), so each (device, stream) owns its workspace and its
+# status words; calls on one stream are ordered by the stream.
 
 _ws = {}
 _status = {}
+_ws_lock = threading.Lock()
 
 
 def workspace(n: int) -> tuple[int, int]:
     dev = device()
+    key = (dev.index, stream_handle())
     need = int(lib().pfr_workspace_bytes(OP_ANY, int(n), 0))
-    cur = _ws.get(dev.index)
+    cur = _ws.get(key)
     if cur is None or cur.numel() < need:
         # zero-filled once: the fused delivery keeps its counters in it (pfr.h)
         cur = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
-        _ws[dev.index] = cur
+        with _ws_lock:
+            _ws[key] = cur
     return cur.data_ptr(), cur.numel()
 
 
@@ -304,9 +310,10 @@ def _ring() -> _StatusRing:
     rings = getattr(_rings, "by_dev", None)
     if rings is None:
         rings = _rings.by_dev = {}
-    r = rings.get(dev.index)
+    key = (dev.index, stream_handle())
+    r = rings.get(key)
     if r is None:
-        r = rings[dev.index] = _StatusRing(dev)
+        r = rings[key] = _StatusRing(dev)
     return r
 
 
@@ -320,9 +327,15 @@ def new_status() -> torch.Tensor:
 
 
 def status_all() -> int:
-    """OR of every status word handed out since the ring last wrapped."""
-    r = _ring()
-    return int(np.bitwise_or.reduce(r.words[: max(r.next, 1)].cpu().numpy())) & 0xFFFFFFFF
+    """OR of every status word this thread handed out on the current device
+    (all streams) since each ring last wrapped."""
+    dev = device()
+    _ring()
+    acc = 0
+    for (d, _), r in getattr(_rings, "by_dev", {}).items():
+        if d == dev.index:
+            acc |= int(np.bitwise_or.reduce(r.words[: max(r.next, 1)].cpu().numpy()))
+    return acc & 0xFFFFFFFF
 
 
 def read_status(st: torch.Tensor) -> int:

@@ -121,10 +121,11 @@ _ws_pf = {}
 
 def _workspace(key, nbytes):
     dev = L.device()
-    cur = _ws_pf.get((dev.index, key))
+    k = (dev.index, key, L.stream_handle())  # per stream: concurrent calls on other streams
+    cur = _ws_pf.get(k)
     if cur is None or cur.numel() < nbytes:
         cur = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
-        _ws_pf[(dev.index, key)] = cur
+        _ws_pf[k] = cur
     return cur
 
 
