@@ -527,6 +527,11 @@ def main():
             targets.update(c5_targets(pf, torch, dev, stream, rank, world))
         except Exception as exc:
             targets["c5_error"] = f"{type(exc).__name__}: {exc}"[:300]
+        if rank == 0:
+            try:
+                targets.update(c3_targets(pf, torch, dev, stream))
+            except Exception as exc:
+                targets["c3_error"] = f"{type(exc).__name__}: {exc}"[:300]
 
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu = None
@@ -770,6 +775,95 @@ def c5_targets(pf, torch, dev, stream, rank, world, filters=4096, n_log2=16, ste
                                          "copy of means/ESS/log-likelihood (the pf_run API call)",
         "cpu_reference_note": "SURVEY.md 6: the reference pf_run takes 1.95 s per filter (N=2^16, T=100) on "
                               "one core, i.e. ~2.2 core-hours for 4096 filters"}} if rank == 0 else {}
+
+
+# the exact 1^T P^B oracle at N=2^22 (E[o_max]/(N p_max))
+C3_EXACT_BIAS = {0.5: {1: .178, 4: .386, 16: .810, 32: .960, 64: .998, 256: 1.000},
+                 1.0: {1: .016, 4: .040, 16: .128, 32: .234, 64: .408, 256: .875},
+                 2.0: {1: .001, 4: .002, 16: .007, 32: .014, 64: .028, 256: .107}}
+
+
+def c3_targets(pf, torch, dev, stream, n_log2=22, reps=8, sigmas=(0.5, 1.0, 1.5, 2.0, 3.0, 4.0),
+               steps=(1, 4, 16, 32, 64, 256)):
+    """BASELINE.json configs[2]: the log-weight sigma sweep at N = 2^22 f32.
+    Metropolis bias vs B -- E[o_max]/(N p_max) over `reps` own-stream
+    replicates (o_max: offspring of the heaviest particle), next to the exact
+    1^T P^B values of SURVEY A.9 where the survey lists them -- and its
+    recipe B (metropolis_num_steps, epsilon = p*/100); rejection acceptance
+    N / sum(trips) against the analytic sum(w) / (N sup_w) with sup_w = max w
+    = 1.  Device times are medians of CUDA events (no L2 flush: behaviour
+    sweep, not a bandwidth number)."""
+    n = 1 << n_log2
+    out = {}
+
+    def ev_time(fn):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return r, e0.elapsed_time(e1)
+
+    for sigma in sigmas:
+        g = np.random.default_rng(int(7000 + 100 * sigma))
+        lw = g.normal(0.0, sigma, n)
+        w64 = np.exp(lw - lw.max())
+        w = torch.from_numpy(w64.astype(np.float32)).to(dev)
+        wsum = float(w.double().sum())
+        jmax = int(torch.argmax(w))
+        p_max = float(w[jmax]) / wsum
+        row = {"p_max": p_max, "ess_over_n": wsum ** 2 / float((w.double() ** 2).sum()) / n}
+        bias = {}
+        for b in steps:
+            omax, ts = [], []
+            for r in range(reps):
+                a, t = ev_time(lambda: pf.metropolis_ancestors(w, b, pf.RngStream(r, (int(sigma * 10), b)),
+                                                              index_dtype=torch.int32))
+                omax.append(int((a == jmax).sum()))
+                ts.append(t)
+            m = float(np.mean(omax))
+            se = float(np.std(omax, ddof=1) / math.sqrt(reps)) if reps > 1 else None
+            cell = {"bias": m / (n * p_max), "bias_se": se / (n * p_max) if se is not None else None,
+                    "kernel_ms": float(np.median(ts)), "ggather_per_s": b * n / (float(np.median(ts)) * 1e-3) / 1e9}
+            ex = C3_EXACT_BIAS.get(sigma, {}).get(b)
+            if ex is not None:
+                cell["exact_survey"] = ex
+            bias[str(b)] = cell
+        row["metropolis"] = bias
+        try:
+            b_rec = int(pf.metropolis_num_steps(p_max, p_max / 100.0, n))
+        except ValueError as exc:  # the recipe's own domain errors (resamplers.py:168-201)
+            b_rec = None
+            rec = {"error": str(exc)[:200]}
+        if b_rec is not None:
+            rec = {"B": b_rec}
+        if b_rec is not None and b_rec * n <= (1 << 38):  # <= ~1 s per replicate
+            omax, ts = [], []
+            for r in range(2):
+                a, t = ev_time(lambda: pf.metropolis_ancestors(w, b_rec, pf.RngStream(100 + r, (int(sigma * 10),)),
+                                                              index_dtype=torch.int32))
+                omax.append(int((a == jmax).sum()))
+                ts.append(t)
+            rec.update({"bias": float(np.mean(omax)) / (n * p_max), "kernel_ms": float(np.median(ts))})
+        elif b_rec is not None:
+            rec["skipped"] = "B * N above 2^38 gathers per replicate"
+        row["metropolis_recipe"] = rec
+        # rejection with the tight bound sup_w = max w = 1
+        expected_trips = n / wsum
+        m = n if expected_trips * n <= 2e11 else (1 << 16)  # huge sigma: a 2^16-slot sample
+        wr = w if m == n else w[:m].contiguous()
+        sup = float(wr.max())
+        (a, trips), t = ev_time(lambda: pf.rejection_ancestors(wr, sup, pf.RngStream(9, (int(sigma * 10),)),
+                                                               return_trips=True, max_rounds=10 ** 9,
+                                                               index_dtype=torch.int32))
+        tsum = float(trips.double().sum())
+        row["rejection"] = {"acceptance": m / tsum, "analytic": float(wr.double().sum()) / (m * sup),
+                            "mean_trips": tsum / m, "slots": m, "ms": t,
+                            "gtrips_per_s": tsum / (t * 1e-3) / 1e9}
+        out[f"sigma={sigma}"] = row
+        del w, a
+    return {f"c3_sigma_sweep_2^{n_log2}_f32": out}
 
 
 if __name__ == "__main__":
