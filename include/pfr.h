@@ -240,6 +240,16 @@ int pfr_copy_particles(double* x, int64_t n, int64_t width, const int32_t* c, vo
 int pfr_metropolis_range(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng, int64_t chain_begin,
                          int64_t chain_count, int32_t* a, uint32_t* status, void* stream);
 
+/* rejection_ancestors / rejection_ancestors_capped (resamplers.py:237-310)
+ * for slots [slot_begin, slot_begin + slot_count) of the N-slot resampler
+ * over the full weight vector w[n]: a, trips, out_w indexed slot -
+ * slot_begin; every slot draws from its global number's PHILOX stream, so
+ * the union over ranks equals the single-GPU result (rejection
+ * partitions the output slots over the all-gathered weights). */
+int pfr_rejection_range(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
+                        int64_t max_rounds, int64_t slot_begin, int64_t slot_count, int32_t* a, int32_t* trips,
+                        void* out_w, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
 /* Cumulative offspring of this shard's parents in global slot numbers
  * (_offspring_from_positions, resamplers.py:139-153): W = prefix + W_loc[i]
  * (W_loc = the shard's inclusive scan in float64), r = (W*N)/total,

@@ -75,6 +75,7 @@ _SIGNATURES = {
     "pfr_multinomial": ([_P, _I64, _INT, _INT, _RNGP, _P, _INT, _P, _P, _P, _SZ, _P], _INT),
     "pfr_metropolis": ([_P, _I64, _INT, _I64, _RNGP, _P, _P, _INT, _P, _P, _P, _SZ, _P], _INT),
     "pfr_rejection": ([_P, _I64, _INT, _DBL, _DBL, _RNGP, _I64, _P, _P, _P, _P, _P, _SZ, _P], _INT),
+    "pfr_rejection_range": ([_P, _I64, _INT, _DBL, _DBL, _RNGP, _I64, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P], _INT),
     "pfr_cumulative_to_ancestors": ([_P, _I64, _INT, _P, _P, _P, _SZ, _P], _INT),
     "pfr_ancestors_to_offspring": ([_P, _I64, _INT, _P, _P, _P], _INT),
     "pfr_prepermute": ([_P, _I64, _INT, _P, _P, _P], _INT),

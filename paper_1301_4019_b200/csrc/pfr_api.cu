@@ -304,6 +304,24 @@ int pfr_rejection(const void* w, int64_t n, int dtype, double bound, double cap,
   return PFR_OK;
 }
 
+int pfr_rejection_range(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
+                        int64_t max_rounds, int64_t slot_begin, int64_t slot_count, int32_t* a, int32_t* trips,
+                        void* out_w, uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && (a || slot_count == 0) && status, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(rng && rng->mode == PFR_RNG_PHILOX, "slot ranges need the PHILOX stream");
+  PFR_REQUIRE(slot_begin >= 0 && slot_count >= 0 && slot_begin + slot_count <= n, "slot range outside [0, N)");
+  const double b = cap > 0 ? cap : bound;
+  if (!(b > 0) || !std::isfinite(b)) return fail(PFR_E_ARG, "weight bound must be finite and positive");
+  if (cap > 0) PFR_REQUIRE(out_w || slot_count == 0, "capped rejection needs out_w");
+  if (slot_count == 0) return PFR_OK;
+  PFR_WS(PFR_OP_REJECTION);
+  PFR_CHECK_LAUNCH(launch_rejection(w, n, dtype, bound, cap, rng, max_rounds, a, trips, out_w, status, ws,
+                                    (cudaStream_t)stream, slot_begin, slot_count),
+                   "pfr_rejection_range");
+  return PFR_OK;
+}
+
 int pfr_cumulative_to_ancestors(const void* O, int64_t n, int idx_dtype, int32_t* a, uint32_t* status, void* ws_ptr,
                                 size_t ws_bytes, void* stream) {
   (void)ws_ptr;

@@ -96,7 +96,8 @@ cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps
                               uint32_t* status, cudaStream_t s, int64_t c_begin = 0, int64_t c_count = -1);
 cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
                              int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
-                             const Workspace& ws, cudaStream_t s);
+                             const Workspace& ws, cudaStream_t s, int64_t s_begin = 0,
+                             int64_t s_count = -1);
 
 // launchers (pfr_shard.cu): weight-sharded single filter
 cudaError_t launch_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double prefix, double total,

@@ -198,6 +198,8 @@ struct RejArgs {
   double cap;  // > 0: capped variant, v = min(w, cap), bound = cap
   uint32_t k0, k1, threshold;
   uint32_t max_trips;
+  int64_t s0;     // first slot of this launch (global number: RNG counters, trip 0)
+  int64_t count;  // slots of this launch; outputs are indexed slot - s0
   int32_t* a;
   int32_t* trips;
   T* out_w;
@@ -269,19 +271,19 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_rejection_philox(RejArgs<T>
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(A.next_chunk, (unsigned long long)kRejChunk);
         base = __shfl_sync(0xffffffffu, base, 0);
-        if ((int64_t)base >= A.n) {
+        if ((int64_t)base >= A.count) {
           exhausted = true;
           break;
         }
         chunk_next = (int64_t)base;
-        chunk_end = min((int64_t)base + kRejChunk, A.n);
+        chunk_end = min((int64_t)base + kRejChunk, A.count);
       }
       const int rank = __popc(idle & ((1u << lane) - 1));
       const int take = min((int64_t)__popc(idle), chunk_end - chunk_next);
       if (slot < 0 && rank < take) {
         slot = chunk_next + rank;
         trip = 0;
-        rej_draws<T, kRejBatch>(A, (uint32_t)slot, 0u, cur);
+        rej_draws<T, kRejBatch>(A, (uint32_t)(A.s0 + slot), 0u, cur);
       }
       chunk_next += take;
       idle = __ballot_sync(0xffffffffu, slot < 0);
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_rejection_philox(RejArgs<T>
       for (int q = 0; q < kRejBatch; ++q) wj[q] = ldg(A.w + cur.j[q]);
       // next batch's draws overlap the gathers' latency
       RejBatch<T, kRejBatch> nxt;
-      rej_draws<T, kRejBatch>(A, (uint32_t)slot, trip + kRejBatch, nxt);
+      rej_draws<T, kRejBatch>(A, (uint32_t)(A.s0 + slot), trip + kRejBatch, nxt);
       int done = -1;  // batch position of the first accepting trip
 #pragma unroll
       for (int q = kRejBatch - 1; q >= 0; --q) {
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_rejection_philox(RejArgs<T>
         slot = -1;
       } else if (done == -2) {
         flags |= PFR_ST_NOPROGRESS;
-        A.a[slot] = (int32_t)slot;
+        A.a[slot] = (int32_t)(A.s0 + slot);
         if (A.trips) A.trips[slot] = (int32_t)A.max_trips;
         if (kCapped) A.out_w[slot] = T(1);
         slot = -1;
@@ -572,7 +574,8 @@ cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps
 
 cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
                              int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
-                             const Workspace& ws, cudaStream_t s) {
+                             const Workspace& ws, cudaStream_t s, int64_t s_begin, int64_t s_count) {
+  if (s_count < 0) s_count = n - s_begin;
   if (!rng || rng->mode != PFR_RNG_PHILOX) return cudaErrorNotSupported;
   unsigned long long* next = reinterpret_cast<unsigned long long*>(&ws.hdr->cell[2]);
   cudaError_t e = cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
@@ -605,14 +608,14 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
   } while (0)
   if (dtype == PFR_F64) {
     RejArgs<double> A{(const double*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
-                      a, trips, (double*)out_w, next, status};
+                      s_begin, s_count, a, trips, (double*)out_w, next, status};
     if (cap > 0)
       PFR_REJ_DISPATCH(double, true);
     else
       PFR_REJ_DISPATCH(double, false);
   } else {
     RejArgs<float> A{(const float*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
-                     a, trips, (float*)out_w, next, status};
+                     s_begin, s_count, a, trips, (float*)out_w, next, status};
     if (cap > 0)
       PFR_REJ_DISPATCH(float, true);
     else

@@ -259,6 +259,31 @@ class CudaShardOps:
                int(c_begin), int(c_count), a.data_ptr(), self.status.data_ptr(), L.stream_handle())
         return a
 
+    def rejection_range(self, w_full, config, rng, mode, s_begin, s_count):
+        """rejection_ancestors(_capped) for slots [s_begin, s_begin + s_count)
+        of the full weight vector (resamplers.py:237-310), global parent
+        numbers; PHILOX stream only (like the single-GPU rejection)."""
+        from .resamplers import MAX_REJECTION_ROUNDS
+
+        if mode not in (None, "philox"):
+            raise NotImplementedError("sharded rejection uses the GPU's own Philox stream")
+        w_full = L.as_weights(w_full)
+        capped = config.algorithm == "rejection-capped"
+        if capped and config.sup_v is None:
+            raise ValueError("rejection-capped requires sup_v")
+        sup = config.sup_w if config.sup_w is not None else float(w_full.max())  # as resample_ancestors
+        bound = float(config.sup_v if capped else sup)
+        a = torch.empty(max(s_count, 1), dtype=torch.int32, device=self.dev)
+        out_w = torch.empty(max(s_count, 1), dtype=w_full.dtype, device=self.dev) if capped else None
+        k0, k1 = as_stream(rng).key()
+        r = L.PfrRng(k0, k1, L.RNG_PHILOX, 0)
+        ws, wsb = L.workspace(w_full.numel())
+        L.call("pfr_rejection_range", w_full.data_ptr(), w_full.numel(), L.dtype_code(w_full),
+               0.0 if capped else bound, bound if capped else 0.0, r, int(MAX_REJECTION_ROUNDS), int(s_begin),
+               int(s_count), a.data_ptr(), None, L.ptr(out_w), self.status.data_ptr(), ws, wsb,
+               L.stream_handle())
+        return a[:s_count]
+
     def full_ancestors(self, w_full, config, rng, mode):
         from .resamplers import resample_ancestors
 
@@ -316,8 +341,8 @@ def deliver_sharded(w_local, config, rng, *, comm, ops=None, rng_mode=None, unif
     slice c[base:base+n_local] (global parent indices, int32).
 
     systematic / stratified: weight-sharded (see module docstring);
-    metropolis: chain-partitioned over the all-gathered weights;
-    multinomial / rejection: replicated over the all-gathered weights."""
+    metropolis / rejection: chains / slots partitioned over the all-gathered
+    weights; multinomial: replicated over the all-gathered weights."""
     ops = ops or CudaShardOps()
     alg = config.algorithm
     if alg in ("systematic", "stratified"):
@@ -331,6 +356,9 @@ def deliver_sharded(w_local, config, rng, *, comm, ops=None, rng_mode=None, unif
         a_loc = metropolis_sharded(w_local, config, rng, comm=comm, ops=ops, rng_mode=rng_mode, _w_full=w_full,
                                    _sizes=sizes)
         a_full = comm.all_gather_var(a_loc)
+    elif alg in ("rejection", "rejection-capped"):
+        # slots partitioned like Metropolis' chains
+        a_full = comm.all_gather_var(ops.rejection_range(w_full, config, rng, rng_mode, base, n_loc))
     else:
         a_full = ops.full_ancestors(w_full, config, rng, rng_mode)
     c_full = ops.permute(torch.as_tensor(a_full))

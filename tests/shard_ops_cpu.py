@@ -129,6 +129,14 @@ class NumpyShardOps:
         a = orc.metropolis_stream(_np(w_full), b, rng.seed, rng.ids)
         return torch.from_numpy(a[c_begin: c_begin + c_count].astype(np.int32))
 
+    def rejection_range(self, w_full, config, rng, mode, s_begin, s_count):
+        # the reference's rejection loop is round-synchronous over the whole
+        # pending set (not slot-separable): the CPU stand-in slices the full run
+        w = _np(w_full)
+        sup = config.sup_w if config.sup_w is not None else float(w.max())
+        a = orc.rejection_stream(w, sup, rng.seed, rng.ids)[0]
+        return torch.from_numpy(a[s_begin: s_begin + s_count].astype(np.int32))
+
     def full_ancestors(self, w_full, config, rng, mode):
         w = _np(w_full)
         if config.algorithm == "multinomial":

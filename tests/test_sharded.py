@@ -75,11 +75,12 @@ def sharded_threads(w, world, alg, rs, ops_factory, cuts=None, **kw):
     cuts = split(w.size, world, 7) if cuts is None else cuts
     comms = ThreadComm.group(world)
     cfg = ResamplerConfig(alg, b=kw.pop("b", None))
+    mode = kw.pop("rng_mode", "numpy")
 
     def fn(r):
         ops = ops_factory()
         shard = torch.from_numpy(w[cuts[r]: cuts[r + 1]].copy())
-        return deliver_sharded(shard, cfg, rs, comm=comms[r], ops=ops, rng_mode="numpy", return_max_steps=True, **kw)
+        return deliver_sharded(shard, cfg, rs, comm=comms[r], ops=ops, rng_mode=mode, return_max_steps=True, **kw)
 
     res = run_threads(world, fn)
     c = np.concatenate([x[0].cpu().numpy() for x in res]).astype(np.int64)
@@ -119,6 +120,16 @@ def test_threads_ancestry_algorithms(alg):
     c, _ = sharded_threads(w, 3, alg, rs, NumpyShardOps, b=8 if alg == "metropolis" else None)
     want = orc.deliver(w, alg, rs.seed, rs.ids, b=8)
     np.testing.assert_array_equal(c, want)
+
+
+def test_threads_rejection_slots_partitioned():
+    """Rejection partitions the output slots over the all-gathered weights
+    (SURVEY 8(e)); the CPU stand-in slices the reference loop."""
+    w = int_weights(1024, 33)
+    rs = RngStream(8, (2,))
+    c, _ = sharded_threads(w, 3, "rejection", rs, NumpyShardOps)
+    a = orc.rejection_stream(w, float(w.max()), rs.seed, rs.ids)[0]
+    np.testing.assert_array_equal(c, orc.permute(a))
 
 
 def test_threads_errors_raise_on_every_rank():
@@ -242,4 +253,21 @@ def test_gpu_sharded_metropolis_bit_identical():
     rs = RngStream(11)
     c, _ = sharded_threads(w, 4, "metropolis", rs, CudaShardOps, b=32)
     single = pf.deliver(w, ResamplerConfig("metropolis", b=32), rs, rng_mode="numpy").cpu().numpy()
+    np.testing.assert_array_equal(c, single)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_gpu_sharded_rejection_bit_identical(world):
+    """Slot-partitioned rejection (pfr_rejection_range on each rank's slots,
+    every slot on its global Philox stream) equals the single-GPU delivery."""
+    import paper_1301_4019_b200 as pf
+    from paper_1301_4019_b200.sharded import CudaShardOps
+
+    g = np.random.default_rng(5)
+    lw = g.normal(0, 1, 1 << 16)
+    w = np.exp(lw - lw.max()).astype(np.float32)
+    rs = RngStream(12, (world,))
+    c, _ = sharded_threads(w, world, "rejection", rs, CudaShardOps, rng_mode="philox")
+    single = pf.deliver(w, ResamplerConfig("rejection"), rs, rng_mode="philox").cpu().numpy()
     np.testing.assert_array_equal(c, single)
