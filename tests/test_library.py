@@ -101,6 +101,17 @@ def test_argument_validation_without_gpu(lib):
     rc = lib.pfr_rejection(ctypes.addressof(buf), 4, L.F32, 0.0, 0.0, L.PfrRng(0, 0, 0, 0), 10,
                            ctypes.addressof(buf), None, None, ctypes.addressof(buf), None, 0, None)
     assert rc == L.E_ARG and b"finite and positive" in lib.pfr_last_error()
+    philox = L.PfrRng(0, 0, L.RNG_PHILOX, 0)
+    rc = lib.pfr_rejection_range(ctypes.addressof(buf), 4, L.F32, 1.0, 0.0, philox, 10, 3, 2,
+                                 ctypes.addressof(buf), None, None, ctypes.addressof(buf), None, 0, None)
+    assert rc == L.E_ARG and b"slot range" in lib.pfr_last_error()
+    rc = lib.pfr_rejection_range(ctypes.addressof(buf), 4, L.F32, 1.0, 0.0, L.PfrRng(0, 0, L.RNG_NUMPY, 0), 10, 0,
+                                 2, ctypes.addressof(buf), None, None, ctypes.addressof(buf), None, 0, None)
+    assert rc == L.E_ARG and b"PHILOX" in lib.pfr_last_error()
+    rc = lib.pfr_probe_gather(ctypes.addressof(buf), 3, 4, 1, ctypes.addressof(buf), None)
+    assert rc == L.E_ARG and b"power of two" in lib.pfr_last_error()
+    rc = lib.pfr_probe_gather(ctypes.addressof(buf), 4, 2, 1, ctypes.addressof(buf), None)
+    assert rc == L.E_ARG and b"elem_bytes" in lib.pfr_last_error()
 
 
 def test_host_scalars():
