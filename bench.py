@@ -651,6 +651,17 @@ def north_star_targets(pf, torch, dev, stream, flush, hbm, reps=10, probes=None)
     out["systematic_delivery_2^24_f32"] = {"us": t * 1e3, "particles_per_s": n / (t * 1e-3),
                                            "algorithmic_bytes": b, "achieved_gbs": b / (t * 1e-3) / 1e9,
                                            "frac": b / (t * 1e-3) / 1e9 / hbm, "target_frac": 0.70}
+    # the same delivery from log-weights: fused (exp(lw - max) on load) vs
+    # logweights_to_weights + deliver
+    lw = torch.log(w)
+    t_f = timeit(lambda r: pf.deliver(lw, cfg, pf.RngStream(r), index_dtype=torch.int32, out=c, log_weights=True))
+    t_2 = timeit(lambda r: pf.deliver(pf.logweights_to_weights(lw), cfg, pf.RngStream(r), index_dtype=torch.int32,
+                                      out=c))
+    out["systematic_delivery_from_logweights_2^24_f32"] = {
+        "us_fused": t_f * 1e3, "us_two_step": t_2 * 1e3, "particles_per_s": n / (t_f * 1e-3),
+        "achieved_gbs": b / (t_f * 1e-3) / 1e9, "frac": b / (t_f * 1e-3) / 1e9 / hbm,
+        "note": "algorithmic bytes s+4 as for weights; the fused path reads lw three times (max, K1, K2)"}
+    del lw
     t = timeit(lambda r: pf.metropolis_ancestors(w, B_STEPS, pf.RngStream(r), index_dtype=torch.int32))
     b = (4 + 4 + B_STEPS * 4) * n
     out["metropolis_B32_2^24_f32_kernel"] = {"us": t * 1e3, "particles_per_s": n / (t * 1e-3),

@@ -170,6 +170,15 @@ int pfr_deliver_offspring(const void* w, int64_t n, int dtype, int accum, int st
                           const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,
                           int32_t* max_steps, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
 
+/* The same delivery from LOG-weights: logweights_to_weights (diagnostics.py:
+ * 138-155) fused into the delivery -- one max pass over lw (its validation:
+ * NaN / +inf / all -inf), then the delivery computes w = exp(lw - max lw) as
+ * it loads each tile (twice: K1 and K2), so w is never written.  Results are
+ * identical to pfr_logweights_to_weights followed by pfr_deliver_offspring. */
+int pfr_deliver_offspring_logw(const void* lw, int64_t n, int dtype, int accum, int stratified, double offset,
+                               const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,
+                               int32_t* max_steps, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
 /* multinomial_ancestors (resamplers.py:56-74).
  *   rng mode ARRAYS: `uniforms` are the pre-scaled draws in [0, W[N-1]);
  *   rng mode NUMPY : u = random(N) * W[N-1] replayed from the stream; out a is unsorted;

@@ -72,6 +72,7 @@ _SIGNATURES = {
     "pfr_logweights_to_weights": ([_P, _P, _I64, _INT, _P, _P, _SZ, _P], _INT),
     "pfr_cumulative_offspring": ([_P, _I64, _INT, _INT, _INT, _DBL, _P, _RNGP, _P, _P, _P, _SZ, _P], _INT),
     "pfr_deliver_offspring": ([_P, _I64, _INT, _INT, _INT, _DBL, _P, _RNGP, _P, _P, _P, _P, _P, _SZ, _P], _INT),
+    "pfr_deliver_offspring_logw": ([_P, _I64, _INT, _INT, _INT, _DBL, _P, _RNGP, _P, _P, _P, _P, _P, _SZ, _P], _INT),
     "pfr_multinomial": ([_P, _I64, _INT, _INT, _RNGP, _P, _INT, _P, _P, _P, _SZ, _P], _INT),
     "pfr_metropolis": ([_P, _I64, _INT, _I64, _RNGP, _P, _P, _INT, _P, _P, _P, _SZ, _P], _INT),
     "pfr_rejection": ([_P, _I64, _INT, _DBL, _DBL, _RNGP, _I64, _P, _P, _P, _P, _P, _SZ, _P], _INT),

@@ -260,6 +260,19 @@ int pfr_deliver_offspring(const void* w, int64_t n, int dtype, int accum, int st
   return PFR_OK;
 }
 
+int pfr_deliver_offspring_logw(const void* lw, int64_t n, int dtype, int accum, int stratified, double offset,
+                               const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,
+                               int32_t* max_steps, uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && lw && c && status, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "log-weights must be float32 or float64");
+  if (stratified) PFR_REQUIRE(uniforms || rng, "stratified needs uniforms or an rng");
+  PFR_WS(PFR_OP_DELIVER);
+  PFR_CHECK_LAUNCH(launch_deliver(lw, n, dtype, accum, stratified, offset, uniforms, rng, c, O_out, max_steps, status,
+                                  ws, (cudaStream_t)stream, 1),
+                   "pfr_deliver_offspring_logw");
+  return PFR_OK;
+}
+
 int pfr_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng, const double* uniforms,
                     int sorted_serial, int32_t* a, uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
   PFR_REQUIRE(valid_n(n) && w && a, "bad arguments");

@@ -239,4 +239,14 @@ __device__ __forceinline__ int ceil_log2_i64(int64_t x) {
   return l;
 }
 
+// order-preserving 64-bit encoding of doubles (atomicMax on a max cell)
+__device__ __forceinline__ unsigned long long ordered_bits(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_ordered(unsigned long long o) {
+  unsigned long long b = (o & 0x8000000000000000ull) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o;
+  return __longlong_as_double((long long)b);
+}
+
 }  // namespace pfr

@@ -72,6 +72,7 @@ struct DvArgs {
   DvState* state;
   uint32_t* status;
   int fx_S;          // fixed-point fraction bits of the offspring fast path
+  const unsigned long long* logw_max;  // non-null: p.w holds log-weights, w = exp(lw - max) on the fly
   int expand;        // 1: full delivery; 0: cumulative offspring O_out only
   // rare-path scratch
   int32_t* O;        // [n]
@@ -82,14 +83,16 @@ struct DvArgs {
 // ---------------------------------------------------------------------------
 // stratum offsets (cast to the weight dtype, resamplers.py:124/135)
 enum UMode { kUSys = 0, kUArr = 1, kUNp = 2, kUPh = 3 };
+constexpr int kULogW = 4;  // OR-ed into UM: the input holds log-weights (tile_weights)
 
 template <typename T, typename A, int UM>
 __device__ __forceinline__ A stratum_u(int64_t k0, const DvArgs<A>& p) {
-  if constexpr (UM == kUSys) {
+  constexpr int M = UM & 3;
+  if constexpr (M == kUSys) {
     return p.u_sys;
-  } else if constexpr (UM == kUArr) {
+  } else if constexpr (M == kUArr) {
     return (A)(T)p.uniforms[k0];
-  } else if constexpr (UM == kUNp) {
+  } else if constexpr (M == kUNp) {
     return (A)(T)u64_to_unit(numpy_raw64(p.key, (uint64_t)k0));
   } else {
     uint32_t o[4];
@@ -128,7 +131,7 @@ __device__ __forceinline__ int32_t offspring_of(A W, A total, const FxParams& f,
     const long long r = fx_round(W, f.sfx);
     bool ok = fx_safe(r, f.mask);
     long long ufx = f.ufx;
-    if constexpr (UM != kUSys) {
+    if constexpr ((UM & 3) != kUSys) {
       long long k = (r >> f.S) + 1;
       if (k > n) k = n;
       if (k < 1) k = 1;
@@ -145,6 +148,29 @@ __device__ __forceinline__ int32_t offspring_of(A W, A total, const FxParams& f,
 // K1: one CTA per 4096-element tile: validation flags and the tile aggregate
 // (the tile-local inclusive value at its last position, in exactly the
 // association K2 uses); tile prefixes built hierarchically (pfr_hier.cuh).
+// the tile's weights in registers: loaded, or exp(lw - max lw) computed from
+// log-weights exactly as logweights_to_weights does (diagnostics.py:138-155;
+// the same expression as k_logw_exp, so both paths see identical weights);
+// positions past n stay 0
+template <typename T, typename A, bool LW>
+__device__ __forceinline__ void tile_weights(const DvArgs<A>& p, int64_t base, T (&x)[kTileItems]) {
+  tile_load_any<T>((const T*)p.w, p.n, base, x);
+  if constexpr (LW) {
+    const T m = (T)from_ordered(__ldcg(p.logw_max));
+    const int64_t e0 = base + (int64_t)threadIdx.x * kTileItems;
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      T v;
+      if constexpr (sizeof(T) == 8)
+        v = exp(x[j] - m);
+      else
+        v = expf(x[j] - m);
+      // all -inf (max -inf): every weight 0, which K1 reports (no positive weight)
+      x[j] = (e0 + j < p.n && m > -INFINITY) ? v : T(0);
+    }
+  }
+}
+
 template <typename A>
 __device__ __forceinline__ Hier<A> hier_of(const DvArgs<A>& p) {
   return Hier<A>{p.agg, p.excl, p.sum_scratch, p.state, p.tiles};
@@ -154,7 +180,7 @@ __device__ __forceinline__ A tile_excl(const DvArgs<A>& p, int64_t b) {
   return hier_of(p).tile_excl(b);
 }
 
-template <typename T, typename A, int kTilesPerCta>
+template <typename T, typename A, int kTilesPerCta, bool LW = false>
 __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ uint32_t cta_flags;
@@ -166,7 +192,7 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
   T x[kTilesPerCta][kTileItems];
 #pragma unroll
   for (int t = 0; t < kTilesPerCta; ++t)
-    if (b0 + t < p.tiles) tile_load_any<T>((const T*)p.w, p.n, (b0 + t) * kTile, x[t]);
+    if (b0 + t < p.tiles) tile_weights<T, A, LW>(p, (b0 + t) * kTile, x[t]);
 #pragma unroll
   for (int t = 0; t < kTilesPerCta; ++t) {
     const int64_t b = b0 + t;
@@ -196,7 +222,7 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
                                                int32_t (&o)[kTileItems], int32_t& o_prev) {
   const int64_t base = b * kTile;
   T x[kTileItems];
-  tile_load_any<T>((const T*)p.w, p.n, base, x);
+  tile_weights<T, A, (UM & kULogW) != 0>(p, base, x);
   TileScan<A> s;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
@@ -506,7 +532,7 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   const unsigned tiles = (unsigned)p.tiles;
   // one tile per CTA (2 or 4 consecutive tiles per CTA measured 29 -> 37 / 43
   // us at 2^24: the per-tile hierarchy step is serial inside a CTA)
-  k_dv_reduce<T, A, 1><<<(unsigned)p.tiles, kTileThreads, 0, s>>>(p);
+  k_dv_reduce<T, A, 1, (UM & kULogW) != 0><<<(unsigned)p.tiles, kTileThreads, 0, s>>>(p);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || stages < 2) return e;
@@ -544,6 +570,12 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
 
 template <typename T, typename A>
 cudaError_t deliver_mode(DvArgs<A> p, int stratified, const double* uniforms, const pfr_rng* rng, cudaStream_t s) {
+  if (p.logw_max) {  // log-weights: the same pipeline with exp(lw - max) on load
+    if (!stratified) return deliver_typed<T, A, kUSys | kULogW>(p, s);
+    if (uniforms) return deliver_typed<T, A, kUArr | kULogW>(p, s);
+    if (rng && rng->mode == PFR_RNG_NUMPY) return deliver_typed<T, A, kUNp | kULogW>(p, s);
+    return deliver_typed<T, A, kUPh | kULogW>(p, s);
+  }
   if (!stratified) return deliver_typed<T, A, kUSys>(p, s);
   if (uniforms) return deliver_typed<T, A, kUArr>(p, s);
   if (rng && rng->mode == PFR_RNG_NUMPY) return deliver_typed<T, A, kUNp>(p, s);
@@ -571,6 +603,7 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
   p.state = ws.dv;
   p.status = status;
   p.fx_S = fx_bits(n);
+  p.logw_max = nullptr;
   p.expand = c != nullptr;
   p.O = ws.O;
   p.tmax = reinterpret_cast<int64_t*>(ws.j1);  // tiles << n
@@ -613,22 +646,35 @@ cudaError_t launch_offspring(const void* w, int64_t n, int dtype, int accum, int
 
 cudaError_t launch_deliver(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
                            const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,
-                           int32_t* max_steps, uint32_t* status, const Workspace& ws, cudaStream_t s) {
+                           int32_t* max_steps, uint32_t* status, const Workspace& ws, cudaStream_t s, int logw) {
   if (max_steps) {
     cudaError_t e = cudaMemsetAsync(max_steps, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
   }
+  // log-weights: one max pass (with the log-weight validation flags), then
+  // K1/K2 compute exp(lw - max) as they load -- w is never stored
+  const unsigned long long* lmax = nullptr;
+  if (logw) {
+    unsigned long long* cell = reinterpret_cast<unsigned long long*>(&ws.hdr->cell[1]);
+    cudaError_t e = launch_logw_max(w, n, dtype, cell, status, s);
+    if (e != cudaSuccess) return e;
+    lmax = cell;
+  }
+  auto args = [&](auto a) {
+    a.logw_max = lmax;
+    return a;
+  };
   if (dtype == PFR_F64)
     return deliver_mode<double, double>(
-        make_args<double, double>(w, n, offset, uniforms, rng, c, O_out, max_steps, status, ws), stratified,
+        args(make_args<double, double>(w, n, offset, uniforms, rng, c, O_out, max_steps, status, ws)), stratified,
         uniforms, rng, s);
   if (accum == PFR_ACC_NATIVE)
     return deliver_mode<float, float>(
-        make_args<float, float>(w, n, offset, uniforms, rng, c, O_out, max_steps, status, ws), stratified, uniforms,
-        rng, s);
+        args(make_args<float, float>(w, n, offset, uniforms, rng, c, O_out, max_steps, status, ws)), stratified,
+        uniforms, rng, s);
   return deliver_mode<float, double>(
-      make_args<float, double>(w, n, offset, uniforms, rng, c, O_out, max_steps, status, ws), stratified, uniforms,
-      rng, s);
+      args(make_args<float, double>(w, n, offset, uniforms, rng, c, O_out, max_steps, status, ws)), stratified,
+      uniforms, rng, s);
 }
 
 }  // namespace pfr

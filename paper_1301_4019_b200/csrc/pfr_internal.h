@@ -64,10 +64,12 @@ cudaError_t launch_offspring(const void* w, int64_t n, int dtype, int accum, int
                              const Workspace& ws, cudaStream_t s);
 cudaError_t launch_deliver(const void* w, int64_t n, int dtype, int accum, int stratified, double offset,
                            const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,
-                           int32_t* max_steps, uint32_t* status, const Workspace& ws, cudaStream_t s);
+                           int32_t* max_steps, uint32_t* status, const Workspace& ws, cudaStream_t s, int logw = 0);
 cudaError_t launch_check_weights(const void* w, int64_t n, int dtype, uint32_t* status, cudaStream_t s);
 cudaError_t launch_adjacent_difference(const void* in, void* out, int64_t n, int dtype, int out_dtype,
                                        uint32_t* status, cudaStream_t s);
+cudaError_t launch_logw_max(const void* lw, int64_t n, int dtype, unsigned long long* cell, uint32_t* status,
+                            cudaStream_t s);
 cudaError_t launch_logweights(const void* lw, void* w, int64_t n, int dtype, uint32_t* status, const Workspace& ws,
                               cudaStream_t s);
 

@@ -253,14 +253,6 @@ __global__ void k_adjacent_difference(const T* __restrict__ in, U* __restrict__ 
 }
 
 // log-weights: ordered-integer max (exact) then exp(lw - max)
-__device__ __forceinline__ unsigned long long ordered_bits(double x) {
-  unsigned long long b = (unsigned long long)__double_as_longlong(x);
-  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double from_ordered(unsigned long long o) {
-  unsigned long long b = (o & 0x8000000000000000ull) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o;
-  return __longlong_as_double((long long)b);
-}
 
 template <typename T>
 __global__ void k_logw_max(const T* __restrict__ lw, int64_t n, unsigned long long* cell, uint32_t* status) {
@@ -420,6 +412,20 @@ cudaError_t launch_adjacent_difference(const void* in, void* out, int64_t n, int
     default:
       return cudaErrorInvalidValue;
   }
+  note_launch();
+  return cudaGetLastError();
+}
+
+// max of the log-weights (ordered bits) into *cell, with the validation flags
+cudaError_t launch_logw_max(const void* lw, int64_t n, int dtype, unsigned long long* cell, uint32_t* status,
+                            cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(cell, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  const int g = grid_for(n, 256);
+  if (dtype == PFR_F64)
+    k_logw_max<double><<<g, 256, 0, s>>>((const double*)lw, n, cell, status);
+  else
+    k_logw_max<float><<<g, 256, 0, s>>>((const float*)lw, n, cell, status);
   note_launch();
   return cudaGetLastError();
 }

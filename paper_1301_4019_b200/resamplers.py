@@ -345,11 +345,20 @@ def resample_ancestors(w, config: ResamplerConfig, rng, **kw) -> ResampleOutput:
 
 
 def deliver(w, config: ResamplerConfig, rng, *, rng_mode=None, accum=None, index_dtype=None,
-            return_max_steps: bool = False, out: torch.Tensor | None = None):
+            return_max_steps: bool = False, out: torch.Tensor | None = None, log_weights: bool = False):
     """Resample and permute to an in-place-valid ancestry c (o[i] > 0 => c[i] = i):
     the bench's delivery contract (bench.py:155-161).  Equals
-    permute_parallel(resample_ancestors(w, config, rng).ancestors)."""
+    permute_parallel(resample_ancestors(w, config, rng).ancestors).
+
+    ``log_weights=True``: ``w`` holds log-weights; equals the same call on
+    ``logweights_to_weights(w)`` (diagnostics.py:138-155).  For systematic /
+    stratified the conversion is fused into the delivery (w is never stored)."""
     alg = config.algorithm
+    if log_weights and alg not in _OFFSPRING:
+        from .diagnostics import logweights_to_weights
+
+        w = logweights_to_weights(w)
+        log_weights = False
     if alg in _OFFSPRING:
         w = L.as_weights(w)
         n = w.numel()
@@ -360,9 +369,17 @@ def deliver(w, config: ResamplerConfig, rng, *, rng_mode=None, accum=None, index
         strat = alg == "stratified"
         u = 0.0 if strat else _systematic_offset(rng, rng_mode)
         r = _rng(rng, rng_mode)
-        L.call("pfr_deliver_offspring", w.data_ptr(), n, L.dtype_code(w), L.accum_code(accum), int(strat), u, None,
+        entry = "pfr_deliver_offspring_logw" if log_weights else "pfr_deliver_offspring"
+        L.call(entry, w.data_ptr(), n, L.dtype_code(w), L.accum_code(accum), int(strat), u, None,
                r, c.data_ptr(), None, L.ptr(steps), st.data_ptr(), ws, wsb, L.stream_handle())
-        _raise(st)
+        if log_weights and L.config.check:
+            bits = L.read_status(st)
+            if bits & L.ST_NONFINITE:
+                raise ValueError("log-weights may not contain NaN or +inf")
+            if not bits & L.ST_POSITIVE:
+                raise ValueError("all log-weights are -inf: no positive weight")
+        else:
+            _raise(st)
         c = L.to_index_dtype(c, index_dtype) if out is None else c
         return (c, int(steps.item())) if return_max_steps else c
     kw = {"rng_mode": rng_mode}

@@ -528,3 +528,34 @@ def test_concurrent_streams_match_sequential():
     for k, c in enumerate(outs):
         np.testing.assert_array_equal(np_(c), seq[k], err_msg=jobs[k][0])
     assert isinstance(pf._lib.status_all(), int)  # the rings of every stream are readable
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("alg", ["systematic", "stratified"])
+@pytest.mark.parametrize("n", [1000, 1 << 16, (1 << 20) + 3])
+def test_deliver_from_log_weights_is_fused_and_identical(dtype, alg, n):
+    """deliver(lw, log_weights=True) equals deliver(logweights_to_weights(lw))
+    element for element (the fused path computes the same exp(lw - max))."""
+    g = np.random.default_rng(n)
+    lw = (g.normal(0, 2.0, n) - 30.0).astype(dtype)
+    lw[::53] = -np.inf
+    lwt = torch.from_numpy(lw).cuda()
+    cfg = pf.ResamplerConfig(alg)
+    fused = pf.deliver(lwt, cfg, pf.RngStream(4, (n,)), log_weights=True, index_dtype=torch.int32)
+    two = pf.deliver(pf.logweights_to_weights(lwt), cfg, pf.RngStream(4, (n,)), index_dtype=torch.int32)
+    np.testing.assert_array_equal(np_(fused), np_(two))
+    assert O.satisfies_predicate(np_(fused))
+
+
+def test_deliver_from_log_weights_errors_and_other_algorithms():
+    cfg = pf.ResamplerConfig("systematic")
+    with pytest.raises(ValueError, match=r"NaN or \+inf"):
+        pf.deliver(torch.tensor([0.0, float("nan"), 1.0], device="cuda"), cfg, pf.RngStream(0), log_weights=True)
+    with pytest.raises(ValueError, match="all log-weights are -inf"):
+        pf.deliver(torch.full((5,), float("-inf"), device="cuda", dtype=torch.float64), cfg, pf.RngStream(0),
+                   log_weights=True)
+    lw = torch.from_numpy(np.random.default_rng(1).normal(0, 1, 4096)).cuda()
+    mh = pf.ResamplerConfig("metropolis", b=8)
+    a = pf.deliver(lw, mh, pf.RngStream(2), log_weights=True)
+    b = pf.deliver(pf.logweights_to_weights(lw), mh, pf.RngStream(2))
+    np.testing.assert_array_equal(np_(a), np_(b))
