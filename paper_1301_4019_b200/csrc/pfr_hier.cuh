@@ -82,7 +82,8 @@ __device__ __forceinline__ void hier_tile_done(const Hier<A>& h, int64_t b, uint
     *stage = (t == (unsigned)gsize - 1) ? 1 : 0;
   }
   __syncthreads();
-  if (!*stage) return;
+  if (!*stage) return;  // block-uniform
+  __syncthreads();      // every thread has read *stage before warp 0 rewrites it below
   // last tile of group g: scan the group's aggregates
   if (warp == 0) {
     __threadfence();

@@ -13,3 +13,9 @@ if [ -z "$NO_BENCH" ]; then
   timeout 900 python bench.py --steps ${STEPS:-3} --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.txt 2>&1; echo "bench rc=$?" >> gpurun_out/bench.txt
   tail -c 3000 gpurun_out/bench.txt
 fi
+if [ -n "$SANITIZE" ]; then
+  for tool in memcheck racecheck synccheck; do
+    timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_paths.py > gpurun_out/sanitize_$tool.txt 2>&1
+    tail -1 gpurun_out/sanitize_$tool.txt
+  done
+fi
