@@ -48,6 +48,9 @@ enum pfr_accum {
 /* OR-ed into pfr_scan's `accum`: repair ulp-level non-monotonicity with an
  * exact running max (only meaningful for non-negative inputs such as weights) */
 #define PFR_SCAN_MONOTONE 0x100
+/* the input is a weight vector: the scan also reports check_weights' flags
+ * (negative, any-positive; non-finite is always reported) */
+#define PFR_SCAN_WEIGHTS 0x200
 
 /* where the random draws come from */
 enum pfr_rng_mode {

@@ -652,7 +652,8 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
     note_launch();
     return cudaGetLastError();
   }
-  cudaError_t e = launch_scan(w, W, n, dtype, dtype, scan_flags, 0, nullptr, -1, status, ws, s);
+  // the weight scan also validates w (check_weights' flags into status)
+  cudaError_t e = launch_scan(w, W, n, dtype, dtype, scan_flags | PFR_SCAN_WEIGHTS, 0, nullptr, -1, status, ws, s);
   if (e != cudaSuccess) return e;
   const int mode = uniforms ? PFR_RNG_ARRAYS : (rng ? rng->mode : PFR_RNG_PHILOX);
   if (mode == PFR_RNG_ARRAYS) {

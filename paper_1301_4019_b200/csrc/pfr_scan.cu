@@ -53,7 +53,7 @@ __device__ __forceinline__ void griddep_wait_scan() { asm volatile("griddepcontr
 //     reference's serial fold) for the rare-path running-max repair S3.
 template <typename T, typename A, bool kFloat>
 __global__ void __launch_bounds__(kTileThreads) k_sc_reduce(const T* __restrict__ in, int64_t n, Hier<A> h,
-                                                             uint32_t* status) {
+                                                             uint32_t* status, uint32_t fmask) {
   __shared__ A warp_sums[kTileThreads / 32];
   __shared__ uint32_t cta_flags;
   __shared__ int stage;
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sc_reduce(const T* __restrict_
       FlagAcc<T> acc;
 #pragma unroll
       for (int j = 0; j < kTileItems; ++j) acc.add(x[j]);
-      f = acc.flags() & PFR_ST_NONFINITE;
+      f = acc.flags() & fmask;  // NONFINITE, plus NEGATIVE | POSITIVE for weights
     } else {
 #pragma unroll
       for (int j = 0; j < kTileItems; ++j)
@@ -330,12 +330,13 @@ cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, cudaStream_t s, bool pdl,
 
 template <typename T, typename A, typename U, bool kFloat>
 cudaError_t scan_typed(const void* in, void* out, int64_t n, int exclusive, int repair, void* total,
-                       int64_t expect_total, uint32_t* status, const Workspace& ws, cudaStream_t s) {
+                       int64_t expect_total, uint32_t* status, const Workspace& ws, cudaStream_t s,
+                       uint32_t fmask) {
   const int64_t tiles = num_tiles(n);
   A* agg = reinterpret_cast<A*>(ws.sum_cells);
   Hier<A> h{agg, reinterpret_cast<A*>(ws.max_cells), agg + tiles + 8, ws.dv, tiles};
   cudaError_t e = launch_ex(k_sc_reduce<T, A, kFloat>, dim3((unsigned)tiles), dim3(kTileThreads), s, false, false,
-                            (const T*)in, n, h, status);
+                            (const T*)in, n, h, status, fmask);
   if (e != cudaSuccess) return e;
   e = launch_ex(k_sc_apply<T, A, U, kFloat>, dim3((unsigned)tiles), dim3(kTileThreads), s, true, false,
                 (const T*)in, (U*)out, n, h, exclusive, repair, total, expect_total, status);
@@ -357,7 +358,9 @@ cudaError_t launch_scan(const void* in, void* out, int64_t n, int dtype, int out
                         void* total, int64_t expect_total, uint32_t* status, const Workspace& ws, cudaStream_t s) {
   const int repair = (accum & PFR_SCAN_MONOTONE) ? 1 : 0;
   const bool native = (accum & 0xFF) == PFR_ACC_NATIVE;
-#define PFR_SCAN_ARGS in, out, n, exclusive, repair, total, expect_total, status, ws, s
+  const uint32_t fmask =
+      PFR_ST_NONFINITE | ((accum & PFR_SCAN_WEIGHTS) ? (uint32_t)(PFR_ST_NEGATIVE | PFR_ST_POSITIVE) : 0u);
+#define PFR_SCAN_ARGS in, out, n, exclusive, repair, total, expect_total, status, ws, s, fmask
   switch (dtype) {
     case PFR_F64:
       return scan_typed<double, double, double, true>(PFR_SCAN_ARGS);

@@ -172,8 +172,10 @@ def multinomial_ancestors(w, rng, *, uniforms=None, rng_mode=None, accum=None, i
     ``uniforms``: pre-scaled draws in [0, W[N-1]) -> binary search (parity);
     numpy mode: the reference's draws replayed -> binary search (parity);
     philox mode: sorted order statistics from exponential spacings, searched
-    in W -> a sorted ancestry (the same multinomial law)."""
-    w, st = _weights_checked(w)
+    in W -> a sorted ancestry (the same multinomial law).  The weight scan
+    inside pfr_multinomial reports check_weights' flags (no separate pass)."""
+    w = L.as_weights(w)
+    st = L.new_status()
     n = w.numel()
     a = torch.empty(n, dtype=torch.int32, device=w.device)
     uni = None

@@ -559,3 +559,16 @@ def test_deliver_from_log_weights_errors_and_other_algorithms():
     a = pf.deliver(lw, mh, pf.RngStream(2), log_weights=True)
     b = pf.deliver(pf.logweights_to_weights(lw), mh, pf.RngStream(2))
     np.testing.assert_array_equal(np_(a), np_(b))
+
+
+def test_multinomial_validates_inside_its_scan():
+    """multinomial_ancestors has no separate check pass: the weight scan
+    reports check_weights' flags with the reference's messages."""
+    with pytest.raises(ValueError, match="non-negative"):
+        pf.multinomial_ancestors(np.array([1.0, -1.0, 2.0]), pf.RngStream(0))
+    with pytest.raises(ValueError, match="finite"):
+        pf.multinomial_ancestors(np.array([1.0, np.inf, 2.0]), pf.RngStream(0))
+    with pytest.raises(ValueError, match="positive"):
+        pf.multinomial_ancestors(np.zeros(5), pf.RngStream(0))
+    a = np_(pf.multinomial_ancestors(np.array([0.0, 0.0, 5.0, 0.0]), pf.RngStream(1)))
+    np.testing.assert_array_equal(a, [2, 2, 2, 2])
