@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kIpThreads, kMinBlocks) k_dv_inplace(const uin
 #pragma unroll
     for (int q = 0; q < kScanG; ++q) {
       const uint32_t gp = pg(g + q);
-      wd[q] = __ldcs(words + gp * kGroup + lane);
+      wd[q] = __ldg(words + gp * kGroup + lane);
       bw[q] = __ldg(bitmap + gp);
     }
 #pragma unroll
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kIpThreads, kMinBlocks) k_dv_inplace(const uin
     const uint32_t gp = pg(g);
     const uint32_t x = gp * kGroup + lane;
     const bool in = kSegs || x < nn;
-    const uint32_t wd = in ? __ldcs(words + x) : 0u;
+    const uint32_t wd = in ? __ldg(words + x) : 0u;
     scan_group(Q, warp, lane, x, in, wd, __ldg(bitmap + gp), qlen, c);
     __syncwarp();
   }
