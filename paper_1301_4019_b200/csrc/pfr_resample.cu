@@ -53,11 +53,11 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_metropolis_philox(const T* __restrict__ w, int64_t n, int64_t steps,
                                                            uint32_t k0, uint32_t k1, uint32_t threshold,
                                                            int64_t c_begin, int64_t c_count,
-                                                           int32_t* __restrict__ a) {
+                                                           int32_t* __restrict__ a, uint32_t* status) {
   // chains [c_begin, c_begin + c_count) of the N-chain resampler (a sharded
   // rank runs its slice with global chain numbers: same draws, same result)
+  __shared__ uint32_t blk_flags;
   const int64_t local = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kChainsPerThread;
-  if (local >= c_count) return;
   const int64_t first = c_begin + local;
   int64_t k[kChainsPerThread];
   T wk[kChainsPerThread];
@@ -67,6 +67,23 @@ __global__ void __launch_bounds__(256) k_metropolis_philox(const T* __restrict__
     k[c] = i;
     wk[c] = ldg(w + i);
   }
+  if (status) {  // launch-uniform
+    // check_weights (diagnostics.py:38-51) on the chains' own weights: every
+    // w[i] of the launch's slice is read once here, so no separate pass.
+    // One global atomic per block, and only for bits not yet set.
+    if (threadIdx.x == 0) blk_flags = 0;
+    __syncthreads();
+    FlagAcc<T> facc;
+#pragma unroll
+    for (int c = 0; c < kChainsPerThread; ++c)
+      if (local + c < c_count) facc.add(wk[c]);
+    const uint32_t f = __reduce_or_sync(0xffffffffu, facc.flags());
+    if ((threadIdx.x & 31) == 0 && f) atomicOr(&blk_flags, f);
+    __syncthreads();
+    if (threadIdx.x == 0 && blk_flags && (*(volatile uint32_t*)status & blk_flags) != blk_flags)
+      atomicOr(status, blk_flags);
+  }
+  if (local >= c_count) return;
   const uint32_t nn = (uint32_t)n;
   for (int64_t b = 0; b < steps; b += 2) {
     uint32_t j[kChainsPerThread][2];
@@ -564,9 +581,11 @@ cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps
     const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
     const uint32_t thr = lemire_threshold(n);
     if (dtype == PFR_F64)
-      k_metropolis_philox<double><<<blocks, 256, 0, s>>>((const double*)w, n, steps, k0, k1, thr, c_begin, c_count, a);
+      k_metropolis_philox<double><<<blocks, 256, 0, s>>>((const double*)w, n, steps, k0, k1, thr, c_begin, c_count, a,
+                                                          status);
     else
-      k_metropolis_philox<float><<<blocks, 256, 0, s>>>((const float*)w, n, steps, k0, k1, thr, c_begin, c_count, a);
+      k_metropolis_philox<float><<<blocks, 256, 0, s>>>((const float*)w, n, steps, k0, k1, thr, c_begin, c_count, a,
+                                                         status);
   }
   note_launch();
   return cudaGetLastError();

@@ -229,8 +229,14 @@ def metropolis_num_steps(p_star: float, epsilon: float | None, n: int) -> int:
 def metropolis_ancestors(w, b: int, rng, *, u_draws=None, j_draws=None, rng_mode=None, index_dtype=None):
     """N independent B-step Metropolis chains (resamplers.py:204-234).
     ``u_draws``/``j_draws`` (shape (B, N)) replay supplied draws (any N);
-    numpy mode replays the reference stream (power-of-two N)."""
-    w, st = _weights_checked(w, require_positive_total=False)
+    numpy mode replays the reference stream (power-of-two N).  In philox mode
+    the kernel validates w itself as each chain reads its own weight."""
+    own = u_draws is None and j_draws is None and (rng_mode or L.config.rng_mode) == "philox"
+    if own:
+        w = L.as_weights(w)
+        st = L.new_status()
+    else:
+        w, st = _weights_checked(w, require_positive_total=False)
     b = int(b)
     if b < 0:
         raise ValueError("number of chain steps must be non-negative")

@@ -572,3 +572,20 @@ def test_multinomial_validates_inside_its_scan():
         pf.multinomial_ancestors(np.zeros(5), pf.RngStream(0))
     a = np_(pf.multinomial_ancestors(np.array([0.0, 0.0, 5.0, 0.0]), pf.RngStream(1)))
     np.testing.assert_array_equal(a, [2, 2, 2, 2])
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_metropolis_own_stream_validates_in_kernel(dtype):
+    """Own-stream Metropolis has no separate check pass: the chains' first
+    reads report check_weights' flags (all-zero weights are allowed, as in
+    the reference)."""
+    with pytest.raises(ValueError, match="non-negative"):
+        pf.metropolis_ancestors(np.array([1.0, -1.0, 2.0, 3.0], dtype=dtype), 4, pf.RngStream(0))
+    with pytest.raises(ValueError, match="finite"):
+        pf.metropolis_ancestors(np.array([1.0, np.nan, 2.0, 3.0], dtype=dtype), 4, pf.RngStream(0))
+    a = np_(pf.metropolis_ancestors(np.zeros(8, dtype=dtype), 4, pf.RngStream(0)))
+    assert a.min() >= 0 and a.max() < 8
+    big = np.exp(np.random.default_rng(3).normal(0, 1, 100003)).astype(dtype)
+    big[77777] = -0.5
+    with pytest.raises(ValueError, match="non-negative"):
+        pf.metropolis_ancestors(big, 2, pf.RngStream(1))
