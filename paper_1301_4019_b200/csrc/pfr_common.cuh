@@ -19,7 +19,9 @@ constexpr int kWarp = 32;
 // ---------------------------------------------------------------------------
 // status word (device); host maps bits to the reference's exceptions
 __device__ __forceinline__ void status_or(uint32_t* status, uint32_t bits) {
-  if (bits && status) atomicOr(status, bits);
+  // read first: informational bits (any-positive) are set by nearly every
+  // warp, and a same-address atomic per warp would serialise in L2
+  if (bits && status && (*(volatile uint32_t*)status & bits) != bits) atomicOr(status, bits);
 }
 
 // warp-aggregated OR: one atomic per warp

@@ -589,3 +589,17 @@ def test_metropolis_own_stream_validates_in_kernel(dtype):
     big[77777] = -0.5
     with pytest.raises(ValueError, match="non-negative"):
         pf.metropolis_ancestors(big, 2, pf.RngStream(1))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_rejection_validates_in_kernel(dtype):
+    """Rejection has no separate check pass: each slot's first trip (which
+    proposes the slot itself) reports check_weights' flags."""
+    with pytest.raises(ValueError, match="non-negative"):
+        pf.rejection_ancestors(np.array([1.0, -1.0, 2.0, 3.0], dtype=dtype), 3.0, pf.RngStream(0))
+    w = np.exp(np.random.default_rng(4).normal(0, 1, 50001)).astype(dtype)
+    a, trips = pf.rejection_ancestors(w, float(w.max()), pf.RngStream(2), return_trips=True)
+    assert np_(trips).min() >= 1 and O.satisfies_predicate(O.permute(np_(a)))
+    w[31337] = -1.0
+    with pytest.raises(ValueError, match="non-negative"):
+        pf.rejection_ancestors(w, float(w.max()), pf.RngStream(2))
