@@ -182,6 +182,14 @@ int pfr_deliver_offspring_logw(const void* lw, int64_t n, int dtype, int accum, 
                                const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,
                                int32_t* max_steps, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
 
+/* Fused Metropolis delivery (own PHILOX stream): permute_parallel(
+ * metropolis_ancestors(w, steps)) (resamplers.py:204-234, ancestry.py:
+ * 125-174) with the permute's claims made by the chains as they finish, so
+ * the ancestry is never re-read for claiming; c is the in-place-valid
+ * ancestry.  Identical to pfr_metropolis followed by pfr_permute. */
+int pfr_deliver_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng, int32_t* c,
+                           int32_t* max_steps, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
 /* multinomial_ancestors (resamplers.py:56-74).
  *   rng mode ARRAYS: `uniforms` are the pre-scaled draws in [0, W[N-1]);
  *   rng mode NUMPY : u = random(N) * W[N-1] replayed from the stream; out a is unsorted;

@@ -515,6 +515,28 @@ cudaError_t launch_permute(const void* a, int64_t n, int idx_dtype, int32_t* c, 
   return cudaGetLastError();
 }
 
+// the general permute in two halves, for producers that claim while they
+// write the ancestry (the fused Metropolis delivery): reset d (and the
+// overflow marker) before the producer, then the walk
+cudaError_t launch_claims_reset(int64_t n, int32_t* max_steps, const Workspace& ws, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(&ws.hdr->overflow, 0, sizeof(int32_t), s);
+  if (e != cudaSuccess) return e;
+  if (max_steps) {
+    e = cudaMemsetAsync(max_steps, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaMemsetAsync(ws.d, 0x7F, (size_t)n * sizeof(int32_t), s);
+}
+
+cudaError_t launch_walk(const int32_t* a, int64_t n, int32_t* c, int32_t* max_steps, uint32_t* status,
+                        const Workspace& ws, cudaStream_t s) {
+  const int gw = grid_for((n + 3) / 4, 256);
+  unsigned int* done = &ws.dv->pad[0];
+  k_walk<int32_t><<<gw, 256, 0, s>>>(a, n, ws.d, c, max_steps, ws.hdr, done, ws.j0, ws.j1, ws.r0, ws.r1, status);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_prepermute(const void* a, int64_t n, int idx_dtype, int32_t* d, uint32_t* status,
                               cudaStream_t s) {
   const int g = grid_for(n, 256);

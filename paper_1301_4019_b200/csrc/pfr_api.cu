@@ -273,6 +273,23 @@ int pfr_deliver_offspring_logw(const void* lw, int64_t n, int dtype, int accum, 
   return PFR_OK;
 }
 
+int pfr_deliver_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng, int32_t* c,
+                           int32_t* max_steps, uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && c && status, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(steps >= 0, "number of chain steps must be non-negative");
+  PFR_REQUIRE(rng && rng->mode == PFR_RNG_PHILOX, "the fused Metropolis delivery uses the PHILOX stream");
+  PFR_WS(PFR_OP_DELIVER);
+  cudaStream_t s = (cudaStream_t)stream;
+  // claims reset, chains + claims (a in the workspace's sorted-ancestry
+  // scratch), then the permute's walk
+  PFR_CHECK_LAUNCH(launch_claims_reset(n, max_steps, ws, s), "pfr_deliver_metropolis");
+  PFR_CHECK_LAUNCH(launch_metropolis(w, n, dtype, steps, rng, nullptr, nullptr, PFR_I32, ws.a, status, s, 0, n, ws.d),
+                   "pfr_deliver_metropolis");
+  PFR_CHECK_LAUNCH(launch_walk(ws.a, n, c, max_steps, status, ws, s), "pfr_deliver_metropolis");
+  return PFR_OK;
+}
+
 int pfr_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng, const double* uniforms,
                     int sorted_serial, int32_t* a, uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
   PFR_REQUIRE(valid_n(n) && w && a, "bad arguments");

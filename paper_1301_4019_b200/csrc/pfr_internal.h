@@ -76,6 +76,9 @@ cudaError_t launch_logweights(const void* lw, void* w, int64_t n, int dtype, uin
 // launchers (pfr_ancestry.cu)
 cudaError_t launch_permute_cumulative(const int32_t* O, int64_t n, int32_t* c, int32_t* max_steps, uint32_t* status,
                                       const Workspace& ws, cudaStream_t s);
+cudaError_t launch_claims_reset(int64_t n, int32_t* max_steps, const Workspace& ws, cudaStream_t s);
+cudaError_t launch_walk(const int32_t* a, int64_t n, int32_t* c, int32_t* max_steps, uint32_t* status,
+                        const Workspace& ws, cudaStream_t s);
 cudaError_t launch_permute(const void* a, int64_t n, int idx_dtype, int32_t* c, int32_t* max_steps,
                            uint32_t* status, const Workspace& ws, cudaStream_t s);
 cudaError_t launch_prepermute(const void* a, int64_t n, int idx_dtype, int32_t* d, uint32_t* status,
@@ -95,7 +98,7 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
                                const Workspace& ws, cudaStream_t s);
 cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng,
                               const double* u_draws, const void* j_draws, int idx_dtype, int32_t* a,
-                              uint32_t* status, cudaStream_t s, int64_t c_begin = 0, int64_t c_count = -1);
+                              uint32_t* status, cudaStream_t s, int64_t c_begin = 0, int64_t c_count = -1, int32_t* claim = nullptr);
 cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
                              int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
                              const Workspace& ws, cudaStream_t s, int64_t s_begin = 0,

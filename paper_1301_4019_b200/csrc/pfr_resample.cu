@@ -53,7 +53,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_metropolis_philox(const T* __restrict__ w, int64_t n, int64_t steps,
                                                            uint32_t k0, uint32_t k1, uint32_t threshold,
                                                            int64_t c_begin, int64_t c_count,
-                                                           int32_t* __restrict__ a, uint32_t* status) {
+                                                           int32_t* __restrict__ a, uint32_t* status,
+                                                           int32_t* __restrict__ claim) {
   // chains [c_begin, c_begin + c_count) of the N-chain resampler (a sharded
   // rank runs its slice with global chain numbers: same draws, same result)
   __shared__ uint32_t blk_flags;
@@ -125,7 +126,11 @@ __global__ void __launch_bounds__(256) k_metropolis_philox(const T* __restrict__
   }
 #pragma unroll
   for (int c = 0; c < kChainsPerThread; ++c)
-    if (local + c < c_count) a[local + c] = (int32_t)k[c];
+    if (local + c < c_count) {
+      a[local + c] = (int32_t)k[c];
+      // fused delivery: the permute's claim (prepermute, ancestry.py:125-136)
+      if (claim) atomicMin(claim + k[c], (int32_t)(c_begin + local + c));
+    }
 }
 
 // Metropolis replaying numpy's stream (power-of-two N): per step the
@@ -549,7 +554,7 @@ cudaError_t launch_lower_bound(const void* W, int64_t n, int dtype, const double
 
 cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng,
                               const double* u_draws, const void* j_draws, int idx_dtype, int32_t* a,
-                              uint32_t* status, cudaStream_t s, int64_t c_begin, int64_t c_count) {
+                              uint32_t* status, cudaStream_t s, int64_t c_begin, int64_t c_count, int32_t* claim) {
   const int mode = rng ? rng->mode : PFR_RNG_ARRAYS;
   if (c_count < 0) c_count = n;
   if (mode == PFR_RNG_ARRAYS && (c_begin != 0 || c_count != n)) return cudaErrorNotSupported;
@@ -582,10 +587,10 @@ cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps
     const uint32_t thr = lemire_threshold(n);
     if (dtype == PFR_F64)
       k_metropolis_philox<double><<<blocks, 256, 0, s>>>((const double*)w, n, steps, k0, k1, thr, c_begin, c_count, a,
-                                                          status);
+                                                          status, claim);
     else
       k_metropolis_philox<float><<<blocks, 256, 0, s>>>((const float*)w, n, steps, k0, k1, thr, c_begin, c_count, a,
-                                                         status);
+                                                         status, claim);
   }
   note_launch();
   return cudaGetLastError();

@@ -390,6 +390,20 @@ def deliver(w, config: ResamplerConfig, rng, *, rng_mode=None, accum=None, index
             _raise(st)
         c = L.to_index_dtype(c, index_dtype) if out is None else c
         return (c, int(steps.item())) if return_max_steps else c
+    if alg == "metropolis" and (rng_mode or L.config.rng_mode) == "philox":
+        # fused: the chains make the permute's claims as they finish
+        w = L.as_weights(w)
+        b = resolve_metropolis_steps(w, config)
+        n = w.numel()
+        c = out if out is not None else torch.empty(n, dtype=torch.int32, device=w.device)
+        steps = torch.zeros(1, dtype=torch.int32, device=w.device) if return_max_steps else None
+        st = L.new_status()
+        ws, wsb = L.workspace(n)
+        L.call("pfr_deliver_metropolis", w.data_ptr(), n, L.dtype_code(w), int(b), _rng(rng, rng_mode),
+               c.data_ptr(), L.ptr(steps), st.data_ptr(), ws, wsb, L.stream_handle())
+        _raise(st, require_positive_total=False)
+        c = L.to_index_dtype(c, index_dtype) if out is None else c
+        return (c, int(steps.item())) if return_max_steps else c
     kw = {"rng_mode": rng_mode}
     if alg.startswith("multinomial"):
         kw["accum"] = accum

@@ -603,3 +603,19 @@ def test_rejection_validates_in_kernel(dtype):
     w[31337] = -1.0
     with pytest.raises(ValueError, match="non-negative"):
         pf.rejection_ancestors(w, float(w.max()), pf.RngStream(2))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [1000, 1 << 16, (1 << 20) + 5])
+def test_fused_metropolis_delivery_equals_two_calls(dtype, n):
+    """deliver(metropolis) in the own stream (claims made by the chains)
+    equals permute_parallel(metropolis_ancestors(...)) element for element,
+    max steps included."""
+    g = np.random.default_rng(n)
+    w = torch.from_numpy(np.exp(g.normal(0, 1.5, n)).astype(dtype)).cuda()
+    cfg = pf.ResamplerConfig("metropolis", b=12)
+    c, s = pf.deliver(w, cfg, pf.RngStream(8, (n,)), return_max_steps=True, index_dtype=torch.int32)
+    a = pf.metropolis_ancestors(w, 12, pf.RngStream(8, (n,)), index_dtype=torch.int32)
+    c2, s2 = pf.permute_parallel(a, return_max_steps=True, index_dtype=torch.int32)
+    np.testing.assert_array_equal(np_(c), np_(c2))
+    assert s == s2
