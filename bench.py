@@ -339,12 +339,10 @@ def main():
     conc_out = [torch.empty(n, dtype=torch.int32, device=dev) for _ in jobs]
 
     def run_delivery(alg, dt, w, rs, out):
-        if alg in ("systematic", "stratified"):
+        if alg in ("systematic", "stratified", "metropolis"):  # fused deliveries
             return pf.deliver(w, cfgs[alg], rs, index_dtype=torch.int32, out=out)
         if alg == "multinomial":
             a = pf.multinomial_ancestors(w, rs, index_dtype=torch.int32)
-        elif alg == "metropolis":
-            a = pf.metropolis_ancestors(w, B_STEPS, rs, index_dtype=torch.int32)
         else:
             a = pf.rejection_ancestors(w, sup[dt], rs, index_dtype=torch.int32)
         return pf.permute_parallel(a, index_dtype=torch.int32)
