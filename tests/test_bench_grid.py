@@ -57,3 +57,17 @@ def test_pf_demo_cli():
     res = CliRunner().invoke(main, ["pf", "demo", "--n", "1024", "--steps", "10", "--filters", "8"])
     assert res.exit_code == 0, res.output
     assert "exact log-likelihood" in res.output
+
+
+@pytest.mark.gpu
+def test_grid_is_deterministic_across_workers_and_runs():
+    """SPEC C11 (test_acceptance.py:350-388): the same grid twice, with 1 and
+    4 workers, gives identical records except the timing columns."""
+    cfg1 = B.BenchConfig(n_values=(64, 1024), y_values=(0.0, 2.0), replicates=2, workers=1)
+    cfg4 = B.BenchConfig(n_values=(64, 1024), y_values=(0.0, 2.0), replicates=2, workers=4)
+    r1, e1 = B.run_grid(cfg1)
+    r4, e4 = B.run_grid(cfg4)
+    assert e1 == e4 == 0
+    key = lambda r: (r.algorithm, r.n, r.y, r.replicate, r.mse,  # noqa: E731
+                     {k: v for k, v in r.extras.items() if k != "gbps"})
+    assert [key(r) for r in r1] == [key(r) for r in r4]
