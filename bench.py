@@ -250,9 +250,16 @@ def main():
     import paper_1301_4019_b200 as pf
     from paper_1301_4019_b200 import _lib as L
 
+    # PFR_BENCH_BACKEND / PFR_BENCH_DEVICE (test knobs): run the multi-rank
+    # protocol with gloo on one GPU to check it before a multi-GPU run
+    backend = os.environ.get("PFR_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("PFR_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     pf.config.check = False  # validation kernels still run; statuses are read after timing

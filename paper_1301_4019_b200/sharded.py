@@ -174,6 +174,11 @@ class CudaShardOps:
     def tensor(self, x, dtype):
         return torch.as_tensor(x, dtype=dtype).to(self.dev)
 
+    def _on_dev(self, t):
+        """Protocol payloads arrive on the communicator's device (host memory
+        for gloo): the kernels need them on this rank's GPU."""
+        return torch.as_tensor(t).to(self.dev).contiguous()
+
     def status_bits(self) -> int:
         return L.read_status(self.status)
 
@@ -201,6 +206,7 @@ class CudaShardOps:
         return float(L.lib().pfr_stream_uniform(r, 0, _TAG_SYSTEMATIC))
 
     def offspring(self, W, wdtype, prefix, total, n_global, last, stratified, offset, uniforms, rng, mode):
+        W = self._on_dev(W)
         n = W.numel()
         O = torch.empty(n, dtype=torch.int32, device=self.dev)
         k0, k1 = as_stream(rng).key() if rng is not None else (0, 0)
@@ -212,6 +218,7 @@ class CudaShardOps:
         return O
 
     def words(self, O, base, o_begin):
+        O = self._on_dev(O)
         n = O.numel()
         o_end = int(O[-1].item())
         words = torch.empty(max(o_end - o_begin, 0), dtype=torch.int32, device=self.dev)
@@ -221,6 +228,7 @@ class CudaShardOps:
         return words, has
 
     def resolve(self, words, has, base):
+        words, has = self._on_dev(words), self._on_dev(has)
         n = has.numel()
         c = torch.empty(n, dtype=torch.int32, device=self.dev)
         pend = torch.empty((n, 3), dtype=torch.int32, device=self.dev)
@@ -236,7 +244,7 @@ class CudaShardOps:
         fwd = torch.empty((max(k, 1), 3), dtype=torch.int32, device=self.dev)
         cnt = torch.zeros(3, dtype=torch.int32, device=self.dev)  # [done, fwd, max steps]
         if k:
-            walkers = walkers.contiguous()
+            walkers, words = self._on_dev(walkers), self._on_dev(words)
             L.call("pfr_shard_advance", walkers.data_ptr(), k, words.data_ptr(), int(n_loc), int(base),
                    done.data_ptr(), cnt[0:].data_ptr(), fwd.data_ptr(), cnt[1:].data_ptr(), cnt[2:].data_ptr(),
                    self.status.data_ptr(), L.stream_handle())
@@ -246,7 +254,7 @@ class CudaShardOps:
     def scatter(self, done, base, c):
         k = done.shape[0]
         if k:
-            done = done.contiguous()
+            done = self._on_dev(done)
             L.call("pfr_shard_scatter", done.data_ptr(), k, int(base), c.numel(), c.data_ptr(),
                    self.status.data_ptr(), L.stream_handle())
 
