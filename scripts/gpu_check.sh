@@ -17,6 +17,7 @@ if [ -n "$SANITIZE" ]; then
   for tool in memcheck racecheck synccheck; do
     timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_paths.py > gpurun_out/sanitize_$tool.txt 2>&1
     timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_paths_large.py >> gpurun_out/sanitize_$tool.txt 2>&1
+    timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_paths_modes.py >> gpurun_out/sanitize_$tool.txt 2>&1
     tail -1 gpurun_out/sanitize_$tool.txt
   done
 fi
