@@ -619,3 +619,35 @@ def test_fused_metropolis_delivery_equals_two_calls(dtype, n):
     c2, s2 = pf.permute_parallel(a, return_max_steps=True, index_dtype=torch.int32)
     np.testing.assert_array_equal(np_(c), np_(c2))
     assert s == s2
+
+
+@pytest.mark.parametrize("alg", ["systematic", "metropolis"])
+def test_config4_full_size_properties(alg):
+    """BASELINE config 4 at its full size, N = 2^28 float32 on one GPU:
+    size-independent properties of the delivered ancestry (in-place
+    predicate, multiset = the resampler's ancestry; systematic: offspring
+    within 1 of N w/W)."""
+    n = 1 << 28
+    g = torch.Generator(device="cuda")
+    g.manual_seed(4)
+    lw = torch.randn(n, device="cuda", generator=g)
+    w = torch.exp(lw - lw.max())
+    del lw
+    if alg == "systematic":
+        rs = pf.RngStream(9)
+        O_ = pf.systematic_cumulative_offspring(w, rs, index_dtype=torch.int32)
+        c = pf.deliver(w, pf.ResamplerConfig("systematic"), rs, index_dtype=torch.int32)
+        o = pf.ancestors_to_offspring(c)
+        assert torch.equal(o, pf.cumulative_to_offspring(O_, index_dtype=torch.int32))
+        m = w.double() * (n / w.double().sum())
+        assert float((o.double() - m).abs().max()) < 1.0 + 1e-6
+        del O_, m
+    else:
+        rs = pf.RngStream(10)
+        a = pf.metropolis_ancestors(w, 4, rs, index_dtype=torch.int32)
+        c = pf.deliver(w, pf.ResamplerConfig("metropolis", b=4), rs, index_dtype=torch.int32)
+        assert torch.equal(pf.ancestors_to_offspring(c), pf.ancestors_to_offspring(a))
+        del a
+    assert pf.satisfies_inplace_predicate(c)
+    del c, w
+    torch.cuda.empty_cache()
