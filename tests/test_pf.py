@@ -165,3 +165,21 @@ def test_batched_filter_unaligned_sizes_track_kalman(n):
     se = ll.std(ddof=1) / math.sqrt(len(ll))
     assert abs(ll.mean() - exact.log_likelihood) < 5 * se + 0.2, (ll.mean(), exact.log_likelihood, se)
     assert np.abs(res.filtered_means.mean(axis=0) - exact.means).max() < 0.1
+
+
+@pytest.mark.gpu
+def test_config5_full_size_against_kalman():
+    """BASELINE config 5 at its full size (4096 filters x 2^16 particles,
+    T = 100): the mean log-likelihood and filtered means of the batch agree
+    with the exact Kalman recursion (C10, test_acceptance.py:316-347)."""
+    import paper_1301_4019_b200 as pf
+
+    model = LinearGaussianModel(coeff=0.9, trans_std=1.0, obs_std=1.0)
+    y = simulate_observations(model, 100, 2024)
+    exact = exact_filter(model, y)
+    res = pf.pf_run(model, y, 1 << 16, "systematic", 0.5, seed=11, filters=4096)
+    ll = res.log_likelihood
+    se = ll.std(ddof=1) / math.sqrt(ll.size)
+    assert abs(ll.mean() - exact.log_likelihood) < 5 * se + 0.01, (ll.mean(), exact.log_likelihood, se)
+    assert np.abs(res.filtered_means.mean(axis=0) - exact.means).max() < 2e-3
+    assert 0.2 < res.resampled.mean() < 0.8
