@@ -5,6 +5,8 @@ fixtures (stable_sum bit for bit: the pairwise tree's association is fixed)."""
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -91,3 +93,17 @@ def test_weight_stats_kats():
         pf.resampling_mse([1, 1], [1.0, 1.0, 1.0])
     assert pf.ess(np.ones(100)) == pytest.approx(100.0)
     assert pf.ess([0.0, 0.0, 3.0]) == pytest.approx(1.0)
+
+
+@pytest.mark.gpu
+def test_ctypes_example_without_torch():
+    """examples/ctypes_deliver.py: the C ABI driven through ctypes and
+    cuda-python only (the FFI path of a non-Python host)."""
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(os.path.dirname(__file__)), "examples",
+                                                     "ctypes_deliver.py"), "100003"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr[-2000:]
+    assert "hold" in r.stdout
