@@ -107,3 +107,22 @@ def test_ctypes_example_without_torch():
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr[-2000:]
     assert "hold" in r.stdout
+
+
+@pytest.mark.gpu
+def test_c_example_compiles_and_runs(tmp_path):
+    """examples/deliver.c: include/pfr.h is plain C; a C host links
+    libpfr.so and runs a fused delivery."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1301_4019_b200")
+    exe = str(tmp_path / "deliver")
+    cc = subprocess.run(["gcc", "-std=c11", "-Wall", "-I", os.path.join(root, "include"), "-I",
+                         "/usr/local/cuda/include", os.path.join(root, "examples", "deliver.c"), "-L", libdir,
+                         "-lpfr", "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{libdir}",
+                         "-Wl,-rpath,/usr/local/cuda/lib64", "-o", exe], capture_output=True, text=True)
+    assert cc.returncode == 0, cc.stderr
+    r = subprocess.run([exe, "300007"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "holds" in r.stdout
