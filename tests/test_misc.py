@@ -126,3 +126,15 @@ def test_c_example_compiles_and_runs(tmp_path):
     r = subprocess.run([exe, "300007"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "holds" in r.stdout
+
+
+@pytest.mark.gpu
+def test_graft_entry_smoke():
+    """__graft_entry__.smoke(): one small delivery + Metropolis on cuda:0,
+    checked against the oracle (the driver runs it at round end)."""
+    import importlib
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    entry = importlib.import_module("__graft_entry__")
+    entry.smoke()
