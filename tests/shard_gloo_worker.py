@@ -24,7 +24,7 @@ cuts = [n * r // world for r in range(world + 1)]  # uneven shards when world do
 w = torch.from_numpy(w_full[cuts[rank]:cuts[rank + 1]].copy()).cuda()
 comm = sharded.DistComm()
 ops = sharded.CudaShardOps()
-for alg in ("systematic", "stratified", "metropolis", "rejection"):
+for alg in ("systematic", "stratified", "metropolis", "rejection", "multinomial"):
     cfg = pf.ResamplerConfig(alg, b=8 if alg == "metropolis" else None)
     c = sharded.deliver_sharded(w, cfg, pf.RngStream(3), comm=comm, ops=ops)
     torch.cuda.synchronize()
