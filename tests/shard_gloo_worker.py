@@ -24,8 +24,10 @@ cuts = [n * r // world for r in range(world + 1)]  # uneven shards when world do
 w = torch.from_numpy(w_full[cuts[rank]:cuts[rank + 1]].copy()).cuda()
 comm = sharded.DistComm()
 ops = sharded.CudaShardOps()
-for alg in ("systematic", "stratified", "metropolis", "rejection", "multinomial"):
-    cfg = pf.ResamplerConfig(alg, b=8 if alg == "metropolis" else None)
+sup_v = float(np.quantile(w_full, 0.95))
+for alg in ("systematic", "stratified", "metropolis", "rejection", "rejection-capped", "multinomial"):
+    cfg = pf.ResamplerConfig(alg, b=8 if alg == "metropolis" else None,
+                             sup_v=sup_v if alg == "rejection-capped" else None)
     c = sharded.deliver_sharded(w, cfg, pf.RngStream(3), comm=comm, ops=ops)
     torch.cuda.synchronize()
     parts = [None] * world

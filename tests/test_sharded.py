@@ -278,7 +278,8 @@ def test_gpu_sharded_rejection_bit_identical(world):
 def test_gpu_sharded_real_processes(procs):
     """torch.distributed with real processes (gloo; every rank's kernels on
     one GPU, uneven shards at 3): systematic, stratified, Metropolis,
-    rejection and (replicated) multinomial deliveries equal the single-GPU ones."""
+    rejection (plain and capped) and (replicated) multinomial deliveries
+    equal the single-GPU ones."""
     import subprocess
     import sys
 
@@ -288,4 +289,4 @@ def test_gpu_sharded_real_processes(procs):
            os.path.join(os.path.dirname(__file__), "shard_gloo_worker.py"), "18"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
-    assert r.stdout.count("identical") == 5 and "DIFFERENT" not in r.stdout, r.stdout
+    assert r.stdout.count("identical") == 6 and "DIFFERENT" not in r.stdout, r.stdout
