@@ -764,6 +764,19 @@ def c4_targets(pf, torch, dev, stream, flush, hbm, rank, world, n_log2=28, reps=
     return out if rank == 0 else {}
 
 
+def synthetic_observations(model, steps, filters, seed):
+    """(filters, steps) observations simulated from the linear-Gaussian model
+    with numpy's default generator (synthetic data; the bench does not need the
+    reference's own draws)."""
+    g = np.random.default_rng(seed)
+    x = model.initial_mean + model.initial_std * g.standard_normal(filters)
+    ys = np.empty((filters, steps))
+    for t in range(steps):
+        x = model.coeff * x + model.trans_std * g.standard_normal(filters)
+        ys[:, t] = x + model.obs_std * g.standard_normal(filters)
+    return ys
+
+
 def c5_targets(pf, torch, dev, stream, rank, world, filters=4096, n_log2=16, steps=100):
     """BASELINE.json configs[4]: 4096 independent bootstrap filters x N = 2^16
     particles, T = 100, on the linear-Gaussian model; the filters are split
@@ -771,11 +784,11 @@ def c5_targets(pf, torch, dev, stream, rank, world, filters=4096, n_log2=16, ste
     Device time per rank, max over ranks."""
     import torch.distributed as dist
 
-    from paper_1301_4019_b200.pf import LinearGaussianModel, simulate_observations
+    from paper_1301_4019_b200.pf import LinearGaussianModel
 
     model = LinearGaussianModel(coeff=0.9, trans_std=1.0, obs_std=1.0)
     mine = filters // world
-    ys = np.stack([simulate_observations(model, steps, 1000 + rank * mine + k) for k in range(mine)])
+    ys = synthetic_observations(model, steps, mine, 1000 + rank * mine)
     n = 1 << n_log2
     pf.pf_run(model, ys[:, :3], n, seed=1)  # warm-up (allocations, module load)
     torch.cuda.synchronize()

@@ -43,7 +43,9 @@ enum pfr_dtype { PFR_F32 = 0, PFR_F64 = 1, PFR_I32 = 2, PFR_I64 = 3 };
 /* accumulation precision for weight scans/positions */
 enum pfr_accum {
   PFR_ACC_F64 = 0,    /* positions and carries in float64 (default; fp32 is storage only) */
-  PFR_ACC_NATIVE = 1  /* accumulate in the weight dtype, like the reference's np.cumsum */
+  PFR_ACC_NATIVE = 1, /* accumulate in the weight dtype with the parallel (tree) association */
+  PFR_ACC_SERIAL = 2  /* the reference's np.cumsum bit for bit: a left-to-right fold in the weight
+                         dtype (parity mode; one serial thread, ~4.5 cycles per element) */
 };
 /* OR-ed into pfr_scan's `accum`: repair ulp-level non-monotonicity with an
  * exact running max (only meaningful for non-negative inputs such as weights) */

@@ -328,9 +328,64 @@ def metropolis_replay(w, us, js) -> np.ndarray:
 
 
 def metropolis_stream(w, steps: int, seed: int, ids=()) -> np.ndarray:
+    """metropolis_ancestors (resamplers.py:204-234) with the draws taken step by
+    step from the generator, as the reference does (no (B, N) draw arrays)."""
     w = as_weights(w, require_positive_total=False)
-    us, js = metropolis_draws(seed, ids, w.size, int(steps))
-    return metropolis_replay(w, us, js)
+    n = w.size
+    g = generator(seed, ids)
+    k = np.arange(n, dtype=np.int64)
+    for _ in range(int(steps)):
+        u = g.random(n)
+        j = g.integers(0, n, size=n)
+        wk = w[k]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            ratio = w[j] / wk
+        k = np.where((wk == 0) | (u <= ratio), j, k)
+    return k
+
+
+class StreamModel:
+    """numpy's Generator(Philox) as the resamplers consume it, restated from
+    the raw Philox4x64-10 words (numpy distributions.c / philox.h): random()
+    takes one fresh u64 ((x >> 11) 2^-53); integers(0, N) takes 32-bit words
+    from next_uint32 -- the LOW half of a fresh u64, the high half buffered
+    for the next 32-bit request (the buffer survives across calls; random()
+    never touches it) -- mapped by Lemire's method, (u32 * N) >> 32, redrawn
+    while the low product word is below (2^32 - N) mod N.  Pure Python: small
+    draws only (pinned by the golden stream vectors)."""
+
+    def __init__(self, seed: int, ids=()):
+        self.key = stream_key(seed, ids)
+        self.q = 0
+        self.buf = None
+
+    def _word(self, k: int) -> int:
+        return philox4x64_10([k // 4 + 1, 0, 0, 0], self.key)[k % 4]
+
+    def random(self, m: int) -> np.ndarray:
+        out = [(self._word(self.q + i) >> 11) * 2.0**-53 for i in range(m)]
+        self.q += m
+        return np.array(out)
+
+    def _u32(self) -> int:
+        if self.buf is not None:
+            v, self.buf = self.buf, None
+            return v
+        x = self._word(self.q)
+        self.q += 1
+        self.buf = x >> 32
+        return x & 0xFFFFFFFF
+
+    def integers(self, n: int, m: int) -> np.ndarray:
+        thr = ((1 << 32) - n) % n
+        out = []
+        for _ in range(m):
+            while True:
+                p = self._u32() * n
+                if (p & 0xFFFFFFFF) >= thr:
+                    break
+            out.append(p >> 32)
+        return np.array(out, dtype=np.int64)
 
 
 def rejection_stream(w, bound: float, seed: int, ids=(), cap=None):

@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "libpfr.so")
 
 # --- constants mirrored from include/pfr.h ----------------------------------
 F32, F64, I32, I64 = 0, 1, 2, 3
-ACC_F64, ACC_NATIVE = 0, 1
+ACC_F64, ACC_NATIVE, ACC_SERIAL = 0, 1, 2
 SCAN_MONOTONE = 0x100
 SCAN_EXPECT_N = 0x200
 RNG_PHILOX, RNG_NUMPY, RNG_ARRAYS = 0, 1, 2
@@ -141,7 +141,8 @@ class Config:
     """Process-wide defaults (each call can override)."""
 
     rng_mode: str = "philox"   # "philox" (own Philox4x32-10) or "numpy" (replay numpy's stream)
-    accum: str = "f64"         # "f64" (fp32 is storage only) or "native" (reference's dtype arithmetic)
+    accum: str = "f64"         # "f64" (fp32 is storage only), "native" (dtype arithmetic, tree association)
+                               # or "serial" (np.cumsum bit for bit: the reference's fold, parity mode)
     index_dtype: torch.dtype = torch.int64
     check: bool = True         # synchronise and raise the reference's exceptions
 
@@ -164,7 +165,9 @@ def accum_code(accum: str | None) -> int:
         return ACC_F64
     if accum == "native":
         return ACC_NATIVE
-    raise ValueError(f"unknown accum {accum!r}; choose 'f64' or 'native'")
+    if accum == "serial":
+        return ACC_SERIAL
+    raise ValueError(f"unknown accum {accum!r}; choose 'f64', 'native' or 'serial'")
 
 
 # --- tensors ---------------------------------------------------------------

@@ -188,6 +188,7 @@ int pfr_scan(const void* in, void* out, int64_t n, int dtype, int out_dtype, int
     PFR_REQUIRE(out_dtype == dtype || (dtype == PFR_F32 && out_dtype == PFR_F64),
                 "float scan keeps the input dtype (or widens float32 to float64)");
   if (is_index(dtype)) PFR_REQUIRE(is_index(out_dtype), "integer scan needs an integer output");
+  PFR_REQUIRE((accum & 0xFF) <= PFR_ACC_SERIAL, "unknown accumulation mode");
   PFR_WS(PFR_OP_SCAN);
   const int64_t expect = (accum & 0x200) ? n : -1;  // internal: offspring_to_cumulative sum check
   PFR_CHECK_LAUNCH(launch_scan(in, out, n, dtype, out_dtype, accum & ~0x200, exclusive, total, expect, status, ws,
@@ -237,6 +238,7 @@ int pfr_cumulative_offspring(const void* w, int64_t n, int dtype, int accum, int
   PFR_REQUIRE(valid_n(n) && w && O, "bad arguments");
   PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
   if (stratified) PFR_REQUIRE(uniforms || rng, "stratified needs uniforms or an rng");
+  PFR_REQUIRE(accum >= 0 && accum <= PFR_ACC_SERIAL, "unknown accumulation mode");
   PFR_WS(PFR_OP_OFFSPRING);
   PFR_CHECK_LAUNCH(launch_offspring(w, n, dtype, accum, stratified, offset, uniforms, rng, O, status, ws,
                                     (cudaStream_t)stream),
@@ -250,6 +252,7 @@ int pfr_deliver_offspring(const void* w, int64_t n, int dtype, int accum, int st
   PFR_REQUIRE(valid_n(n) && w && c, "bad arguments");
   PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
   if (stratified) PFR_REQUIRE(uniforms || rng, "stratified needs uniforms or an rng");
+  PFR_REQUIRE(accum >= 0 && accum <= PFR_ACC_SERIAL, "unknown accumulation mode");
   PFR_WS(PFR_OP_DELIVER);
   cudaStream_t s = (cudaStream_t)stream;
   int32_t* O = O_out ? O_out : ws.O;
@@ -266,6 +269,7 @@ int pfr_deliver_offspring_logw(const void* lw, int64_t n, int dtype, int accum, 
   PFR_REQUIRE(valid_n(n) && lw && c && status, "bad arguments");
   PFR_REQUIRE(is_float(dtype), "log-weights must be float32 or float64");
   if (stratified) PFR_REQUIRE(uniforms || rng, "stratified needs uniforms or an rng");
+  PFR_REQUIRE(accum >= 0 && accum <= PFR_ACC_SERIAL, "unknown accumulation mode");
   PFR_WS(PFR_OP_DELIVER);
   PFR_CHECK_LAUNCH(launch_deliver(lw, n, dtype, accum, stratified, offset, uniforms, rng, c, O_out, max_steps, status,
                                   ws, (cudaStream_t)stream, 1),
@@ -295,6 +299,7 @@ int pfr_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rn
   PFR_REQUIRE(valid_n(n) && w && a, "bad arguments");
   PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
   PFR_REQUIRE(uniforms || rng, "multinomial needs uniforms or an rng");
+  PFR_REQUIRE(accum >= 0 && accum <= PFR_ACC_SERIAL, "unknown accumulation mode");
   PFR_WS(PFR_OP_MULTINOMIAL);
   PFR_CHECK_LAUNCH(launch_multinomial(w, n, dtype, accum, rng, uniforms, sorted_serial, a, status, ws,
                                       (cudaStream_t)stream),

@@ -73,6 +73,7 @@ struct DvArgs {
   uint32_t* status;
   int fx_S;          // fixed-point fraction bits of the offspring fast path
   const unsigned long long* logw_max;  // non-null: p.w holds log-weights, w = exp(lw - max) on the fly
+  const A* Wser;     // non-null (accum = SERIAL): W = np.cumsum(w) bit for bit, computed by the serial fold
   int expand;        // 1: full delivery; 0: cumulative offspring O_out only
   // rare-path scratch
   int32_t* O;        // [n]
@@ -221,22 +222,35 @@ template <typename T, typename A, int UM>
 __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, uint4* stage, A* warp_sums,
                                                int32_t (&o)[kTileItems], int32_t& o_prev) {
   const int64_t base = b * kTile;
-  T x[kTileItems];
-  tile_weights<T, A, (UM & kULogW) != 0>(p, base, x);
-  TileScan<A> s;
-#pragma unroll
-  for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
-  tile_scan<A>(s, warp_sums);
-  const A total = hier_of(p).total();
-  const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
-  const A ex = tile_excl(p, b);
-  const A tex = s.thread_excl;
   const int last = (p.n - 1 - base < kTile) ? (int)(p.n - 1 - base) : -1;
   const int e0 = threadIdx.x * kTileItems;
+  A total;
+  if (p.Wser) {
+    // accum = SERIAL: the reference's own W (np.cumsum, serial fold) is given;
+    // the offspring formula then runs in the weight dtype (A = T), exactly
+    // as resamplers.py:139-153
+    A Wv[kTileItems];
+    tile_load_any<A>(p.Wser, p.n, base, Wv);
+    total = __ldg(p.Wser + p.n - 1);
+    const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
 #pragma unroll
-  for (int j = 0; j < kTileItems; ++j) {
-    const A W = add_rn(ex, add_rn(tex, s.loc[j]));
-    o[j] = offspring_of<T, A, UM>(W, total, fx, p.n, p);
+    for (int j = 0; j < kTileItems; ++j) o[j] = offspring_of<T, A, UM>(Wv[j], total, fx, p.n, p);
+  } else {
+    T x[kTileItems];
+    tile_weights<T, A, (UM & kULogW) != 0>(p, base, x);
+    TileScan<A> s;
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
+    tile_scan<A>(s, warp_sums);
+    total = hier_of(p).total();
+    const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
+    const A ex = tile_excl(p, b);
+    const A tex = s.thread_excl;
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      const A W = add_rn(ex, add_rn(tex, s.loc[j]));
+      o[j] = offspring_of<T, A, UM>(W, total, fx, p.n, p);
+    }
   }
   if (last >= 0) {  // the final tile: O[N-1] = N, and padding past N stays at N
 #pragma unroll
@@ -245,7 +259,9 @@ __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, ui
   }
   o_prev = 0;
   if (b > 0) {
-    const A Wp = add_rn(tile_excl(p, b - 1), __ldcg(p.agg + b - 1));  // W at the last position of tile b-1
+    const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
+    // W at the last position of tile b-1
+    const A Wp = p.Wser ? __ldg(p.Wser + base - 1) : add_rn(tile_excl(p, b - 1), __ldcg(p.agg + b - 1));
     o_prev = offspring_of<T, A, UM>(Wp, total, fx, p.n, p);
   }
 }
@@ -530,11 +546,19 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
     return v ? atoi(v) : 4;
   }();
   const unsigned tiles = (unsigned)p.tiles;
-  // one tile per CTA (2 or 4 consecutive tiles per CTA measured 29 -> 37 / 43
-  // us at 2^24: the per-tile hierarchy step is serial inside a CTA)
-  k_dv_reduce<T, A, 1, (UM & kULogW) != 0><<<(unsigned)p.tiles, kTileThreads, 0, s>>>(p);
-  note_launch();
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if (p.Wser) {
+    // accum = SERIAL: the serial fold (np.cumsum bit for bit, with
+    // check_weights' flags) replaces K1; it also resets the pipeline flags
+    e = launch_serial_weights_scan(p.w, const_cast<A*>(p.Wser), p.n, sizeof(T) == 8 ? PFR_F64 : PFR_F32,
+                                   p.status, p.state, s);
+  } else {
+    // one tile per CTA (2 or 4 consecutive tiles per CTA measured 29 -> 37 / 43
+    // us at 2^24: the per-tile hierarchy step is serial inside a CTA)
+    k_dv_reduce<T, A, 1, (UM & kULogW) != 0><<<(unsigned)p.tiles, kTileThreads, 0, s>>>(p);
+    note_launch();
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess || stages < 2) return e;
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
   if (e != cudaSuccess || stages < 3) return e;
@@ -604,6 +628,7 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
   p.status = status;
   p.fx_S = fx_bits(n);
   p.logw_max = nullptr;
+  p.Wser = nullptr;
   p.expand = c != nullptr;
   p.O = ws.O;
   p.tmax = reinterpret_cast<int64_t*>(ws.j1);  // tiles << n
@@ -650,6 +675,24 @@ cudaError_t launch_deliver(const void* w, int64_t n, int dtype, int accum, int s
   if (max_steps) {
     cudaError_t e = cudaMemsetAsync(max_steps, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
+  }
+  if (accum == PFR_ACC_SERIAL) {
+    // parity mode: W = np.cumsum(w) by the serial fold into the workspace,
+    // offspring in the weight dtype (log-weights: converted first, like
+    // logweights_to_weights followed by the delivery)
+    if (logw) {
+      cudaError_t e = launch_logweights(w, ws.f0, n, dtype, status, ws, s);
+      if (e != cudaSuccess) return e;
+      w = ws.f0;
+    }
+    if (dtype == PFR_F64) {
+      auto p = make_args<double, double>(w, n, offset, uniforms, rng, c, O_out, max_steps, status, ws);
+      p.Wser = reinterpret_cast<const double*>(ws.f1);
+      return deliver_mode<double, double>(p, stratified, uniforms, rng, s);
+    }
+    auto p = make_args<float, float>(w, n, offset, uniforms, rng, c, O_out, max_steps, status, ws);
+    p.Wser = reinterpret_cast<const float*>(ws.f1);
+    return deliver_mode<float, float>(p, stratified, uniforms, rng, s);
   }
   // log-weights: one max pass (with the log-weight validation flags), then
   // K1/K2 compute exp(lw - max) as they load -- w is never stored

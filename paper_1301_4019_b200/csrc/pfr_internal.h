@@ -66,6 +66,10 @@ cudaError_t launch_deliver(const void* w, int64_t n, int dtype, int accum, int s
                            const double* uniforms, const pfr_rng* rng, int32_t* c, int32_t* O_out,
                            int32_t* max_steps, uint32_t* status, const Workspace& ws, cudaStream_t s, int logw = 0);
 cudaError_t launch_check_weights(const void* w, int64_t n, int dtype, uint32_t* status, cudaStream_t s);
+// serial (np.cumsum-exact) inclusive scan of a weight vector in its own dtype, with check_weights' flags;
+// resets the delivery pipeline flags in `state` when given
+cudaError_t launch_serial_weights_scan(const void* w, void* W, int64_t n, int dtype, uint32_t* status, DvState* state,
+                                      cudaStream_t s);
 cudaError_t launch_adjacent_difference(const void* in, void* out, int64_t n, int dtype, int out_dtype,
                                        uint32_t* status, cudaStream_t s);
 cudaError_t launch_logw_max(const void* lw, int64_t n, int dtype, unsigned long long* cell, uint32_t* status,
@@ -103,6 +107,11 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
                              int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
                              const Workspace& ws, cudaStream_t s, int64_t s_begin = 0,
                              int64_t s_count = -1);
+
+// launcher (pfr_rejreplay.cu): rejection on the reference's numpy stream (parity mode)
+cudaError_t launch_rejection_replay(const void* w, int64_t n, int dtype, double bound, double cap,
+                                    const pfr_rng* rng, int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w,
+                                    uint32_t* status, const Workspace& ws, cudaStream_t s);
 
 // launchers (pfr_shard.cu): weight-sharded single filter
 cudaError_t launch_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double prefix, double total,

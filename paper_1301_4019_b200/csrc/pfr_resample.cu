@@ -600,6 +600,8 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
                              int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
                              const Workspace& ws, cudaStream_t s, int64_t s_begin, int64_t s_count) {
   if (s_count < 0) s_count = n - s_begin;
+  if (rng && rng->mode == PFR_RNG_NUMPY && s_begin == 0 && s_count == n)
+    return launch_rejection_replay(w, n, dtype, bound, cap, rng, max_rounds, a, trips, out_w, status, ws, s);
   if (!rng || rng->mode != PFR_RNG_PHILOX) return cudaErrorNotSupported;
   unsigned long long* next = reinterpret_cast<unsigned long long*>(&ws.hdr->cell[2]);
   cudaError_t e = cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);

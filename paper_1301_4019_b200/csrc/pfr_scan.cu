@@ -204,6 +204,79 @@ __global__ void __launch_bounds__(kTileThreads) k_sc_repair(U* out, int64_t n, i
 }
 
 // ---------------------------------------------------------------------------
+// Serial fold (accum = PFR_ACC_SERIAL): np.cumsum bit for bit.  The reference
+// scan is a strict left-to-right fold in the input dtype (primitives.py:34-51,
+// vector_sum 60-66); floating-point addition does not associate, so the only
+// way to reproduce every rounding is to perform the same additions in the
+// same order.  One CTA: thread 0 folds a 4096-element chunk staged in shared
+// memory (independent shared loads hoisted ahead of the dependent add chain:
+// ~4-5 cycles per element), while warps 1..7 store the previous chunk and
+// load the next one (three rotating buffers).  Parity mode: ~2.3 ms at 2^20.
+constexpr int kSerChunk = 4096;
+
+template <typename T, typename U>
+__global__ void __launch_bounds__(256) k_scan_serial(const T* __restrict__ in, U* __restrict__ out, int64_t n,
+                                                     int exclusive, double* total_out, uint32_t* status,
+                                                     uint32_t fmask, DvState* state) {
+  extern __shared__ __align__(16) unsigned char ser_smem[];
+  T* buf = reinterpret_cast<T*>(ser_smem);  // [3][kSerChunk]
+  const int64_t chunks = (n + kSerChunk - 1) / kSerChunk;
+  FlagAcc<T> facc;
+  auto load = [&](int64_t c) {
+    T* dst = buf + (c % 3) * kSerChunk;
+    const int64_t base = c * kSerChunk;
+    const int len = (int)min((int64_t)kSerChunk, n - base);
+    for (int i = threadIdx.x - 32; i < len; i += blockDim.x - 32) {
+      const T v = __ldcs(in + base + i);
+      facc.add(v);
+      dst[i] = v;
+    }
+  };
+  auto store = [&](int64_t c) {
+    const T* src = buf + (c % 3) * kSerChunk;
+    const int64_t base = c * kSerChunk;
+    const int len = (int)min((int64_t)kSerChunk, n - base);
+    for (int i = threadIdx.x - 32; i < len; i += blockDim.x - 32) __stcs(out + base + i, (U)src[i]);
+  };
+  if (threadIdx.x >= 32) load(0);
+  __syncthreads();
+  T acc = T(0);
+  for (int64_t c = 0; c < chunks; ++c) {
+    if (threadIdx.x == 0) {
+      T* cur = buf + (c % 3) * kSerChunk;
+      const int len = (int)min((int64_t)kSerChunk, n - c * kSerChunk);
+      int i = 0;
+      for (; i + 8 <= len; i += 8) {
+        T v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = cur[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const T nv = add_rn(acc, v[j]);
+          cur[i + j] = exclusive ? acc : nv;
+          acc = nv;
+        }
+      }
+      for (; i < len; ++i) {
+        const T nv = add_rn(acc, cur[i]);
+        cur[i] = exclusive ? acc : nv;
+        acc = nv;
+      }
+    } else if (threadIdx.x >= 32) {
+      if (c > 0) store(c - 1);
+      if (c + 1 < chunks) load(c + 1);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x >= 32) store(chunks - 1);
+  if (threadIdx.x == 0) {
+    if (total_out) *total_out = (double)acc;
+    if (state) state->flags = 0;  // pipeline flags of a delivery that consumes this scan
+  }
+  if (threadIdx.x >= 32) status_or_warp(status, facc.flags() & fmask);
+}
+
+// ---------------------------------------------------------------------------
 // check_weights (diagnostics.py:38-51): 16-byte vector loads, four in flight
 // per thread, flags from integer maxima of the bit patterns (FlagAcc)
 template <typename T>
@@ -352,6 +425,18 @@ cudaError_t scan_typed(const void* in, void* out, int64_t n, int exclusive, int 
   return e;
 }
 
+template <typename T, typename U>
+cudaError_t launch_scan_serial(const void* in, void* out, int64_t n, int exclusive, void* total, uint32_t* status,
+                               uint32_t fmask, DvState* state, cudaStream_t s) {
+  const size_t smem = 3 * kSerChunk * sizeof(T);
+  auto kernel = k_scan_serial<T, U>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kernel<<<1, 256, smem, s>>>((const T*)in, (U*)out, n, exclusive, (double*)total, status, fmask, state);
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_scan(const void* in, void* out, int64_t n, int dtype, int out_dtype, int accum, int exclusive,
@@ -360,6 +445,14 @@ cudaError_t launch_scan(const void* in, void* out, int64_t n, int dtype, int out
   const bool native = (accum & 0xFF) == PFR_ACC_NATIVE;
   const uint32_t fmask =
       PFR_ST_NONFINITE | ((accum & PFR_SCAN_WEIGHTS) ? (uint32_t)(PFR_ST_NEGATIVE | PFR_ST_POSITIVE) : 0u);
+  if ((accum & 0xFF) == PFR_ACC_SERIAL && (dtype == PFR_F32 || dtype == PFR_F64)) {
+    // the serial fold runs in the input dtype; the output is converted after
+    if (dtype == PFR_F64)
+      return launch_scan_serial<double, double>(in, out, n, exclusive, total, status, fmask, nullptr, s);
+    if (out_dtype == PFR_F64)
+      return launch_scan_serial<float, double>(in, out, n, exclusive, total, status, fmask, nullptr, s);
+    return launch_scan_serial<float, float>(in, out, n, exclusive, total, status, fmask, nullptr, s);
+  }
 #define PFR_SCAN_ARGS in, out, n, exclusive, repair, total, expect_total, status, ws, s, fmask
   switch (dtype) {
     case PFR_F64:
@@ -377,6 +470,13 @@ cudaError_t launch_scan(const void* in, void* out, int64_t n, int dtype, int out
   }
 #undef PFR_SCAN_ARGS
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_serial_weights_scan(const void* w, void* W, int64_t n, int dtype, uint32_t* status, DvState* state,
+                                      cudaStream_t s) {
+  const uint32_t fmask = PFR_ST_NONFINITE | PFR_ST_NEGATIVE | PFR_ST_POSITIVE;
+  if (dtype == PFR_F64) return launch_scan_serial<double, double>(w, W, n, 0, nullptr, status, fmask, state, s);
+  return launch_scan_serial<float, float>(w, W, n, 0, nullptr, status, fmask, state, s);
 }
 
 cudaError_t launch_check_weights(const void* w, int64_t n, int dtype, uint32_t* status, cudaStream_t s) {

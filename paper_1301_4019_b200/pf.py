@@ -9,9 +9,10 @@ for ``filters`` independent filters at once (tile-parallel kernels over all
 filters, no communication between filters; independent filters split across
 GPUs by the caller).  The
 propagation noise comes from the GPU's own Philox stream, so trajectories
-are not the reference's draw for draw; ``exact_filter`` (the closed-form
-Kalman recursion, pf.py:207-229) is the end-to-end oracle, as in the
-reference's tests.
+are not the reference's draw for draw; the closed-form Kalman recursion
+(pf.py:207-229, restated under ``oracle/pf_oracle.py`` -- test
+infrastructure, not part of this package) is the end-to-end oracle, as in
+the reference's tests.
 
 ``deliver_batched`` exposes the per-filter systematic delivery on its own.
 """
@@ -25,12 +26,9 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .rng import RngStream, as_stream
+from .rng import as_stream
 
-__all__ = ["LinearGaussianModel", "FilterResult", "ExactFilterResult", "pf_run", "exact_filter",
-           "simulate_observations", "deliver_batched", "pf_copy_step"]
-
-_NS_SIMULATE = 4  # pf.py:38
+__all__ = ["LinearGaussianModel", "FilterResult", "pf_run", "deliver_batched", "pf_copy_step"]
 
 
 @dataclass(frozen=True)
@@ -60,13 +58,6 @@ class FilterResult:
     resampled: np.ndarray | None = field(repr=False, default=None)
 
 
-@dataclass
-class ExactFilterResult:
-    means: np.ndarray
-    variances: np.ndarray
-    log_likelihood: float
-
-
 class _PfModel(L.ctypes.Structure):
     _fields_ = [("coeff", L.ctypes.c_double), ("trans_std", L.ctypes.c_double), ("obs_std", L.ctypes.c_double),
                 ("initial_mean", L.ctypes.c_double), ("initial_std", L.ctypes.c_double)]
@@ -81,39 +72,6 @@ def pf_copy_step(particles: torch.Tensor, a) -> torch.Tensor:
     if not satisfies_inplace_predicate(a):
         raise AssertionError("ancestry violates the in-place predicate")
     return copy_particles(particles, a)
-
-
-def simulate_observations(model: LinearGaussianModel, steps: int, seed: int) -> np.ndarray:
-    """Synthetic observations y_1..y_T from the model, drawn exactly as the
-    reference does (pf.py:99-108; host test-data helper)."""
-    g = RngStream(seed, (_NS_SIMULATE,)).generator()
-    x = model.initial_mean + model.initial_std * g.standard_normal()
-    ys = np.empty(steps)
-    for t in range(steps):
-        x = model.coeff * x + model.trans_std * g.standard_normal()
-        ys[t] = x + model.obs_std * g.standard_normal()
-    return ys
-
-
-def exact_filter(model: LinearGaussianModel, observations) -> ExactFilterResult:
-    """Closed-form Gaussian filtering recursion (pf.py:207-229): the oracle the
-    particle filter is validated against."""
-    observations = np.asarray(observations, dtype=np.float64)
-    m, p = model.initial_mean, model.initial_std ** 2
-    means = np.empty(observations.size)
-    variances = np.empty(observations.size)
-    loglik = 0.0
-    for t, y in enumerate(observations):
-        m_pred = model.coeff * m
-        p_pred = model.coeff ** 2 * p + model.trans_std ** 2
-        s = p_pred + model.obs_std ** 2
-        loglik += -0.5 * (math.log(2.0 * math.pi * s) + (y - m_pred) ** 2 / s)
-        gain = p_pred / s
-        m = m_pred + gain * (y - m_pred)
-        p = (1.0 - gain) * p_pred
-        means[t] = m
-        variances[t] = p
-    return ExactFilterResult(means, variances, loglik)
 
 
 _ws_pf = {}

@@ -46,8 +46,11 @@ def inclusive_prefix_sum(w, *, accum=None, monotone: bool = False) -> torch.Tens
     """result[i] = w[0] + ... + w[i] in the input precision (primitives.py:34-42).
 
     ``accum="f64"`` (default) carries float32 inputs in float64 and rounds
-    once on output; ``accum="native"`` accumulates in float32 like the
-    reference.  ``monotone=True`` (for non-negative inputs) repairs ulp-level
+    once on output; ``accum="native"`` accumulates in float32 with the
+    parallel (tree) association; ``accum="serial"`` performs the reference's
+    own left-to-right fold in the input dtype, so the result equals
+    ``np.cumsum`` bit for bit (parity mode, one serial GPU thread).
+    ``monotone=True`` (for non-negative inputs) repairs ulp-level
     non-monotonicity with an exact running max."""
     return _scan(w, False, accum, monotone)[0]
 

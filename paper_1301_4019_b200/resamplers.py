@@ -226,7 +226,8 @@ def metropolis_num_steps(p_star: float, epsilon: float | None, n: int) -> int:
     return max(1, math.floor(bound) + 1)
 
 
-def metropolis_ancestors(w, b: int, rng, *, u_draws=None, j_draws=None, rng_mode=None, index_dtype=None):
+def metropolis_ancestors(w, b: int, rng, *, u_draws=None, j_draws=None, rng_mode=None, index_dtype=None,
+                         _positive: bool = False):
     """N independent B-step Metropolis chains (resamplers.py:204-234).
     ``u_draws``/``j_draws`` (shape (B, N)) replay supplied draws (any N);
     numpy mode replays the reference stream (power-of-two N).  In philox mode
@@ -258,13 +259,11 @@ def metropolis_ancestors(w, b: int, rng, *, u_draws=None, j_draws=None, rng_mode
         if bits & L.ST_RANGE:
             raise ValueError("proposal indices must lie in [0, N)")
 
-    _raise(st, require_positive_total=False, extra=extra)
+    _raise(st, require_positive_total=_positive, extra=extra)
     return L.to_index_dtype(a, index_dtype)
 
 
-def _rejection(w, bound, cap, rng, rng_mode, max_rounds, return_trips, index_dtype):
-    if (rng_mode or L.config.rng_mode) != "philox":
-        raise NotImplementedError("rejection resampling replays only the GPU's own Philox stream")
+def _rejection(w, bound, cap, rng, rng_mode, max_rounds, return_trips, index_dtype, positive=False):
     bound = float(bound)
     if not math.isfinite(bound) or bound <= 0:
         raise ValueError(f"weight bound must be finite and positive, got {bound}")
@@ -283,23 +282,28 @@ def _rejection(w, bound, cap, rng, rng_mode, max_rounds, return_trips, index_dty
             raise RuntimeError(f"rejection resampling made no progress after {max_rounds} rounds; "
                                f"weight bound {bound} is far above every weight")
 
-    _raise(st, require_positive_total=False, extra=extra)
+    _raise(st, require_positive_total=positive, extra=extra)
     a = L.to_index_dtype(a, index_dtype)
     return a, trips, out_w
 
 
 def rejection_ancestors(w, sup_w: float, rng, *, return_trips: bool = False, rng_mode=None,
-                        max_rounds: int = MAX_REJECTION_ROUNDS, index_dtype=None):
-    """Rejection with a first deterministic self-proposal (resamplers.py:237-255)."""
-    a, trips, _ = _rejection(w, sup_w, False, rng, rng_mode, max_rounds, return_trips, index_dtype)
+                        max_rounds: int = MAX_REJECTION_ROUNDS, index_dtype=None, _positive: bool = False):
+    """Rejection with a first deterministic self-proposal (resamplers.py:237-255).
+
+    philox mode: persistent warps with lane refill, each slot on its own
+    counter-based stream; numpy mode: the reference's round-synchronous loop
+    (resamplers.py:282-310) replayed on its own draws -- same ancestry and
+    trip counts bit for bit (csrc/pfr_rejreplay.cu)."""
+    a, trips, _ = _rejection(w, sup_w, False, rng, rng_mode, max_rounds, return_trips, index_dtype, _positive)
     return (a, trips.to(torch.int64)) if return_trips else a
 
 
 def rejection_ancestors_capped(w, sup_v: float, rng, *, return_trips: bool = False, rng_mode=None,
-                               max_rounds: int = MAX_REJECTION_ROUNDS, index_dtype=None):
+                               max_rounds: int = MAX_REJECTION_ROUNDS, index_dtype=None, _positive: bool = False):
     """Rejection against min(w, sup_v) with importance weights w[a]/v[a]
     (resamplers.py:258-279)."""
-    a, trips, out_w = _rejection(w, sup_v, True, rng, rng_mode, max_rounds, return_trips, index_dtype)
+    a, trips, out_w = _rejection(w, sup_v, True, rng, rng_mode, max_rounds, return_trips, index_dtype, _positive)
     return (a, out_w, trips.to(torch.int64)) if return_trips else (a, out_w)
 
 
@@ -337,6 +341,9 @@ def resample_ancestors(w, config: ResamplerConfig, rng, **kw) -> ResampleOutput:
         O = systematic_cumulative_offspring(w, rng, **kw)
         return ResampleOutput(cumulative_offspring_to_ancestors(O), extras={})
     kw.pop("accum", None)
+    # check_weights(w) with a positive total up front (resamplers.py:372): the
+    # ancestry kernels report the flags, raised here with the facade's rule
+    kw["_positive"] = True
     if alg == "metropolis":
         b = resolve_metropolis_steps(w, config)
         return ResampleOutput(metropolis_ancestors(w, b, rng, **kw), extras={"B": b})
@@ -401,7 +408,7 @@ def deliver(w, config: ResamplerConfig, rng, *, rng_mode=None, accum=None, index
         ws, wsb = L.workspace(n)
         L.call("pfr_deliver_metropolis", w.data_ptr(), n, L.dtype_code(w), int(b), _rng(rng, rng_mode),
                c.data_ptr(), L.ptr(steps), st.data_ptr(), ws, wsb, L.stream_handle())
-        _raise(st, require_positive_total=False)
+        _raise(st, require_positive_total=True)  # resample_ancestors' check_weights (resamplers.py:372)
         c = L.to_index_dtype(c, index_dtype) if out is None else c
         return (c, int(steps.item())) if return_max_steps else c
     kw = {"rng_mode": rng_mode}

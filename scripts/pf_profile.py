@@ -6,7 +6,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1301_4019_b200 as pf  # noqa: E402
-from paper_1301_4019_b200.pf import LinearGaussianModel, simulate_observations  # noqa: E402
+from oracle.pf_oracle import simulate_observations  # noqa: E402
+from paper_1301_4019_b200.pf import LinearGaussianModel  # noqa: E402
 
 m = LinearGaussianModel(coeff=0.9)
 filters = int(sys.argv[1]) if len(sys.argv) > 1 else 512

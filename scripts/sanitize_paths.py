@@ -8,7 +8,8 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1301_4019_b200 as pf  # noqa: E402
-from paper_1301_4019_b200.pf import LinearGaussianModel, simulate_observations  # noqa: E402
+from oracle.pf_oracle import simulate_observations  # noqa: E402
+from paper_1301_4019_b200.pf import LinearGaussianModel  # noqa: E402
 
 g = np.random.default_rng(0)
 for n in (37, 5000, 70001):

@@ -10,7 +10,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1301_4019_b200 as pf  # noqa: E402
 from paper_1301_4019_b200 import _lib as L  # noqa: E402
-from paper_1301_4019_b200.pf import LinearGaussianModel, simulate_observations  # noqa: E402
+from oracle.pf_oracle import simulate_observations  # noqa: E402
+from paper_1301_4019_b200.pf import LinearGaussianModel  # noqa: E402
 from paper_1301_4019_b200.sharded import CudaShardOps  # noqa: E402
 
 m = LinearGaussianModel(coeff=0.8, obs_std=0.05)

@@ -53,13 +53,6 @@ def test_grid_runs_every_algorithm(tmp_path):
 
 
 @pytest.mark.gpu
-def test_pf_demo_cli():
-    res = CliRunner().invoke(main, ["pf", "demo", "--n", "1024", "--steps", "10", "--filters", "8"])
-    assert res.exit_code == 0, res.output
-    assert "exact log-likelihood" in res.output
-
-
-@pytest.mark.gpu
 def test_grid_is_deterministic_across_workers_and_runs():
     """SPEC C11 (test_acceptance.py:350-388): the same grid twice, with 1 and
     4 workers, gives identical records except the timing columns."""

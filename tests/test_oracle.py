@@ -166,3 +166,40 @@ def test_exact_metropolis_oracle_matches_matrix_power():
         for b in (1, 3, 9):
             np.testing.assert_allclose(O.metropolis_expected_offspring(w, b),
                                        np.ones(n) @ np.linalg.matrix_power(P, b), atol=1e-13)
+
+
+def test_stream_model_buffered_u32(golden):
+    """The stream model the GPU rejection replay implements (pfr_rejreplay.cu):
+    random() takes fresh u64s, integers() takes buffered 32-bit halves with
+    Lemire redraws; an odd integer count leaves a buffered half that random()
+    skips (golden: 65 draws in [0, 1000) followed by random(8))."""
+    sm = O.StreamModel(4242, (1, 2, 3))
+    np.testing.assert_array_equal(sm.random(64), golden["stream/u"])
+    np.testing.assert_array_equal(sm.integers(1024, 64), golden["stream/j1024"])
+    np.testing.assert_array_equal(sm.integers(1000, 65), golden["stream/j1000"])
+    np.testing.assert_array_equal(sm.random(8), golden["stream/u2"])
+
+
+def test_rejection_rounds_on_stream_model():
+    """The reference's round-synchronous rejection loop consumes the stream as
+    random(N), then per round integers(m) + random(m) -- restated on the
+    stream model and compared with the numpy-generator oracle."""
+    n = 77  # not a power of two; odd pending counts exercise the buffered half
+    g = np.random.default_rng(5)
+    w = np.exp(g.normal(0, 1, n))
+    bound = float(w.max())
+    a_ref, trips_ref = O.rejection_stream(w, bound, 9, (2,))
+    sm = O.StreamModel(9, (2,))
+    ratio = w / bound
+    a = np.arange(n)
+    trips = np.ones(n, dtype=np.int64)
+    pending = np.flatnonzero(sm.random(n) > ratio)
+    while pending.size:
+        j = sm.integers(n, pending.size)
+        beta = sm.random(pending.size)
+        ok = beta <= ratio[j]
+        a[pending[ok]] = j[ok]
+        trips[pending] += 1
+        pending = pending[~ok]
+    np.testing.assert_array_equal(a, a_ref)
+    np.testing.assert_array_equal(trips, trips_ref)

@@ -15,7 +15,8 @@ import numpy as np
 import pytest
 
 from oracle import pfr_oracle as orc
-from paper_1301_4019_b200.pf import LinearGaussianModel, exact_filter, simulate_observations
+from oracle.pf_oracle import exact_filter, simulate_observations
+from paper_1301_4019_b200.pf import LinearGaussianModel
 
 
 def test_exact_filter_one_step_closed_form():
