@@ -20,7 +20,8 @@
 // 1)[k % 4] (pfr_rng.cuh); random() = (u64 >> 11) 2^-53; integers(0, N)
 // takes 32-bit words from next_uint32, which returns the LOW half of a fresh
 // u64 and keeps the high half buffered for the next 32-bit request (the
-// buffer survives across calls; random() never touches it), mapped by
+// buffer survives across calls, so it can hold a word from before the
+// previous random() call; random() never touches it), mapped by
 // Lemire's method: j = (u32 * N) >> 32, redrawn while the low word is below
 // (2^32 - N) mod N.  A power-of-two N never redraws; otherwise a redraw
 // (probability ~N/2^32 per draw) shifts every later draw of its round, so
@@ -46,13 +47,14 @@ constexpr int64_t kTailM = 16384;
 
 struct StreamPos {
   uint64_t q;   // next fresh u64 index
-  uint32_t bf;  // 1: the high half of u64 q-1 is buffered for next_uint32
+  uint64_t bq;  // the u64 whose high half is buffered (valid when bf)
+  uint32_t bf;  // 1: a high half is buffered for next_uint32
 };
 
 // t-th 32-bit request of an integers() call starting at state s
 __device__ __forceinline__ uint32_t stream_u32(Key2x64 key, StreamPos s, uint64_t t) {
   if (s.bf) {
-    if (t == 0) return (uint32_t)(numpy_raw64(key, s.q - 1) >> 32);
+    if (t == 0) return (uint32_t)(numpy_raw64(key, s.bq) >> 32);
     t -= 1;
   }
   const uint64_t x = numpy_raw64(key, s.q + t / 2);
@@ -68,6 +70,7 @@ __device__ __forceinline__ StreamPos stream_after_u32(StreamPos s, uint64_t u32s
   }
   s.q += (u32s + 1) / 2;
   s.bf = (uint32_t)(u32s & 1);
+  s.bq = s.q - 1;  // an odd count leaves the high half of the last fresh word
   return s;
 }
 
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(kRrThreads) k_rej_replay(RrArgs<T> p) {
       run += tot;
     }
   }
-  StreamPos st{(uint64_t)n, 0u};  // random(N) consumed N fresh words
+  StreamPos st{(uint64_t)n, 0u, 0u};  // random(N) consumed N fresh words
   int32_t* L = p.list0;
   int32_t* Ln = p.list1;
   sync();
