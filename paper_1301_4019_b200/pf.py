@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .rng import as_stream
+from .rng import RngStream, as_stream
 
 __all__ = ["LinearGaussianModel", "FilterResult", "pf_run", "deliver_batched", "pf_copy_step"]
 
