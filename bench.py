@@ -34,6 +34,7 @@ import argparse
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -181,6 +182,24 @@ def cpu_step(n, pool, seed=0):
     return time.perf_counter() - t0
 
 
+def host_cpu_info() -> dict:
+    """nproc and the CPU model of this host (the CPU arm states its hardware)."""
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        affinity = os.cpu_count() or 1
+    return {"nproc": affinity, "cpu_count": os.cpu_count(), "cpu_model": model or "unknown"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -202,7 +221,8 @@ def run_reference(args, rank, world):
         "config": workload_config(n, world),
         "cpu_baseline": {"value": value, "unit": "particles/s", "cores": cores, "kind": "port",
                          "sample": f"the full step: 5 resamplers x (f32, f64) at N=2^{int(math.log2(n))}, "
-                                   f"oracle/pfr_oracle.py (NumPy + Python chain walk) over a {cores}-process pool"},
+                                   f"oracle/pfr_oracle.py (NumPy + Python chain walk) over a {cores}-process pool",
+                         **host_cpu_info()},
         "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -556,7 +576,8 @@ def main():
             cpu_s = cpu_step(n, pool)
         cpu = {"value": units_per_step / cpu_s, "unit": "particles/s", "cores": cores, "kind": "port",
                "sample": f"one step (5 resamplers x f32/f64 at N=2^{int(math.log2(n))}) of the oracle port "
-                         f"(NumPy + Python chain walk, like the reference), {cores} processes, {cpu_s:.1f} s"}
+                         f"(NumPy + Python chain walk, like the reference), {cores} processes, {cpu_s:.1f} s",
+               **host_cpu_info()}
 
     if rank == 0:
         line = {

@@ -20,7 +20,7 @@ thread_local uint64_t g_launches = 0;
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t dv, hdr, sum, max, O, d, a, scratch, end;
+  size_t dv, hdr, sum, max, sub, O, d, a, scratch, end;
 };
 
 Layout layout(int64_t n) {
@@ -36,6 +36,8 @@ Layout layout(int64_t n) {
   off = align_up(off + cells, 256);
   L.max = off;
   off = align_up(off + cells, 256);
+  L.sub = off;  // per-subtile (512 elements) aggregates of the fused delivery
+  off = align_up(off + (size_t)(tiles * 8 + 16) * sizeof(uint64_t), 256);
   const size_t reset_end = off;
   (void)reset_end;
   L.O = off;
@@ -126,6 +128,7 @@ bool workspace_carve(void* base, size_t bytes, int64_t n, Workspace& ws) {
   ws.tiles = num_tiles(n);
   ws.sum_cells = reinterpret_cast<uint64_t*>(b + L.sum);
   ws.max_cells = reinterpret_cast<uint64_t*>(b + L.max);
+  ws.sub_cells = reinterpret_cast<uint64_t*>(b + L.sub);
   ws.reset_bytes = L.O - L.hdr;
   ws.bytes = bytes;
   if (bytes >= L.d) ws.O = reinterpret_cast<int32_t*>(b + L.O);

@@ -61,6 +61,7 @@ struct DvArgs {
   A* agg;        // [tiles]
   A* excl;       // see K1: in-group tile prefixes, total, group prefixes, tile flags
   A* sum_scratch;  // [groups] group totals
+  A* sub;        // [8 * tiles] subtile (512-element) aggregates, written by K1
   A u_sys;       // systematic offset (cast to the weight dtype)
   const double* uniforms;
   Key2x64 key;
@@ -145,6 +146,40 @@ __device__ __forceinline__ int32_t offspring_of(A W, A total, const FxParams& f,
   return offspring_exact<T, A, UM>(W, total, n, p);
 }
 
+// Branch-free fast path for the streaming loops: the fixed-point O and an
+// "unsafe" flag (the fractional part within the margin of an integer, or an
+// accumulator without the fast path); the caller redoes flagged elements with
+// offspring_exact after its loop, so the hot loop has no call and no
+// divergent branch.  Systematic: t = round(W * sfx + ufx) from ONE fma
+// against 2^52 + ufx (ufx is an integer, so this is round(W * sfx) + ufx up
+// to the tie rule, inside the same error bound); only t's fraction matters
+// because every stratum has the same offset (resamplers.py:145-153).
+template <typename T, typename A, int UM>
+__device__ __forceinline__ int32_t offspring_fast(A W, const FxParams& f, double csys, int32_t n, bool& unsafe,
+                                                  const DvArgs<A>& p) {
+  if constexpr (sizeof(A) == 8) {
+    if constexpr ((UM & 3) == kUSys) {
+      const double t = __fma_rn(W, f.sfx, csys);
+      const uint32_t lo = (uint32_t)__double2loint(t);
+      const uint32_t hi = (uint32_t)__double2hiint(t) - 0x43300000u;
+      const uint32_t o = f.S >= 32 ? hi : __funnelshift_r(lo, hi, f.S);
+      unsafe = ((lo + kFxMargin) & f.mask) <= 2 * kFxMargin;
+      return min((int32_t)o, n);
+    } else {
+      const long long r = fx_round(W, f.sfx);
+      long long k = (r >> f.S) + 1;
+      if (k > n) k = n;
+      if (k < 1) k = 1;
+      const long long t = r + fx_round((double)stratum_u<T, A, UM>(k - 1, p), f.scale);
+      unsafe = !(fx_safe(r, f.mask) && fx_safe(t, f.mask));
+      return min((int32_t)(t >> f.S), n);
+    }
+  } else {
+    unsafe = true;
+    return 0;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K1: one CTA per 4096-element tile: validation flags and the tile aggregate
 // (the tile-local inclusive value at its last position, in exactly the
@@ -154,11 +189,29 @@ __device__ __forceinline__ int32_t offspring_of(A W, A total, const FxParams& f,
 // the same expression as k_logw_exp, so both paths see identical weights);
 // positions past n stay 0
 template <typename T, typename A, bool LW>
-__device__ __forceinline__ void tile_weights(const DvArgs<A>& p, int64_t base, T (&x)[kTileItems]) {
-  tile_load_any<T>((const T*)p.w, p.n, base, x);
+__device__ __forceinline__ void lane_weights(const DvArgs<A>& p, int64_t e0, T (&x)[kTileItems]) {
+  constexpr int kPerVec = 16 / sizeof(T);
+  const T* in = (const T*)p.w;
+  if (e0 + kTileItems <= p.n && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    uint4 v[kTileItems / kPerVec];
+#pragma unroll
+    for (int q = 0; q < kTileItems / kPerVec; ++q) v[q] = __ldg(reinterpret_cast<const uint4*>(in + e0) + q);
+#pragma unroll
+    for (int q = 0; q < kTileItems / kPerVec; ++q) {
+      union {
+        uint4 u;
+        T e[kPerVec];
+      } tmp;
+      tmp.u = v[q];
+#pragma unroll
+      for (int e = 0; e < kPerVec; ++e) x[q * kPerVec + e] = tmp.e[e];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) x[j] = (e0 + j < p.n) ? in[e0 + j] : T(0);
+  }
   if constexpr (LW) {
     const T m = (T)from_ordered(__ldcg(p.logw_max));
-    const int64_t e0 = base + (int64_t)threadIdx.x * kTileItems;
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) {
       T v;
@@ -181,89 +234,195 @@ __device__ __forceinline__ A tile_excl(const DvArgs<A>& p, int64_t b) {
   return hier_of(p).tile_excl(b);
 }
 
+// ---------------------------------------------------------------------------
+// The association of W (fast path; fixed by indices alone, so deterministic).
+// A SUBTILE is 512 elements handled by one warp, 16 consecutive per lane.
+//   loc_j   serial inclusive sum of the lane's elements (in A)
+//   tex     exclusive Kogge-Stone scan of the lane totals (lane 0: 0)
+//   sub(s)  = tex(lane 31) + loc_15(lane 31)            (K1 stores it)
+//   Q_q(b)  = serial fold of sub(8b), ..., sub(8b + q - 1)  (Q_0 = 0)
+//   agg(b)  = Q_8(b), the tile aggregate the hierarchy scans (pfr_hier.cuh)
+//   SP(s)   = tile_excl(b) + Q_q(b)                 for s = 8b + q
+//   W       = SP(s) + (tex + loc_j)
+// so W at the last element of subtile s is SP(s) + sub(s), which the next
+// subtile recomputes from the same stored values for its O(prev): slot ranges
+// of neighbouring subtiles always meet exactly.
+constexpr int kSub = 32 * kTileItems;  // 512
+constexpr int kSubPerTile = kTile / kSub;  // 8
+
+// K1: one CTA per 4096-element tile: validation flags, the 8 subtile
+// aggregates and the tile aggregate; tile prefixes built hierarchically.
 template <typename T, typename A, int kTilesPerCta, bool LW = false>
 __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
-  __shared__ A warp_sums[kTileThreads / 32];
+  static_assert(kTilesPerCta == 1, "one tile per CTA");
+  __shared__ A warp_aggs[kTileThreads / 32];
+  __shared__ uint32_t warp_flags[kTileThreads / 32];
   __shared__ uint32_t cta_flags;
   __shared__ int stage;
-  // kTilesPerCta consecutive tiles per CTA, every load issued before the
-  // first reduction (launched with 1: more tiles per CTA, or a persistent
-  // double-buffered variant, measured slower)
-  const int64_t b0 = (int64_t)blockIdx.x * kTilesPerCta;
-  T x[kTilesPerCta][kTileItems];
+  const int64_t b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T x[kTileItems];
+  lane_weights<T, A, LW>(p, b * kTile + (int64_t)threadIdx.x * kTileItems, x);
+  FlagAcc<T> facc;
+  A loc = (A)x[0];
+  facc.add(x[0]);
 #pragma unroll
-  for (int t = 0; t < kTilesPerCta; ++t)
-    if (b0 + t < p.tiles) tile_weights<T, A, LW>(p, (b0 + t) * kTile, x[t]);
-#pragma unroll
-  for (int t = 0; t < kTilesPerCta; ++t) {
-    const int64_t b = b0 + t;
-    if (b >= p.tiles) break;  // CTA-uniform
-    if (threadIdx.x == 0) cta_flags = 0;
-    FlagAcc<T> facc;
-    TileScan<A> s;
-#pragma unroll
-    for (int j = 0; j < kTileItems; ++j) {
-      facc.add(x[t][j]);
-      s.loc[j] = (A)x[t][j];
-    }
-    tile_scan<A>(s, warp_sums);
-    if (threadIdx.x == kTileThreads - 1) p.agg[b] = add_rn(s.thread_excl, s.loc[kTileItems - 1]);
-    const uint32_t flags = __reduce_or_sync(0xffffffffu, facc.flags());
-    if ((threadIdx.x & 31) == 0 && flags) atomicOr(&cta_flags, flags);
-    hier_tile_done(hier_of(p), b, &cta_flags, &stage, p.status);
-    if (stage == 2 && threadIdx.x == 0) p.state->flags = 0;  // pipeline flags of this delivery
+  for (int j = 1; j < kTileItems; ++j) {
+    facc.add(x[j]);
+    loc = add_rn(loc, (A)x[j]);
   }
+  const A incl = warp_inclusive_scan(loc);
+  const A tex = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 31) {
+    const A sa = add_rn(tex, loc);
+    p.sub[b * kSubPerTile + warp] = sa;
+    warp_aggs[warp] = sa;
+  }
+  const uint32_t flags = __reduce_or_sync(0xffffffffu, facc.flags());
+  if (lane == 0) warp_flags[warp] = flags;
+  __syncthreads();
+  if (threadIdx.x == kTileThreads - 1) {
+    A t = warp_aggs[0];
+    uint32_t f = warp_flags[0];
+#pragma unroll
+    for (int w = 1; w < kTileThreads / 32; ++w) {
+      t = add_rn(t, warp_aggs[w]);
+      f |= warp_flags[w];
+    }
+    p.agg[b] = t;
+    cta_flags = f;
+  }
+  hier_tile_done(hier_of(p), b, &cta_flags, &stage, p.status);
+  if (stage == 2 && threadIdx.x == 0) p.state->flags = 0;  // pipeline flags of this delivery
+}
+
+// subtile s -> O of the lane's 16 elements, and O(prev) = O at the last
+// element of subtile s-1 (0 for s = 0), uniform.  One warp, no block barrier;
+// every prefix value is fetched by one lane, all in one round trip with the
+// weights.
+template <typename T, typename A, int UM>
+__device__ __forceinline__ void subtile_offspring(const DvArgs<A>& p, int64_t s, int32_t (&o)[kTileItems],
+                                                  int32_t& o_prev) {
+  const int lane = threadIdx.x & 31;
+  const int64_t e0 = s * kSub + (int64_t)lane * kTileItems;
+  const int64_t b = s >> 3;
+  const int q = (int)(s & 7);
+  const Hier<A> h = hier_of(p);
+  A v = A(0);
+  if (lane < 8) {
+    if (lane < q) v = __ldcg(p.sub + b * kSubPerTile + lane);
+  } else if (lane < 16) {
+    if (q == 0 && b > 0) v = __ldcg(p.sub + (b - 1) * kSubPerTile + (lane - 8));
+  } else if (lane == 16) {
+    v = __ldcg(h.group_prefix() + b / kGroupTiles);
+  } else if (lane == 17) {
+    v = __ldcg(h.excl + b);
+  } else if (lane == 18) {
+    if (b > 0) v = __ldcg(h.group_prefix() + (b - 1) / kGroupTiles);
+  } else if (lane == 19) {
+    if (b > 0) v = __ldcg(h.excl + b - 1);
+  } else if (lane == 20) {
+    v = h.total();
+  }
+  T x[kTileItems];
+  lane_weights<T, A, (UM & kULogW) != 0>(p, e0, x);
+  // uniform prefix arithmetic (every lane, identical)
+  const A te = add_rn(__shfl_sync(0xffffffffu, v, 16), __shfl_sync(0xffffffffu, v, 17));
+  A Q = A(0), Qm = A(0);
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    const A a = __shfl_sync(0xffffffffu, v, i);
+    if (i < q) {
+      Qm = Q;
+      Q = add_rn(Q, a);
+    }
+  }
+  const A SP = add_rn(te, Q);
+  A wprev;
+  if (q > 0) {
+    wprev = add_rn(add_rn(te, Qm), __shfl_sync(0xffffffffu, v, q - 1));
+  } else {
+    const A tep = add_rn(__shfl_sync(0xffffffffu, v, 18), __shfl_sync(0xffffffffu, v, 19));
+    A Qp = A(0);
+#pragma unroll
+    for (int i = 8; i < 15; ++i) Qp = add_rn(Qp, __shfl_sync(0xffffffffu, v, i));
+    wprev = add_rn(add_rn(tep, Qp), __shfl_sync(0xffffffffu, v, 15));
+  }
+  const A total = __shfl_sync(0xffffffffu, v, 20);
+  // the lane's serial partials and the Kogge-Stone exclusive offset; when the
+  // weights are narrower than the accumulator the partials are recomputed in
+  // the second loop (the same sequence) instead of being kept in registers
+  A tot = (A)x[0];
+#pragma unroll
+  for (int j = 1; j < kTileItems; ++j) tot = add_rn(tot, (A)x[j]);
+  const A incl = warp_inclusive_scan(tot);
+  A tex = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) tex = A(0);
+  const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
+  const double csys = 4503599627370496.0 + (double)fx.ufx;  // 2^52 + ufx (exact)
+  const int32_t nn = (int32_t)p.n;
+  A loc = A(0);
+  uint32_t unsafe = 0;
+#pragma unroll
+  for (int j = 0; j < kTileItems; ++j) {
+    loc = j ? add_rn(loc, (A)x[j]) : (A)x[0];
+    bool u;
+    o[j] = offspring_fast<T, A, UM>(add_rn(SP, add_rn(tex, loc)), fx, csys, nn, u, p);
+    unsafe |= (uint32_t)u << j;
+  }
+  if (__any_sync(0xffffffffu, unsafe)) {  // rare: the reference's exact IEEE sequence
+    loc = A(0);
+    for (int j = 0; j < kTileItems; ++j) {
+      loc = j ? add_rn(loc, (A)x[j]) : (A)x[0];
+      if ((unsafe >> j) & 1u) o[j] = offspring_exact<T, A, UM>(add_rn(SP, add_rn(tex, loc)), total, p.n, p);
+    }
+  }
+  if (e0 + kTileItems > p.n - 1) {  // the final subtile: O[N-1] = N, padding past N stays at N
+    const int64_t lim = p.n - 1 - e0;
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j)
+      if (j >= lim) o[j] = nn;
+  }
+  o_prev = s > 0 ? offspring_of<T, A, UM>(wprev, total, fx, p.n, p) : 0;
 }
 
 // ---------------------------------------------------------------------------
-// tile -> O (registers): shared by K2 and the repair path.  Index math is
-// 32-bit inside the tile (N < 2^31).
+// tile -> O (registers, blocked: thread t owns elements [16t, 16t+16)): shared
+// by K2 (cumulative offspring) and the repair path.  Warp w computes subtile
+// 8b + w.  Index math is 32-bit inside the tile (N < 2^31).
 template <typename T, typename A, int UM>
 __device__ __forceinline__ void tile_offspring(const DvArgs<A>& p, int64_t b, uint4* stage, A* warp_sums,
                                                int32_t (&o)[kTileItems], int32_t& o_prev) {
+  (void)stage;
+  (void)warp_sums;
   const int64_t base = b * kTile;
-  const int last = (p.n - 1 - base < kTile) ? (int)(p.n - 1 - base) : -1;
-  const int e0 = threadIdx.x * kTileItems;
-  A total;
   if (p.Wser) {
     // accum = SERIAL: the reference's own W (np.cumsum, serial fold) is given;
     // the offspring formula then runs in the weight dtype (A = T), exactly
     // as resamplers.py:139-153
+    const int last = (p.n - 1 - base < kTile) ? (int)(p.n - 1 - base) : -1;
+    const int e0 = threadIdx.x * kTileItems;
     A Wv[kTileItems];
     tile_load_any<A>(p.Wser, p.n, base, Wv);
-    total = __ldg(p.Wser + p.n - 1);
+    const A total = __ldg(p.Wser + p.n - 1);
     const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) o[j] = offspring_of<T, A, UM>(Wv[j], total, fx, p.n, p);
-  } else {
-    T x[kTileItems];
-    tile_weights<T, A, (UM & kULogW) != 0>(p, base, x);
-    TileScan<A> s;
+    if (last >= 0) {
 #pragma unroll
-    for (int j = 0; j < kTileItems; ++j) s.loc[j] = (A)x[j];
-    tile_scan<A>(s, warp_sums);
-    total = hier_of(p).total();
-    const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
-    const A ex = tile_excl(p, b);
-    const A tex = s.thread_excl;
-#pragma unroll
-    for (int j = 0; j < kTileItems; ++j) {
-      const A W = add_rn(ex, add_rn(tex, s.loc[j]));
-      o[j] = offspring_of<T, A, UM>(W, total, fx, p.n, p);
+      for (int j = 0; j < kTileItems; ++j)
+        if (e0 + j >= last) o[j] = (int32_t)p.n;
     }
+    o_prev = b > 0 ? offspring_of<T, A, UM>(__ldg(p.Wser + base - 1), total, fx, p.n, p) : 0;
+    return;
   }
-  if (last >= 0) {  // the final tile: O[N-1] = N, and padding past N stays at N
-#pragma unroll
-    for (int j = 0; j < kTileItems; ++j)
-      if (e0 + j >= last) o[j] = (int32_t)p.n;
-  }
-  o_prev = 0;
-  if (b > 0) {
-    const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
-    // W at the last position of tile b-1
-    const A Wp = p.Wser ? __ldg(p.Wser + base - 1) : add_rn(tile_excl(p, b - 1), __ldcg(p.agg + b - 1));
-    o_prev = offspring_of<T, A, UM>(Wp, total, fx, p.n, p);
-  }
+  __shared__ int32_t s_oprev;
+  int32_t op;
+  subtile_offspring<T, A, UM>(p, b * kSubPerTile + (threadIdx.x >> 5), o, op);
+  if (threadIdx.x == 0) s_oprev = op;
+  __syncthreads();
+  o_prev = s_oprev;
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -358,6 +517,308 @@ __global__ void __launch_bounds__(kIpThreads, kMinBlocks) k_dv_inplace(const uin
   if (max_steps) {
     longest = __reduce_max_sync(0xffffffffu, longest);
     if (lane == 0 && longest) atomicMax(max_steps, longest);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2w / K3w: the systematic / stratified delivery's production and
+// resolution as two warp-level kernels.  The unit of work is a 512-element
+// SUBTILE owned by one warp (16 consecutive elements per lane): no block
+// barrier anywhere, so every warp of the SM hides the others' latency.
+constexpr int kFWarps = 8;      // warps per CTA
+constexpr int kWBuf = 1024;     // per-warp staging of slot positions (4 KB)
+
+struct __align__(16) WarpSmem {
+  uint32_t buf[kWBuf];
+};
+
+// Words (parent | FIRST) for the subtile's slot range [o_prev, oend) and its
+// has-offspring bitmap, by one warp.  Per 512-slot chunk (16-byte aligned):
+// every parent with offspring writes its index at its first slot O[j-1] (a
+// plain scattered store: first slots are distinct), all other positions hold
+// -1; then a max-scan over the slot positions (lane l owns 16 consecutive
+// ones; Kogge-Stone over the lane maxima; a carry across chunks) gives every
+// slot its parent, since parents increase with the slot.  No loops over
+// offspring counts, no atomics, 16-byte coalesced stores.  Positions are
+// XOR-swizzled in 16-byte units so the per-lane vector accesses are
+// bank-conflict free.
+__device__ __forceinline__ int sw_hd(int v) { return v ^ ((v >> 3) & 3); }  // 16-byte unit swizzle
+__device__ __forceinline__ void subtile_expand(const int32_t (&o)[kTileItems], int32_t prev_l, int32_t o_prev,
+                                               int32_t oend, int64_t s, int64_t n, uint32_t* __restrict__ words,
+                                               uint32_t* __restrict__ bitmap, WarpSmem& W) {
+  const int lane = threadIdx.x & 31;
+  const int64_t base = s * kSub;
+  const int64_t e0 = base + (int64_t)lane * kTileItems;
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < kTileItems; ++j) {
+    const int pv = j ? o[j - 1] : prev_l;
+    if (o[j] > pv) bits |= 1u << j;  // padding past N repeats O = N: never a parent
+  }
+  const uint32_t hi = __shfl_down_sync(0xffffffffu, bits, 1);
+  if ((lane & 1) == 0 && e0 < n) bitmap[(base >> 5) + (lane >> 1)] = bits | (hi << 16);
+  if (oend <= o_prev) return;  // uniform: no slots
+  int32_t* hb = reinterpret_cast<int32_t*>(W.buf);
+  int4* hb4 = reinterpret_cast<int4*>(W.buf);
+  const int pb = (int)e0;  // global index of the lane's first parent
+  int carry = -1;
+  // chunks of kWBuf = 1024 positions (a typical subtile's ~512 slots fit one
+  // chunk whatever their alignment), scanned as up to two rows of 512
+  for (int c0 = o_prev & ~3; c0 < oend; c0 += kWBuf) {
+    const int rows = oend - c0 > kSub ? 2 : 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) hb4[sw_hd(4 * lane + q)] = make_int4(-1, -1, -1, -1);
+    if (rows == 2) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) hb4[sw_hd(128 + 4 * lane + q)] = make_int4(-1, -1, -1, -1);
+    }
+    __syncwarp();
+    {
+      int r = prev_l - c0;  // first slot of parent j = O[j-1], relative
+#pragma unroll
+      for (int j = 0; j < kTileItems; ++j) {
+        if (((bits >> j) & 1u) && (unsigned)r < (unsigned)kWBuf) hb[(sw_hd(r >> 2) << 2) | (r & 3)] = pb + j;
+        r = o[j] - c0;
+      }
+    }
+    __syncwarp();
+    for (int row = 0; row < rows; ++row) {
+      int4 hv[4];
+      int mx = -1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        hv[q] = hb4[sw_hd(128 * row + 4 * lane + q)];
+        mx = max(mx, max(max(hv[q].x, hv[q].y), max(hv[q].z, hv[q].w)));
+      }
+      int incl = mx;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl = max(incl, t);
+      }
+      int cur = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (lane == 0) cur = -1;
+      cur = max(cur, carry);
+      carry = max(carry, __shfl_sync(0xffffffffu, incl, 31));
+      uint32_t wv[kTileItems];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e[4] = {hv[q].x, hv[q].y, hv[q].z, hv[q].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          cur = max(cur, e[t]);
+          wv[4 * q + t] = (uint32_t)cur | (e[t] >= 0 ? kFirst : 0u);
+        }
+      }
+      const int s0 = c0 + kSub * row + lane * kTileItems;
+      if (s0 >= o_prev && s0 + kTileItems <= oend) {
+        uint4* dst = reinterpret_cast<uint4*>(words + s0);
+#pragma unroll
+        for (int q = 0; q < kTileItems / 4; ++q)
+          dst[q] = make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
+      } else if (s0 < oend && s0 + kTileItems > o_prev) {
+        for (int t = 0; t < kTileItems; ++t)
+          if (s0 + t >= o_prev && s0 + t < oend) words[s0 + t] = wv[t];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// K2w: produce every subtile (grid-stride): O from the position formula,
+// the slot words of the subtile's slot range and its has-offspring bitmap.
+template <typename T, typename A, int UM>
+__global__ void __launch_bounds__(kFWarps * 32, 3) k_dv_produce(DvArgs<A> p) {
+  extern __shared__ __align__(16) unsigned char fused_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpSmem& W = reinterpret_cast<WarpSmem*>(fused_smem)[warp];
+  griddep_wait();
+  const int64_t n = p.n;
+  const int64_t nS = (n + kSub - 1) / kSub;
+  for (int64_t k = blockIdx.x * (int64_t)kFWarps + warp; k < nS; k += (int64_t)gridDim.x * kFWarps) {
+    int32_t o[kTileItems];
+    int32_t o_prev;
+    subtile_offspring<T, A, UM>(p, k, o, o_prev);
+    int32_t prev_l = __shfl_up_sync(0xffffffffu, o[kTileItems - 1], 1);
+    if (lane == 0) prev_l = o_prev;
+    const bool bad = __any_sync(0xffffffffu, o[0] < prev_l);
+    const int32_t oend = __shfl_sync(0xffffffffu, o[kTileItems - 1], 31);
+    if (!bad)
+      subtile_expand(o, prev_l, o_prev, oend, k, n, p.words, p.bitmap, W);
+    else if (lane == 0)
+      atomicOr(&p.state->flags, kNeedsRepair);
+  }
+}
+
+// K3w's chain queue: one per warp, in shared memory.
+constexpr int kRQ = 1024;     // entries (>= kRThresh + the 512 chains one subtile can add)
+constexpr int kRThresh = 384; // a pass runs once this many chains wait (~1 pass per subtile)
+struct ResolveQ {
+  uint2 xz[kRQ];  // (hole, next slot)
+  uint8_t st[kRQ];
+};
+
+// One step for every queued chain when every word is written: dense, eight
+// loads per lane in flight, survivors compacted to the front.
+__device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const uint32_t* __restrict__ words,
+                                         int32_t* __restrict__ c, uint32_t n, int& longest, bool& overflow) {
+  constexpr int K = 8;
+  int out = 0;
+  for (int b = 0; b < qlen; b += 32 * K) {
+    uint2 xz[K];
+    uint32_t w[K];
+    int st[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int e = b + 32 * i + lane;
+      if (e < qlen) {
+        xz[i] = Q.xz[e];
+        st[i] = Q.st[e] + 1;
+        w[i] = __ldcg(words + xz[i].y);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (b + 32 * i >= qlen) break;  // warp-uniform
+      const bool valid = b + 32 * i + lane < qlen;
+      bool keep = false;
+      if (valid) {
+        const uint32_t par = w[i] & kParentMask;
+        if (!(w[i] & kFirst)) {
+          c[xz[i].x] = (int32_t)par;
+          longest = max(longest, st[i]);
+        } else if (st[i] >= kBackBound || par >= n) {
+          overflow = true;  // abandoned: the rare-path kernel resolves every chain
+        } else {
+          keep = true;
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int pos = out + __popc(m & ((1u << lane) - 1));
+        Q.xz[pos] = make_uint2(xz[i].x, w[i] & kParentMask);
+        Q.st[pos] = (uint8_t)st[i];
+      }
+      out += __popc(m);
+    }
+    __syncwarp();
+  }
+  return out;
+}
+
+// K3w: resolve every subtile.  Lane l takes indices 128q + 4l + {0..3} of
+// the subtile (q = 0..3): 16-byte coalesced loads of the words (prefetched
+// one subtile ahead) and stores of c, the has-offspring bits from 4 bitmap
+// words.  Trivial indices are final at once; first-slot holes join the
+// warp's chain queue, which advances one step for every queued chain per
+// pass, a pass running once enough chains wait -- so a pass costs one L2
+// round trip for several subtiles' chains, overlapped with the next
+// subtile's prefetched loads.
+template <typename T, typename A, int UM>
+__global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
+  extern __shared__ __align__(16) unsigned char fused_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ResolveQ& Q = reinterpret_cast<ResolveQ*>(fused_smem)[warp];
+  griddep_wait();
+  if (p.state->flags & kNeedsRepair) return;
+  const int64_t n = p.n;
+  const uint32_t nn = (uint32_t)n;
+  const int64_t nS = (n + kSub - 1) / kSub;
+  int qlen = 0, longest = 0;
+  bool overflow = false;
+  auto pass = [&]() { return lean_pass(Q, lane, qlen, p.words, p.c, nn, longest, overflow); };
+  const uint4* __restrict__ words4 = reinterpret_cast<const uint4*>(p.words);
+  int4* __restrict__ c4 = reinterpret_cast<int4*>(p.c);
+  const int64_t stride = (int64_t)gridDim.x * kFWarps;
+  auto load = [&](int64_t rr, uint4 (&wv)[4], uint32_t (&bm)[4]) {
+    const uint32_t xb = (uint32_t)rr * kSub;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t x0 = xb + 128 * q + 4 * lane;
+      if (xb + kSub <= nn) {
+        wv[q] = __ldg(words4 + (x0 >> 2));
+      } else {
+        wv[q].x = x0 < nn ? __ldg(p.words + x0) : 0u;
+        wv[q].y = x0 + 1 < nn ? __ldg(p.words + x0 + 1) : 0u;
+        wv[q].z = x0 + 2 < nn ? __ldg(p.words + x0 + 2) : 0u;
+        wv[q].w = x0 + 3 < nn ? __ldg(p.words + x0 + 3) : 0u;
+      }
+      bm[q] = x0 < nn ? __ldg(p.bitmap + (x0 >> 5)) >> (x0 & 31) : 0u;
+    }
+  };
+  int64_t rr = blockIdx.x * (int64_t)kFWarps + warp;
+  uint4 nwv[4];
+  uint32_t nbm[4];
+  if (rr < nS) load(rr, nwv, nbm);
+  for (; rr < nS; rr += stride) {
+    const uint32_t xb = (uint32_t)rr * kSub;
+    const bool full = xb + kSub <= nn;
+    uint4 wv[4];
+    uint32_t bm[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      wv[q] = nwv[q];
+      bm[q] = nbm[q];
+    }
+    if (rr + stride < nS) load(rr + stride, nwv, nbm);  // prefetch the next subtile
+    uint32_t pend = 0;  // bit 4q + t
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t x0 = xb + 128 * q + 4 * lane;
+      const uint32_t e[4] = {wv[q].x, wv[q].y, wv[q].z, wv[q].w};
+      int32_t o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const bool has = (bm[q] >> t) & 1u;
+        o[t] = has ? (int32_t)(x0 + t) : (int32_t)(e[t] & kParentMask);
+        if (!has && (e[t] & kFirst) && x0 + t < nn) pend |= 1u << (4 * q + t);
+      }
+      // pending holes get a placeholder, overwritten when their chain
+      // resolves (__syncwarp orders the two stores)
+      if (full) {
+        __stcs(c4 + (x0 >> 2), make_int4(o[0], o[1], o[2], o[3]));
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (x0 + t < nn) p.c[x0 + t] = o[t];
+      }
+    }
+    const int cnt = __popc(pend);
+    int off = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= cnt;
+    while (qlen + total > kRQ) qlen = pass();
+    int pos = qlen + off;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t e[4] = {wv[q].x, wv[q].y, wv[q].z, wv[q].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if ((pend >> (4 * q + t)) & 1u) {
+          Q.xz[pos] = make_uint2(xb + 128 * q + 4 * lane + t, e[t] & kParentMask);
+          Q.st[pos] = 0;
+          ++pos;
+        }
+      }
+    }
+    qlen += total;
+    __syncwarp();
+    if (qlen >= kRThresh) qlen = pass();
+  }
+  while (qlen) qlen = pass();
+  if (overflow) {
+    atomicOr(&p.state->flags, kOverflow);
+    status_or(p.status, PFR_ST_OVERFLOW);
+  }
+  if (p.max_steps) {
+    longest = __reduce_max_sync(0xffffffffu, longest);
+    if (lane == 0 && longest) atomicMax(p.max_steps, longest);
   }
 }
 
@@ -560,6 +1021,34 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
     e = cudaGetLastError();
   }
   if (e != cudaSuccess || stages < 2) return e;
+  // PFR_DV_PIPELINE=legacy (A/B aid): the CTA-tile pipeline K2 + K3
+  static const bool legacy = [] {
+    const char* v = getenv("PFR_DV_PIPELINE");
+    return v && v[0] == 'l';
+  }();
+  if (p.expand && !p.Wser && !legacy) {
+    const int smem = (int)(sizeof(WarpSmem) * kFWarps);
+    const int smem3 = (int)(sizeof(ResolveQ) * kFWarps);
+    static int occ2 = -1, occ3 = -1;
+    if (occ2 < 0) {
+      e = cudaFuncSetAttribute(k_dv_produce<T, A, UM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(k_dv_resolve<T, A, UM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+      if (e != cudaSuccess) return e;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_dv_produce<T, A, UM>, kFWarps * 32, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_dv_resolve<T, A, UM>, kFWarps * 32, smem3);
+      occ2 = max(occ2, 1);
+      occ3 = max(occ3, 1);
+    }
+    const int64_t subs = (p.n + kSub - 1) / kSub;
+    const int64_t g2 = max((int64_t)1, min((int64_t)num_sms() * occ2, (subs + kFWarps - 1) / kFWarps));
+    const int64_t g3 = max((int64_t)1, min((int64_t)num_sms() * occ3, (subs + kFWarps - 1) / kFWarps));
+    e = launch_pdl_smem(k_dv_produce<T, A, UM>, dim3((unsigned)g2), dim3(kFWarps * 32), (size_t)smem, s, false, p);
+    if (e != cudaSuccess || stages < 3) return e;
+    e = launch_pdl_smem(k_dv_resolve<T, A, UM>, dim3((unsigned)g3), dim3(kFWarps * 32), (size_t)smem3, s, false, p);
+    if (e != cudaSuccess || stages < 4) return e;
+    return launch_pdl(k_dv_rare<T, A, UM>, dim3(num_sms()), dim3(kTileThreads), s, true, p);
+  }
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
   if (e != cudaSuccess || stages < 3) return e;
   if (p.expand) {
@@ -637,6 +1126,7 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
   p.J1 = ws.j1;
   p.R0 = ws.r0;
   p.R1 = ws.r1;
+  p.sub = reinterpret_cast<A*>(ws.sub_cells);
   return p;
 }
 

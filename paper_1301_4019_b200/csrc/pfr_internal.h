@@ -34,6 +34,7 @@ struct Workspace {
   WsHeader* hdr;
   uint64_t* sum_cells;  // lookback sum tree
   uint64_t* max_cells;  // lookback max tree
+  uint64_t* sub_cells;  // [8 * tiles] subtile aggregates (fused delivery)
   int64_t tiles;
   int32_t* O;  // cumulative offspring scratch
   int32_t* d;  // claims
