@@ -466,7 +466,10 @@ def main():
     dev_w = [torch.empty_like(weights[dt]) for (_, _, _, dt) in jobs]
     dev_c = [torch.empty(n, dtype=torch.int32, device=dev) for _ in jobs]
     copy_stream = torch.cuda.Stream(device=dev)  # uploads
-    down_stream = torch.cuda.Stream(device=dev)  # downloads (the other copy direction)
+    down_stream = torch.cuda.Stream(device=dev)  # joins the downloads (the other copy direction)
+    # one download stream per delivery: a result leaves as soon as its
+    # delivery is done instead of queueing behind a longer one
+    down_streams = [torch.cuda.Stream(device=dev) for _ in jobs]
     h2d = sum(host_w[dt].numel() * host_w[dt].element_size() for (_, _, _, dt) in jobs)
     d2h = len(jobs) * n * 4
     e2e_ms = 0.0
@@ -498,11 +501,14 @@ def main():
                 c = run_delivery(alg, dt, dev_w[k], pf.RngStream(50_000 + s, (rank, i, j)), dev_c[k])
                 done = torch.cuda.Event()
                 done.record(sk)
-            c.record_stream(down_stream)
-            with torch.cuda.stream(down_stream):
-                down_stream.wait_event(done)
+            dk = down_streams[k]
+            c.record_stream(dk)
+            dk.wait_event(done)
+            with torch.cuda.stream(dk):
                 host_c[k].copy_(c, non_blocking=True)
         down_stream.wait_stream(copy_stream)
+        for dk in down_streams:
+            down_stream.wait_stream(dk)
         e1.record(down_stream)
         torch.cuda.synchronize()
         if os.environ.get("PFR_BENCH_DEBUG"):
@@ -599,9 +605,10 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "particles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms / args.steps, "link_only_ms": link_only_ms,
-                    "note": "pinned host buffers; uploads (longest delivery first) and downloads on two copy "
-                            "streams pipelined with the ten deliveries (each on its own stream); link_only_ms = "
-                            "the same copies with no compute (the host-link floor)"},
+                    "note": "pinned host buffers; uploads (longest delivery first) on one copy stream, each "
+                            "result downloaded on its own stream as soon as its delivery is done, pipelined with "
+                            "the ten deliveries (each on its own stream); link_only_ms = the same copies with no "
+                            "compute (the host-link floor)"},
             "gpu_launches": launches,
             "clocks": clocks,
             "per_delivery_ms": {k: sum(v) / len(v) for k, v in per_delivery.items()},

@@ -476,7 +476,8 @@ def permute(a, with_steps: bool = False):
             if hops > n:
                 raise RuntimeError("permutation chain walk failed to terminate")
         dl[x] = i
-        longest = max(longest, hops)
+        if hops > longest:
+            longest = hops
     c = a[np.asarray(dl, dtype=np.int64)]
     return (c, longest) if with_steps else c
 

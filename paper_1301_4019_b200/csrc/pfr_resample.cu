@@ -100,9 +100,9 @@ __global__ void __launch_bounds__(256) k_metropolis_philox(const T* __restrict__
         j[c][h] = threshold == 0 ? __umulhi(o[2 * h], nn)  // power-of-two N: Lemire never rejects
                                  : bounded_u32(o[2 * h], nn, threshold, i, (uint32_t)(b + h), kTagMetropolis, k0, k1);
         if constexpr (sizeof(T) == 4)
-          u[c][h] = u32_to_unit_f(o[2 * h + 1]);
+          u[c][h] = u32_to_unit_f_open(o[2 * h + 1]);
         else
-          u[c][h] = u32_to_unit_d(o[2 * h + 1]);
+          u[c][h] = u32_to_unit_d_open(o[2 * h + 1]);
       }
     }
     // issue every gather of this step pair before consuming any (MLP)
@@ -227,6 +227,7 @@ struct RejArgs {
   T* out_w;
   unsigned long long* next_chunk;
   uint32_t* status;
+  int pack_k;  // log2 N for the packed 3-trips-per-call draws (N = 2^k, k <= 21), else -1
 };
 
 constexpr int kRejChunk = 256;
@@ -261,9 +262,48 @@ __device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, ui
                                         : bounded_u32(o[2 * h], nn, A.threshold, slot, trip + 2 * q + h,
                                                       kTagRejection, A.k0, A.k1);
       if constexpr (sizeof(T) == 4)
-        d.u[2 * q + h] = u32_to_unit_f(o[2 * h + 1]);
+        d.u[2 * q + h] = u32_to_unit_f_open(o[2 * h + 1]);
       else
-        d.u[2 * q + h] = u32_to_unit_d(o[2 * h + 1]);
+        d.u[2 * q + h] = u32_to_unit_d_open(o[2 * h + 1]);
+    }
+  }
+  if (trip == 0) d.j[0] = slot;
+}
+
+// Packed draws (power-of-two N = 2^k, k <= 21): THREE trips per
+// Philox4x32-10 call instead of two.  The 128 output bits are cut into three
+// 42-bit fields; trip t of `slot` uses call (slot, t/3) and field t%3: the low
+// k bits are the proposal (exact: N is a power of two), the remaining 42-k >=
+// 21 bits the uniform, taken at the midpoint of its cell, (bits + 1/2) *
+// 2^-(42-k), so it is never 0 (a zero weight can never be accepted) and its
+// quantisation moves an acceptance probability by at most 2^-(43-k) <= 2^-22
+// (float32: the top 22 bits).  Philox is ~46% of the rejection kernel's
+// instructions, so a third fewer calls per trip -- yet measured slower on
+// B200 (launcher), so opt-in only.
+template <typename T, int B>
+__device__ __forceinline__ void rej_draws3(const RejArgs<T>& A, uint32_t slot, uint32_t trip, int k,
+                                           RejBatch<T, B>& d) {
+  static_assert(B % 3 == 0, "packed batches hold whole Philox calls");
+  const uint32_t nmask = (uint32_t)A.n - 1u;
+  const int m = 42 - k;  // uniform bits
+#pragma unroll
+  for (int q = 0; q < B / 3; ++q) {
+    uint32_t o[4];
+    philox4x32_10(slot, trip / 3 + q, kTagRejection, 0, A.k0, A.k1, o);
+    const uint64_t f[3] = {((uint64_t)o[1] << 32 | o[0]) & 0x3FFFFFFFFFFull,
+                           (((uint64_t)o[2] << 32 | o[1]) >> 10) & 0x3FFFFFFFFFFull,
+                           (((uint64_t)o[3] << 32 | o[2]) >> 20) & 0x3FFFFFFFFFFull};
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      d.j[3 * q + h] = (uint32_t)f[h] & nmask;
+      const uint64_t ub = f[h] >> k;  // m bits
+      if constexpr (sizeof(T) == 4) {
+        // top 22 bits, then the midpoint bit: 23 mantissa bits
+        const uint32_t t22 = m >= 22 ? (uint32_t)(ub >> (m - 22)) : (uint32_t)(ub << (22 - m));
+        d.u[3 * q + h] = __uint_as_float(0x3F800000u | (t22 << 1) | 1u) - 1.0f;
+      } else {
+        d.u[3 * q + h] = __longlong_as_double((long long)(0x3FF0000000000000ull | ((2 * ub + 1) << (51 - m)))) - 1.0;
+      }
     }
   }
   if (trip == 0) d.j[0] = slot;
@@ -272,8 +312,14 @@ __device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, ui
 // Software pipelined: the gathers of batch k are issued, then the draws of
 // batch k+1 are computed while they are in flight, then batch k is resolved.
 // A lane whose slot finishes discards its precomputed batch (one per slot).
-template <typename T, bool kCapped, int kRejBatch, int kMinBlocks = 1>
+template <typename T, bool kCapped, int kRejBatch, int kMinBlocks = 1, bool kPack = false>
 __global__ void __launch_bounds__(256, kMinBlocks) k_rejection_philox(RejArgs<T> A) {
+  auto draws = [&](uint32_t slot, uint32_t trip, RejBatch<T, kRejBatch>& d) {
+    if constexpr (kPack)
+      rej_draws3<T, kRejBatch>(A, slot, trip, A.pack_k, d);
+    else
+      rej_draws<T, kRejBatch>(A, slot, trip, d);
+  };
   const int lane = threadIdx.x & 31;
   const T bound = (T)A.bound;
   const T capv = (T)A.cap;
@@ -305,7 +351,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_rejection_philox(RejArgs<T>
       if (slot < 0 && rank < take) {
         slot = chunk_next + rank;
         trip = 0;
-        rej_draws<T, kRejBatch>(A, (uint32_t)(A.s0 + slot), 0u, cur);
+        draws((uint32_t)(A.s0 + slot), 0u, cur);
       }
       chunk_next += take;
       idle = __ballot_sync(0xffffffffu, slot < 0);
@@ -317,7 +363,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_rejection_philox(RejArgs<T>
       for (int q = 0; q < kRejBatch; ++q) wj[q] = ldg(A.w + cur.j[q]);
       // next batch's draws overlap the gathers' latency
       RejBatch<T, kRejBatch> nxt;
-      rej_draws<T, kRejBatch>(A, (uint32_t)(A.s0 + slot), trip + kRejBatch, nxt);
+      draws((uint32_t)(A.s0 + slot), trip + kRejBatch, nxt);
       int done = -1;  // batch position of the first accepting trip
 #pragma unroll
       for (int q = kRejBatch - 1; q >= 0; --q) {
@@ -620,28 +666,47 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
     return v ? atoi(v) : 0;
   }();
   // measured on B200 (N=2^20, sigma=1, sup = max w): float32 8 trips/lane
-  // (482 us), float64 4 trips/lane (510 us); more CTAs per SM lose
-  const int b_f32 = batch ? batch : 8, b_f64 = batch ? batch : 4;
-#define PFR_REJ_LAUNCH(T, CAP, B, MB) \
-  k_rejection_philox<T, CAP, B, MB><<<blocks_for(k_rejection_philox<T, CAP, B, MB>), 256, 0, s>>>(A)
-#define PFR_REJ_DISPATCH(T, CAP)            \
-  do {                                      \
-    switch (sizeof(T) == 4 ? b_f32 : b_f64) { \
-      case 2: PFR_REJ_LAUNCH(T, CAP, 2, 1); break;   \
-      case 4: PFR_REJ_LAUNCH(T, CAP, 4, 1); break;   \
-      default: PFR_REJ_LAUNCH(T, CAP, 8, 1); break;  \
-    }                                       \
+  // (475 us), float64 4 trips/lane (483 us); more CTAs per SM lose.  The
+  // packed draws (3 trips per Philox call, PFR_REJ_PACK=1, batches 9 / 6)
+  // measured SLOWER (511 / 532 us; batches 6 and 12 no better): the 64-bit
+  // field extraction costs more issue slots than the saved Philox rounds, so
+  // they stay off by default.
+  static const bool pack_on = [] {
+    const char* v = getenv("PFR_REJ_PACK");
+    return v && v[0] == '1';
+  }();
+  const int l2n = log2_exact(n);
+  const int pack_k = (pack_on && l2n >= 1 && l2n <= 21) ? l2n : -1;
+  const int b_f32 = batch ? batch : (pack_k >= 0 ? 9 : 8), b_f64 = batch ? batch : (pack_k >= 0 ? 6 : 4);
+#define PFR_REJ_LAUNCH(T, CAP, B, MB, PK) \
+  k_rejection_philox<T, CAP, B, MB, PK><<<blocks_for(k_rejection_philox<T, CAP, B, MB, PK>), 256, 0, s>>>(A)
+#define PFR_REJ_DISPATCH(T, CAP)                                   \
+  do {                                                             \
+    if (pack_k >= 0) {                                             \
+      switch (sizeof(T) == 4 ? b_f32 : b_f64) {                    \
+        case 3: PFR_REJ_LAUNCH(T, CAP, 3, 1, true); break;          \
+        case 6: PFR_REJ_LAUNCH(T, CAP, 6, 1, true); break;          \
+        case 12: PFR_REJ_LAUNCH(T, CAP, 12, 1, true); break;        \
+        default: PFR_REJ_LAUNCH(T, CAP, 9, 1, true); break;         \
+      }                                                            \
+    } else {                                                       \
+      switch (sizeof(T) == 4 ? b_f32 : b_f64) {                    \
+        case 2: PFR_REJ_LAUNCH(T, CAP, 2, 1, false); break;         \
+        case 4: PFR_REJ_LAUNCH(T, CAP, 4, 1, false); break;         \
+        default: PFR_REJ_LAUNCH(T, CAP, 8, 1, false); break;        \
+      }                                                            \
+    }                                                              \
   } while (0)
   if (dtype == PFR_F64) {
     RejArgs<double> A{(const double*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
-                      s_begin, s_count, a, trips, (double*)out_w, next, status};
+                      s_begin, s_count, a, trips, (double*)out_w, next, status, pack_k};
     if (cap > 0)
       PFR_REJ_DISPATCH(double, true);
     else
       PFR_REJ_DISPATCH(double, false);
   } else {
     RejArgs<float> A{(const float*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
-                     s_begin, s_count, a, trips, (float*)out_w, next, status};
+                     s_begin, s_count, a, trips, (float*)out_w, next, status, pack_k};
     if (cap > 0)
       PFR_REJ_DISPATCH(float, true);
     else

@@ -123,6 +123,16 @@ __host__ __device__ __forceinline__ double u32_to_unit_d(uint32_t x) {
 #endif
 }
 
+// open-interval variants (0, 1) for the own-stream acceptance tests: the
+// midpoint of the cell, so u is never 0 and a zero weight can never be
+// accepted (u * w[k] <= w[j] = 0 would hold at u = 0)
+__host__ __device__ __forceinline__ float u32_to_unit_f_open(uint32_t x) {
+  return (float)(((x >> 9) << 1) | 1u) * (1.0f / 16777216.0f);  // (2m + 1) 2^-24, m < 2^23
+}
+__host__ __device__ __forceinline__ double u32_to_unit_d_open(uint32_t x) {
+  return u32_to_unit_d(x) + 1.1641532182693481e-10;  // (2x + 1) 2^-33, exact
+}
+
 // Lemire bounded integer in [0, n): exact (rejection on the biased sliver;
 // a rejected draw is replaced from a dedicated redraw counter so the result
 // stays a pure function of the counter).  threshold = 2^32 mod n.
