@@ -272,6 +272,25 @@ int pfr_rejection_range(const void* w, int64_t n, int dtype, double bound, doubl
                         int64_t max_rounds, int64_t slot_begin, int64_t slot_count, int32_t* a, int32_t* trips,
                         void* out_w, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
 
+/* multinomial_ancestors (resamplers.py:56-74) for slots [slot_begin,
+ * slot_begin + slot_count) of the N-slot resampler over the full weight
+ * vector w[n]: a is indexed slot - slot_begin.  Own stream: the sorted
+ * uniforms of those slots from the (replicated) spacing scan, merged with W
+ * along their merge-path diagonals only; numpy stream / caller uniforms: the
+ * slots' own draws.  The union over ranks equals pfr_multinomial (SURVEY
+ * 8(e): the weight-sharded multinomial partitions the output slots). */
+int pfr_multinomial_range(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng, const double* uniforms,
+                          int64_t slot_begin, int64_t slot_count, int32_t* a, uint32_t* status, void* ws,
+                          size_t ws_bytes, void* stream);
+
+/* A rank's share of permute_parallel (ancestry.py:139-174): c[x - index_begin]
+ * for x in [index_begin, index_begin + index_count), from the full ancestry
+ * a[n] (claims over all of a, then backward loser walks for the range's
+ * holes only).  The union over ranks equals pfr_permute; a chain longer than
+ * 4096 hops sets PFR_ST_OVERFLOW (fall back to pfr_permute). */
+int pfr_permute_range(const int32_t* a, int64_t n, int64_t index_begin, int64_t index_count, int32_t* c,
+                      int32_t* max_steps, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
 /* Cumulative offspring of this shard's parents in global slot numbers
  * (_offspring_from_positions, resamplers.py:139-153): W = prefix + W_loc[i]
  * (W_loc = the shard's inclusive scan in float64), r = (W*N)/total,
@@ -279,6 +298,31 @@ int pfr_rejection_range(const void* w, int64_t n, int dtype, double bound, doubl
 int pfr_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double prefix, double total, int64_t n_global,
                         int last_global, int stratified, double offset, const double* uniforms, const pfr_rng* rng,
                         int32_t* O, void* stream);
+
+/* Protocol v2 of the weight-sharded systematic / stratified delivery (no
+ * host round trip before the final status exchange; sharded.py):
+ * pfr_shard_offspring_dev is pfr_shard_offspring with prefix_total = {weight
+ * before the shard, W_N} read on the device, and o_before = the O of the
+ * element before the shard (the previous shard's last O; 0 for the first). */
+int pfr_shard_offspring_dev(const double* W_loc, int64_t n_loc, int dtype, const double* prefix_total,
+                            int64_t n_global, int last_global, int first_global, int stratified, double offset,
+                            const double* uniforms, const pfr_rng* rng, int32_t* O, int32_t* o_before, void* stream);
+/* The shard's slot words (parent | FIRST) written into the EXTENDED array
+ * ext[n_loc + 2*halo] covering slots [index_base - halo, index_base + n_loc +
+ * halo) (sentinel 0xFFFFFFFF elsewhere), and has[i] = o_i > 0.  A slot of the
+ * window outside that range sets PFR_ST_OVERFLOW. */
+int pfr_shard_ext_words(const int32_t* O_loc, int64_t n_loc, int64_t index_base, const int32_t* o_before, int64_t halo,
+                        uint32_t* ext, uint8_t* has, uint32_t* status, void* stream);
+/* Fill ext's sentinels from the neighbours' boundary bands: bands[world][4*halo]
+ * holds every rank's ext[0, 2*halo) followed by its ext[n, n + 2*halo). */
+int pfr_shard_merge_bands(uint32_t* ext, int64_t n_loc, int64_t halo, const uint32_t* bands, int rank, int world,
+                          uint32_t* status, void* stream);
+/* The in-place ancestry of the shard's indices (ancestry.py:139-174 read
+ * backwards from each hole) with every chain inside ext; a missing word or a
+ * chain leaving ext sets PFR_ST_OVERFLOW (the caller reruns the general
+ * protocol). */
+int pfr_shard_resolve_ext(const uint32_t* ext, int64_t n_loc, int64_t halo, const uint8_t* has, int64_t index_base,
+                          int32_t* c, int32_t* max_steps, uint32_t* status, void* stream);
 
 /* Slot words of the shard's slot window [o_begin, O[n_loc-1]):
  * words[s - o_begin] = parent | 0x80000000 on a parent's first slot

@@ -528,6 +528,63 @@ cudaError_t launch_claims_reset(int64_t n, int32_t* max_steps, const Workspace& 
   return cudaMemsetAsync(ws.d, 0x7F, (size_t)n * sizeof(int32_t), s);
 }
 
+// ---------------------------------------------------------------------------
+// Partitioned permute (a rank's share of permute_parallel, ancestry.py:139-174,
+// over the all-gathered ancestry): c[x] for the indices x of [c_begin,
+// c_begin + c_count) only.  With the claims d (prepermute over the FULL a),
+// x with offspring keeps c[x] = x; a hole x walks the loser chain BACKWARDS:
+// slot z is the first claim of its parent exactly when d[a[z]] == z, and then
+// the chain came from a[z]; the first z that is not a first claim is the
+// loser, and c[x] = a[z] (the chain's length in hops is the reference's
+// steps).  Order free, so the union over ranks is the single-GPU result.  A
+// chain longer than kRangeBound sets PFR_ST_OVERFLOW (the caller falls back
+// to the full permute).
+constexpr int kRangeBound = 4096;
+__global__ void k_permute_range(const int32_t* __restrict__ a, int64_t n, const int32_t* __restrict__ d,
+                                int64_t c_begin, int64_t c_count, int32_t* __restrict__ c, int32_t* max_steps,
+                                uint32_t* status) {
+  int longest = 0;
+  uint32_t f = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < c_count; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = c_begin + t;
+    if (__ldg(d + x) < n) {
+      c[t] = (int32_t)x;
+      continue;
+    }
+    int64_t z = x;
+    int hops = 0;
+    int32_t p = __ldg(a + z);
+    while (__ldg(d + p) == z) {
+      z = p;
+      p = __ldg(a + z);
+      if (++hops > kRangeBound) {
+        f |= PFR_ST_OVERFLOW;
+        break;
+      }
+    }
+    c[t] = p;
+    longest = max(longest, hops);
+  }
+  status_or_warp(status, f);
+  if (max_steps) {
+    longest = __reduce_max_sync(__activemask(), longest);
+    if ((threadIdx.x & 31) == 0 && longest) atomicMax(max_steps, longest);
+  }
+}
+
+cudaError_t launch_permute_range(const int32_t* a, int64_t n, int64_t c_begin, int64_t c_count, int32_t* c,
+                                 int32_t* max_steps, uint32_t* status, const Workspace& ws, cudaStream_t s) {
+  cudaError_t e = launch_claims_reset(n, max_steps, ws, s);
+  if (e != cudaSuccess) return e;
+  k_claim<int32_t><<<grid_for(n, 256), 256, 0, s>>>(a, n, ws.d, nullptr, status);
+  note_launch();
+  if (c_count > 0) {
+    k_permute_range<<<grid_for(c_count, 256), 256, 0, s>>>(a, n, ws.d, c_begin, c_count, c, max_steps, status);
+    note_launch();
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_walk(const int32_t* a, int64_t n, int32_t* c, int32_t* max_steps, uint32_t* status,
                         const Workspace& ws, cudaStream_t s) {
   const int gw = grid_for((n + 3) / 4, 256);

@@ -360,6 +360,33 @@ int pfr_rejection_range(const void* w, int64_t n, int dtype, double bound, doubl
   return PFR_OK;
 }
 
+int pfr_multinomial_range(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng, const double* uniforms,
+                          int64_t slot_begin, int64_t slot_count, int32_t* a, uint32_t* status, void* ws_ptr,
+                          size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && (a || slot_count == 0), "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(uniforms || rng, "multinomial needs uniforms or an rng");
+  PFR_REQUIRE(accum >= 0 && accum < PFR_ACC_SERIAL, "unknown accumulation mode");
+  PFR_REQUIRE(slot_begin >= 0 && slot_count >= 0 && slot_begin + slot_count <= n, "slot range outside [0, N)");
+  if (slot_count == 0) return PFR_OK;
+  PFR_WS(PFR_OP_MULTINOMIAL);
+  PFR_CHECK_LAUNCH(launch_multinomial(w, n, dtype, accum, rng, uniforms, 0, a, status, ws, (cudaStream_t)stream,
+                                      slot_begin, slot_count),
+                   "pfr_multinomial_range");
+  return PFR_OK;
+}
+
+int pfr_permute_range(const int32_t* a, int64_t n, int64_t index_begin, int64_t index_count, int32_t* c,
+                      int32_t* max_steps, uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && a && (c || index_count == 0) && status, "bad arguments");
+  PFR_REQUIRE(index_begin >= 0 && index_count >= 0 && index_begin + index_count <= n, "index range outside [0, N)");
+  PFR_WS(PFR_OP_PERMUTE);
+  PFR_CHECK_LAUNCH(launch_permute_range(a, n, index_begin, index_count, c, max_steps, status, ws,
+                                        (cudaStream_t)stream),
+                   "pfr_permute_range");
+  return PFR_OK;
+}
+
 int pfr_cumulative_to_ancestors(const void* O, int64_t n, int idx_dtype, int32_t* a, uint32_t* status, void* ws_ptr,
                                 size_t ws_bytes, void* stream) {
   (void)ws_ptr;
@@ -446,6 +473,48 @@ int pfr_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double pr
   PFR_CHECK_LAUNCH(launch_shard_offspring(W_loc, n_loc, dtype, prefix, total, n_global, last_global, stratified, offset,
                                           uniforms, rng, O, (cudaStream_t)stream),
                    "pfr_shard_offspring");
+  return PFR_OK;
+}
+
+int pfr_shard_offspring_dev(const double* W_loc, int64_t n_loc, int dtype, const double* prefix_total,
+                            int64_t n_global, int last_global, int first_global, int stratified, double offset,
+                            const double* uniforms, const pfr_rng* rng, int32_t* O, int32_t* o_before, void* stream) {
+  PFR_REQUIRE(valid_n(n_loc) && valid_n(n_global) && n_loc <= n_global, "bad sizes");
+  PFR_REQUIRE(W_loc && prefix_total && O && o_before, "null array");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  if (stratified) PFR_REQUIRE(uniforms || rng, "stratified needs uniforms or an rng");
+  PFR_CHECK_LAUNCH(launch_shard_offspring_dev(W_loc, n_loc, dtype, prefix_total, n_global, last_global, first_global,
+                                              stratified, offset, uniforms, rng, O, o_before, (cudaStream_t)stream),
+                   "pfr_shard_offspring_dev");
+  return PFR_OK;
+}
+
+int pfr_shard_ext_words(const int32_t* O_loc, int64_t n_loc, int64_t index_base, const int32_t* o_before, int64_t halo,
+                        uint32_t* ext, uint8_t* has, uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n_loc) && index_base >= 0 && halo >= 0, "bad sizes");
+  PFR_REQUIRE(O_loc && o_before && ext && has && status, "null array");
+  PFR_CHECK_LAUNCH(launch_shard_ext(O_loc, n_loc, index_base, o_before, halo, ext, has, status, (cudaStream_t)stream),
+                   "pfr_shard_ext_words");
+  return PFR_OK;
+}
+
+int pfr_shard_merge_bands(uint32_t* ext, int64_t n_loc, int64_t halo, const uint32_t* bands, int rank, int world,
+                          uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n_loc) && halo >= 0 && world >= 1 && rank >= 0 && rank < world, "bad sizes");
+  PFR_REQUIRE(ext && (bands || halo == 0) && status, "null array");
+  if (halo == 0) return PFR_OK;
+  PFR_CHECK_LAUNCH(launch_shard_merge(ext, n_loc, halo, bands, rank, world, status, (cudaStream_t)stream),
+                   "pfr_shard_merge_bands");
+  return PFR_OK;
+}
+
+int pfr_shard_resolve_ext(const uint32_t* ext, int64_t n_loc, int64_t halo, const uint8_t* has, int64_t index_base,
+                          int32_t* c, int32_t* max_steps, uint32_t* status, void* stream) {
+  PFR_REQUIRE(valid_n(n_loc) && halo >= 0 && index_base >= 0, "bad sizes");
+  PFR_REQUIRE(ext && has && c && status, "null array");
+  PFR_CHECK_LAUNCH(launch_shard_resolve_ext(ext, n_loc, halo, has, index_base, c, max_steps, status,
+                                            (cudaStream_t)stream),
+                   "pfr_shard_resolve_ext");
   return PFR_OK;
 }
 

@@ -84,6 +84,8 @@ cudaError_t launch_permute_cumulative(const int32_t* O, int64_t n, int32_t* c, i
 cudaError_t launch_claims_reset(int64_t n, int32_t* max_steps, const Workspace& ws, cudaStream_t s);
 cudaError_t launch_walk(const int32_t* a, int64_t n, int32_t* c, int32_t* max_steps, uint32_t* status,
                         const Workspace& ws, cudaStream_t s);
+cudaError_t launch_permute_range(const int32_t* a, int64_t n, int64_t c_begin, int64_t c_count, int32_t* c,
+                                 int32_t* max_steps, uint32_t* status, const Workspace& ws, cudaStream_t s);
 cudaError_t launch_permute(const void* a, int64_t n, int idx_dtype, int32_t* c, int32_t* max_steps,
                            uint32_t* status, const Workspace& ws, cudaStream_t s);
 cudaError_t launch_prepermute(const void* a, int64_t n, int idx_dtype, int32_t* d, uint32_t* status,
@@ -100,7 +102,7 @@ cudaError_t launch_lower_bound(const void* W, int64_t n, int dtype, const double
                                cudaStream_t s);
 cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng,
                                const double* uniforms, int sorted_serial, int32_t* a, uint32_t* status,
-                               const Workspace& ws, cudaStream_t s);
+                               const Workspace& ws, cudaStream_t s, int64_t s_begin = 0, int64_t s_count = -1);
 cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng,
                               const double* u_draws, const void* j_draws, int idx_dtype, int32_t* a,
                               uint32_t* status, cudaStream_t s, int64_t c_begin = 0, int64_t c_count = -1, int32_t* claim = nullptr);
@@ -118,6 +120,17 @@ cudaError_t launch_rejection_replay(const void* w, int64_t n, int dtype, double 
 cudaError_t launch_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double prefix, double total,
                                    int64_t n_global, int last_global, int stratified, double offset,
                                    const double* uniforms, const pfr_rng* rng, int32_t* O, cudaStream_t s);
+cudaError_t launch_shard_offspring_dev(const double* W_loc, int64_t n_loc, int dtype, const double* prefix_total,
+                                       int64_t n_global, int last_global, int first_global, int stratified,
+                                       double offset, const double* uniforms, const pfr_rng* rng, int32_t* O,
+                                       int32_t* o_before, cudaStream_t s);
+cudaError_t launch_shard_ext(const int32_t* O, int64_t n_loc, int64_t index_base, const int32_t* o_before, int64_t H,
+                             uint32_t* ext, uint8_t* has, uint32_t* status, cudaStream_t s);
+cudaError_t launch_shard_merge(uint32_t* ext, int64_t n_loc, int64_t H, const uint32_t* bands, int rank, int world,
+                               uint32_t* status, cudaStream_t s);
+cudaError_t launch_shard_resolve_ext(const uint32_t* ext, int64_t n_loc, int64_t H, const uint8_t* has,
+                                     int64_t index_base, int32_t* c, int32_t* max_steps, uint32_t* status,
+                                     cudaStream_t s);
 cudaError_t launch_shard_words(const int32_t* O, int64_t n_loc, int64_t index_base, int32_t o_begin, uint32_t* words,
                                uint8_t* has, uint32_t* status, cudaStream_t s);
 cudaError_t launch_shard_resolve(const uint32_t* words, const uint8_t* has, int64_t n_loc, int64_t index_base,

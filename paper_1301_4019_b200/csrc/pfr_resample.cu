@@ -436,11 +436,12 @@ __global__ void k_lower_bound(const T* __restrict__ W, int64_t n, const double* 
 
 // multinomial, numpy stream: u_i = random()_i * float(W[N-1]) (resamplers.py:68-69)
 template <typename T>
-__global__ void k_multinomial_numpy(const T* __restrict__ W, int64_t n, Key2x64 key, int32_t* __restrict__ out) {
+__global__ void k_multinomial_numpy(const T* __restrict__ W, int64_t n, Key2x64 key, int64_t s0, int64_t count,
+                                    int32_t* __restrict__ out) {
   const double total = (double)W[n - 1];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double u = u64_to_unit(numpy_raw64(key, (uint64_t)i)) * total;
-    out[i] = (int32_t)lower_bound_dev(W, n, u);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const double u = u64_to_unit(numpy_raw64(key, (uint64_t)(s0 + t))) * total;
+    out[t] = (int32_t)lower_bound_dev(W, n, u);
   }
 }
 
@@ -497,47 +498,78 @@ __device__ int64_t mm_split(const T* __restrict__ W, const double* __restrict__ 
   return lo;
 }
 
+// number of W elements strictly below u (the merge takes W first only when
+// W[i] < U[j]: ties go to the uniform, as lower_bound)
+template <typename T>
+__device__ int64_t mm_below(const T* __restrict__ W, int64_t n, double u) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((double)W[mid] < u)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Merge of W with the sorted uniforms U[j] = S[j] / S[N] * W[N-1] along the
+// merge path; out[j - s0] = parent of slot j for the slots [s0, s1) (a
+// rank's share: the union over ranks is the full result).  The slots' merge
+// diagonals are [s0 + below(U[s0]), s1 + below(U[s1])) (2N for s1 = N);
+// CTAs stride over kMergeD-diagonal chunks of that range.
 template <typename T>
 __global__ void __launch_bounds__(256) k_multinomial_merge(const T* __restrict__ W, int64_t n,
-                                                           const double* __restrict__ S, int32_t* __restrict__ out) {
+                                                           const double* __restrict__ S, int64_t s0, int64_t s1,
+                                                           int32_t* __restrict__ out) {
   __shared__ double sbuf[kMergeD];  // the CTA's W run, then its U run (nw + nu = D)
   __shared__ int64_t split[2];
+  __shared__ int64_t range[2];
   const double total = (double)W[n - 1];
   const double norm = S[n];
-  const int64_t d0 = (int64_t)blockIdx.x * kMergeD;
-  const int64_t d1 = min(d0 + kMergeD, 2 * n);
-  if (threadIdx.x < 2) split[threadIdx.x] = mm_split<T>(W, S, n, threadIdx.x ? d1 : d0, norm, total);
-  __syncthreads();
-  const int64_t i0 = split[0], i1 = split[1];
-  const int64_t j0 = d0 - i0, j1 = d1 - i1;
-  const int nw = (int)(i1 - i0), nu = (int)(j1 - j0);
-  double* sw = sbuf;
-  double* su = sbuf + nw;
-  for (int t = threadIdx.x; t < nw; t += blockDim.x) sw[t] = (double)W[i0 + t];
-  for (int t = threadIdx.x; t < nu; t += blockDim.x) su[t] = mm_u<T>(S, j0 + t, norm, total);
-  __syncthreads();
-  // per-thread split inside the CTA's run
-  const int per = kMergeD / 256;
-  const int td = threadIdx.x * per;
-  if (td >= nw + nu) return;
-  int lo = td > nu ? td - nu : 0, hi = td < nw ? td : nw;
-  while (lo < hi) {
-    const int i = (lo + hi + 1) >> 1;
-    const int jj = td - i;
-    if (jj >= nu || sw[i - 1] < su[jj])
-      lo = i;
-    else
-      hi = i - 1;
+  if (threadIdx.x < 2) {
+    const int64_t sj = threadIdx.x ? s1 : s0;
+    range[threadIdx.x] = sj >= n ? 2 * n : sj + mm_below<T>(W, n, mm_u<T>(S, sj, norm, total));
   }
-  int i = lo, j = td - lo;
-  const int te = min(td + per, nw + nu);
-  for (int pos = td; pos < te; ++pos) {
-    if (j >= nu || (i < nw && sw[i] < su[j])) {
-      ++i;  // a W element: strictly below the next uniform
-    } else {
-      const int64_t a = i0 + i;
-      out[j0 + j] = (int32_t)(a < n ? a : n - 1);
-      ++j;
+  __syncthreads();
+  const int64_t D0 = range[0], D1 = range[1];
+  for (int64_t d0 = D0 + (int64_t)blockIdx.x * kMergeD; d0 < D1; d0 += (int64_t)gridDim.x * kMergeD) {
+    const int64_t d1 = min(d0 + kMergeD, D1);
+    __syncthreads();
+    if (threadIdx.x < 2) split[threadIdx.x] = mm_split<T>(W, S, n, threadIdx.x ? d1 : d0, norm, total);
+    __syncthreads();
+    const int64_t i0 = split[0], i1 = split[1];
+    const int64_t j0 = d0 - i0, j1 = d1 - i1;
+    const int nw = (int)(i1 - i0), nu = (int)(j1 - j0);
+    double* sw = sbuf;
+    double* su = sbuf + nw;
+    for (int t = threadIdx.x; t < nw; t += blockDim.x) sw[t] = (double)W[i0 + t];
+    for (int t = threadIdx.x; t < nu; t += blockDim.x) su[t] = mm_u<T>(S, j0 + t, norm, total);
+    __syncthreads();
+    // per-thread split inside the CTA's run
+    const int per = kMergeD / 256;
+    const int td = threadIdx.x * per;
+    if (td < nw + nu) {
+      int lo = td > nu ? td - nu : 0, hi = td < nw ? td : nw;
+      while (lo < hi) {
+        const int i = (lo + hi + 1) >> 1;
+        const int jj = td - i;
+        if (jj >= nu || sw[i - 1] < su[jj])
+          lo = i;
+        else
+          hi = i - 1;
+      }
+      int i = lo, j = td - lo;
+      const int te = min(td + per, nw + nu);
+      for (int pos = td; pos < te; ++pos) {
+        if (j >= nu || (i < nw && sw[i] < su[j])) {
+          ++i;  // a W element: strictly below the next uniform
+        } else {
+          const int64_t a = i0 + i;
+          out[j0 + j - s0] = (int32_t)(a < n ? a : n - 1);
+          ++j;
+        }
+      }
     }
   }
 }
@@ -720,7 +752,10 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
 
 cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng,
                                const double* uniforms, int sorted_serial, int32_t* a, uint32_t* status,
-                               const Workspace& ws, cudaStream_t s) {
+                               const Workspace& ws, cudaStream_t s, int64_t s_begin, int64_t s_count) {
+  if (s_count < 0) s_count = n - s_begin;
+  const bool full = s_begin == 0 && s_count == n;
+  if (sorted_serial && !full) return cudaErrorNotSupported;
   // W = inclusive scan of w (monotone, weights are non-negative) into scratch
   void* W = ws.f1;
   const int scan_flags = accum | PFR_SCAN_MONOTONE;
@@ -748,13 +783,15 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
   if (e != cudaSuccess) return e;
   const int mode = uniforms ? PFR_RNG_ARRAYS : (rng ? rng->mode : PFR_RNG_PHILOX);
   if (mode == PFR_RNG_ARRAYS) {
-    return launch_lower_bound(W, n, dtype, uniforms, n, a, s);
+    // the caller's uniforms of these slots
+    return launch_lower_bound(W, n, dtype, uniforms + s_begin, s_count, a, s);
   } else if (mode == PFR_RNG_NUMPY) {
     Key2x64 key{rng->key0, rng->key1};
+    const int gs = grid_for(s_count, 256);
     if (dtype == PFR_F64)
-      k_multinomial_numpy<double><<<g, 256, 0, s>>>((const double*)W, n, key, a);
+      k_multinomial_numpy<double><<<gs, 256, 0, s>>>((const double*)W, n, key, s_begin, s_count, a);
     else
-      k_multinomial_numpy<float><<<g, 256, 0, s>>>((const float*)W, n, key, a);
+      k_multinomial_numpy<float><<<gs, 256, 0, s>>>((const float*)W, n, key, s_begin, s_count, a);
     note_launch();
   } else {
     const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
@@ -764,11 +801,13 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
     e = launch_scan(ws.f0, ws.f0, n + 1, PFR_F64, PFR_F64, PFR_ACC_F64 | PFR_SCAN_MONOTONE, 0, nullptr, -1, status,
                     ws, s);
     if (e != cudaSuccess) return e;
-    const unsigned gm = (unsigned)((2 * n + kMergeD - 1) / kMergeD);
+    // the slots' diagonals number about 2 * s_count (+ the drift)
+    const unsigned gm = (unsigned)((2 * s_count + kMergeD - 1) / kMergeD);
+    const int64_t s1 = s_begin + s_count;
     if (dtype == PFR_F64)
-      k_multinomial_merge<double><<<gm, 256, 0, s>>>((const double*)W, n, ws.f0, a);
+      k_multinomial_merge<double><<<gm, 256, 0, s>>>((const double*)W, n, ws.f0, s_begin, s1, a);
     else
-      k_multinomial_merge<float><<<gm, 256, 0, s>>>((const float*)W, n, ws.f0, a);
+      k_multinomial_merge<float><<<gm, 256, 0, s>>>((const float*)W, n, ws.f0, s_begin, s1, a);
     note_launch();
   }
   return cudaGetLastError();

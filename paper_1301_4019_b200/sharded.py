@@ -16,12 +16,16 @@ exactly, and the data is partitioned so that each GPU streams only its share:
   `slot` (pfr_shard_advance) until they reach their loser, and the value goes
   back to the owner of the hole.  Drift between slot and parent is ~sqrt(N),
   so only a thin band at each boundary travels.
-* **Metropolis** -- the weight vector is all-gathered once; rank g runs the
-  chains of its output slice with their global chain numbers
-  (pfr_metropolis_range), so the union is bit-identical to the single-GPU
-  result; the ancestry is all-gathered and permuted (permute is replicated).
-* **multinomial / rejection** -- replicated over the all-gathered weights
-  (same stream on every rank, identical results), each rank keeps its slice.
+* **Metropolis / rejection / multinomial** -- the weight vector is
+  all-gathered once (the shard sizes and validation bits travel in one
+  all-gather before it, so every rank raises together); rank g draws the
+  ancestors of its output slots with their global stream numbers
+  (pfr_metropolis_range, pfr_rejection_range, pfr_multinomial_range: the
+  union is bit-identical to the single-GPU result).  The ancestry is
+  all-gathered once more and every rank resolves the in-place ancestry of its
+  OWN indices only (pfr_permute_range: claims over the full ancestry, loser
+  chains walked backwards from the rank's holes); a chain past the walk
+  bound on any rank falls back to the replicated permute.
 * **batched independent filters** need no communication at all (each rank
   calls the single-GPU API on its own filters).
 
@@ -35,6 +39,8 @@ the product.
 
 from __future__ import annotations
 
+import math
+import os
 import threading
 
 import numpy as np
@@ -87,6 +93,14 @@ class DistComm:
                                     group=self.group)
         return out.reshape(-1, width) if width > 1 else out
 
+    def all_gather_fixed(self, t: torch.Tensor) -> torch.Tensor:
+        """all-gather of equal-size tensors, rank order, staying on the
+        communicator's device (NCCL: no host round trip)"""
+        t = t.reshape(-1).to(self.device)
+        out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=self.device)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        return out
+
     def all_gather_var(self, t: torch.Tensor) -> torch.Tensor:
         sizes = [int(s) for s in self.all_gather_scalars(t.numel(), torch.int64)]
         m = max(sizes)
@@ -114,20 +128,30 @@ class ThreadComm:
         self.rank = rank
         self.world = hub.world
         self.device = torch.device(device) if device is not None else None  # None: tensors stay where they are
+        # every virtual rank enqueues on its own CUDA stream, as a real rank
+        # does on its own GPU: host threads interleaving launches on ONE
+        # stream measured unsafe (a thread stress test: 3 of 20 runs wrong)
+        self.stream = torch.cuda.Stream() if torch.cuda.is_available() else None
 
     @staticmethod
     def group(world: int, device=None) -> list["ThreadComm"]:
         hub = _ThreadHub(world)
         return [ThreadComm(hub, r, device) for r in range(world)]
 
-    def _exchange(self, obj):
+    def _exchange(self, obj, consume=lambda got: got):
+        """publish obj, let `consume` read every rank's object, and only then
+        release the peers: a producer must not free (and its allocator reuse)
+        a tensor before every consumer's copy of it has run, so the copies
+        are synchronised before the last barrier"""
         h = self.hub
         h.barrier.wait()
         h.slots[self.rank] = obj
         h.barrier.wait()
-        got = list(h.slots)
+        out = consume(list(h.slots))
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            torch.cuda.current_stream().synchronize()
         h.barrier.wait()
-        return got
+        return out
 
     def all_gather_scalars(self, x, dtype) -> list:
         return [type(x)(v) if not isinstance(x, torch.Tensor) else v for v in self._exchange(x)]
@@ -138,17 +162,17 @@ class ThreadComm:
         pieces = [rows[starts[r]: starts[r + 1]] for r in range(self.world)]
         if rows.is_cuda:
             torch.cuda.current_stream().synchronize()  # producers' kernels done before peers read
-        got = self._exchange(pieces)
-        parts = [got[q][self.rank] for q in range(self.world)]
         dev = self.device or send.device
-        return torch.cat([p.to(dev) for p in parts])
+        return self._exchange(pieces, lambda got: torch.cat([got[q][self.rank].to(dev) for q in range(self.world)]))
+
+    def all_gather_fixed(self, t: torch.Tensor) -> torch.Tensor:
+        return self.all_gather_var(t.reshape(-1))
 
     def all_gather_var(self, t: torch.Tensor) -> torch.Tensor:
         if t.is_cuda:
             torch.cuda.current_stream().synchronize()
-        got = self._exchange(t)
         dev = self.device or t.device
-        return torch.cat([g.to(dev) for g in got])
+        return self._exchange(t, lambda got: torch.cat([g.to(dev) for g in got]))
 
 
 # ---------------------------------------------------------------------------
@@ -182,9 +206,25 @@ class CudaShardOps:
     def status_bits(self) -> int:
         return L.read_status(self.status)
 
+    def reset(self):
+        """a fresh status word for this call (an earlier call's error bits
+        must not leak into this one)"""
+        self.status.zero_()
+
+    def check_local(self, w_local):
+        """check_weights (diagnostics.py:38-51) on this rank's shard, into the status word"""
+        w = L.as_weights(w_local)
+        L.call("pfr_check_weights", w.data_ptr(), w.numel(), L.dtype_code(w), self.status.data_ptr(),
+               L.stream_handle())
+
     def check(self):
         bits = L.read_status(self.status)
         L.raise_weight_errors(bits & ~L.ST_POSITIVE, "w", False)
+        if bits & L.ST_NOPROGRESS:
+            from .resamplers import MAX_REJECTION_ROUNDS
+
+            raise RuntimeError(f"rejection resampling made no progress after {MAX_REJECTION_ROUNDS} rounds; "
+                               "the weight bound is far above every weight")
         if bits & L.ST_NONTERMINATION:
             raise RuntimeError("permutation chain walk failed to terminate")
         if bits & (L.ST_RANGE | L.ST_NOTMONOTONE):
@@ -221,11 +261,15 @@ class CudaShardOps:
         O = self._on_dev(O)
         n = O.numel()
         o_end = int(O[-1].item())
-        words = torch.empty(max(o_end - o_begin, 0), dtype=torch.int32, device=self.dev)
+        # a shard without offspring has an empty slot window: keep a 1-element
+        # buffer (a null pointer is an argument error, and that rank would
+        # raise alone while the others wait in the next collective)
+        size = max(o_end - o_begin, 0)
+        words = torch.empty(max(size, 1), dtype=torch.int32, device=self.dev)
         has = torch.empty(n, dtype=torch.uint8, device=self.dev)
         L.call("pfr_shard_words", O.data_ptr(), n, int(base), int(o_begin), words.data_ptr(), has.data_ptr(),
                self.status.data_ptr(), L.stream_handle())
-        return words, has
+        return words[:size], has
 
     def resolve(self, words, has, base):
         words, has = self._on_dev(words), self._on_dev(has)
@@ -258,6 +302,66 @@ class CudaShardOps:
             L.call("pfr_shard_scatter", done.data_ptr(), k, int(base), c.numel(), c.data_ptr(),
                    self.status.data_ptr(), L.stream_handle())
 
+    # ---- protocol v2 (device-resident scalars, boundary bands) ----
+    def local_scan_dev(self, w: torch.Tensor):
+        """the shard's float64 inclusive scan and its total, both on the device"""
+        w = L.as_weights(w)
+        n = w.numel()
+        W = torch.empty(n, dtype=torch.float64, device=self.dev)
+        ws, wsb = self._workspace(n)
+        L.call("pfr_scan", w.data_ptr(), W.data_ptr(), n, L.dtype_code(w), L.F64, L.ACC_F64 | L.SCAN_MONOTONE, 0, None,
+               self.status.data_ptr(), ws, wsb, L.stream_handle())
+        return W, W[-1:]
+
+    def prefix_total(self, totals: torch.Tensor, rank: int) -> torch.Tensor:
+        """{weight before this shard, W_N}: left folds of the shard totals in
+        rank order (the same IEEE additions on every rank), on the device"""
+        totals = self._on_dev(totals).to(torch.float64)
+        acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        prefix = acc
+        for r in range(totals.numel()):
+            if r == rank:
+                prefix = acc.clone()
+            acc = acc + totals[r: r + 1]
+        return torch.cat([prefix, acc])
+
+    def offspring_dev(self, W, wdtype, pt, n_global, last, first, stratified, offset, uniforms, rng, mode):
+        n = W.numel()
+        O = torch.empty(n, dtype=torch.int32, device=self.dev)
+        ob = torch.empty(1, dtype=torch.int32, device=self.dev)
+        k0, k1 = as_stream(rng).key() if rng is not None else (0, 0)
+        r = L.PfrRng(k0, k1, L.rng_mode_code(mode), 0)
+        uni = None if uniforms is None else torch.as_tensor(uniforms, dtype=torch.float64).to(self.dev).contiguous()
+        pt = self._on_dev(pt)
+        L.call("pfr_shard_offspring_dev", W.data_ptr(), n, L.F32 if wdtype == torch.float32 else L.F64, pt.data_ptr(),
+               int(n_global), int(last), int(first), int(stratified), float(offset), L.ptr(uni), r, O.data_ptr(),
+               ob.data_ptr(), L.stream_handle())
+        return O, ob
+
+    def ext_words(self, O, base, o_before, halo):
+        n = O.numel()
+        ext = torch.empty(n + 2 * halo, dtype=torch.int32, device=self.dev)
+        has = torch.empty(n, dtype=torch.uint8, device=self.dev)
+        L.call("pfr_shard_ext_words", O.data_ptr(), n, int(base), o_before.data_ptr(), int(halo), ext.data_ptr(),
+               has.data_ptr(), self.status.data_ptr(), L.stream_handle())
+        return ext, has
+
+    @staticmethod
+    def bands(ext, n_loc, halo):
+        return torch.cat([ext[: 2 * halo], ext[n_loc: n_loc + 2 * halo]])
+
+    def merge(self, ext, n_loc, halo, all_bands, rank, world):
+        all_bands = self._on_dev(all_bands)
+        L.call("pfr_shard_merge_bands", ext.data_ptr(), int(n_loc), int(halo), all_bands.data_ptr(), int(rank),
+               int(world), self.status.data_ptr(), L.stream_handle())
+
+    def resolve_ext(self, ext, n_loc, halo, has, base):
+        c = torch.empty(n_loc, dtype=torch.int32, device=self.dev)
+        st = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        L.call("pfr_shard_resolve_ext", ext.data_ptr(), int(n_loc), int(halo), has.data_ptr(), int(base), c.data_ptr(),
+               st.data_ptr(), self.status.data_ptr(), L.stream_handle())
+        return c, st
+
     def metropolis_range(self, w_full, b, rng, mode, c_begin, c_count):
         w_full = L.as_weights(w_full)
         a = torch.empty(c_count, dtype=torch.int32, device=self.dev)
@@ -285,23 +389,52 @@ class CudaShardOps:
         out_w = torch.empty(max(s_count, 1), dtype=w_full.dtype, device=self.dev) if capped else None
         k0, k1 = as_stream(rng).key()
         r = L.PfrRng(k0, k1, L.RNG_PHILOX, 0)
-        ws, wsb = L.workspace(w_full.numel())
+        ws, wsb = self._workspace(w_full.numel())
         L.call("pfr_rejection_range", w_full.data_ptr(), w_full.numel(), L.dtype_code(w_full),
                0.0 if capped else bound, bound if capped else 0.0, r, int(MAX_REJECTION_ROUNDS), int(s_begin),
                int(s_count), a.data_ptr(), None, L.ptr(out_w), self.status.data_ptr(), ws, wsb,
                L.stream_handle())
         return a[:s_count]
 
-    def full_ancestors(self, w_full, config, rng, mode):
-        from .resamplers import resample_ancestors
+    def multinomial_range(self, w_full, rng, mode, s_begin, s_count, uniforms=None):
+        """multinomial_ancestors (resamplers.py:56-74) for slots [s_begin,
+        s_begin + s_count) of the full weight vector, global parent numbers."""
+        w_full = L.as_weights(w_full)
+        n = w_full.numel()
+        a = torch.empty(max(s_count, 1), dtype=torch.int32, device=self.dev)
+        k0, k1 = as_stream(rng).key() if rng is not None else (0, 0)
+        r = L.PfrRng(k0, k1, L.rng_mode_code(mode), 0)
+        uni = None if uniforms is None else torch.as_tensor(uniforms, dtype=torch.float64).to(self.dev).contiguous()
+        ws, wsb = self._workspace(n)
+        L.call("pfr_multinomial_range", w_full.data_ptr(), n, L.dtype_code(w_full), L.ACC_F64, r, L.ptr(uni),
+               int(s_begin), int(s_count), a.data_ptr(), self.status.data_ptr(), ws, wsb, L.stream_handle())
+        return a[:s_count]
 
-        kw = {"rng_mode": mode, "index_dtype": torch.int32}
-        return resample_ancestors(w_full, config, rng, **kw).ancestors
+    def permute_range(self, a_full, base, n_loc):
+        """this rank's indices of permute_parallel (ancestry.py:139-174) over
+        the full ancestry: (c_local, max steps, overflow)"""
+        a_full = self._on_dev(torch.as_tensor(a_full).to(torch.int32))
+        n = a_full.numel()
+        c = torch.empty(max(n_loc, 1), dtype=torch.int32, device=self.dev)
+        st = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        ws, wsb = self._workspace(n)
+        L.call("pfr_permute_range", a_full.data_ptr(), n, int(base), int(n_loc), c.data_ptr(), st.data_ptr(),
+               flag.data_ptr(), ws, wsb, L.stream_handle())
+        return c[:n_loc], st, flag
+
+    def overflowed(self, flag) -> bool:
+        return bool(L.read_status(flag) & L.ST_OVERFLOW)
 
     def permute(self, a_full):
-        from .ancestry import permute_parallel
-
-        return permute_parallel(a_full, index_dtype=torch.int32)
+        """the replicated full permute (fallback of permute_range)"""
+        a_full = self._on_dev(torch.as_tensor(a_full).to(torch.int32))
+        n = a_full.numel()
+        c = torch.empty(n, dtype=torch.int32, device=self.dev)
+        ws, wsb = self._workspace(n)
+        L.call("pfr_permute", a_full.data_ptr(), n, L.I32, c.data_ptr(), None, self.status.data_ptr(), ws, wsb,
+               L.stream_handle())
+        return c
 
 
 # ---------------------------------------------------------------------------
@@ -342,6 +475,26 @@ def _fold(values):
     return out, acc
 
 
+def _on_rank_stream(fn):
+    """run a protocol entry point on the communicator's own stream, if it has
+    one (virtual ranks), and hand the results back complete"""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, comm, **kw):
+        stream = getattr(comm, "stream", None)
+        if stream is None:
+            return fn(*args, comm=comm, **kw)
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(stream):
+            out = fn(*args, comm=comm, **kw)
+        stream.synchronize()
+        return out
+
+    return wrapper
+
+
+@_on_rank_stream
 def deliver_sharded(w_local, config, rng, *, comm, ops=None, rng_mode=None, uniforms=None,
                     return_max_steps: bool = False):
     """permute_parallel(resample_ancestors(w, config, rng).ancestors) for the
@@ -352,29 +505,53 @@ def deliver_sharded(w_local, config, rng, *, comm, ops=None, rng_mode=None, unif
     metropolis / rejection: chains / slots partitioned over the all-gathered
     weights; multinomial: replicated over the all-gathered weights."""
     ops = ops or CudaShardOps()
+    ops.reset()
     alg = config.algorithm
     if alg in ("systematic", "stratified"):
         return _deliver_offspring_sharded(w_local, alg == "stratified", rng, comm, ops, rng_mode, uniforms,
                                           return_max_steps)
-    sizes = [int(s) for s in comm.all_gather_scalars(int(w_local.numel()), torch.int64)]
+    w_local = torch.as_tensor(w_local)
+    # one exchange before the data moves: shard sizes and this shard's
+    # validation bits (check_weights, diagnostics.py:38-51), so every rank
+    # raises together and no rank waits in a collective another has left
+    ops.check_local(w_local)
+    rows = comm.all_gather_scalars(int(w_local.numel()) | (int(ops.status_bits()) << 40), torch.int64)
+    sizes = [int(r) & ((1 << 40) - 1) for r in rows]
+    bits = 0
+    for r in rows:
+        bits |= int(r) >> 40
+    L.raise_weight_errors(bits, "w", True)
     offs, n = shard_bounds(sizes)
     base, n_loc = int(offs[comm.rank]), sizes[comm.rank]
-    w_full = comm.all_gather_var(torch.as_tensor(w_local))
+    w_full = comm.all_gather_var(w_local)
     if alg == "metropolis":
         a_loc = metropolis_sharded(w_local, config, rng, comm=comm, ops=ops, rng_mode=rng_mode, _w_full=w_full,
                                    _sizes=sizes)
-        a_full = comm.all_gather_var(a_loc)
     elif alg in ("rejection", "rejection-capped"):
         # slots partitioned like Metropolis' chains (SURVEY 8(e))
-        a_full = comm.all_gather_var(ops.rejection_range(w_full, config, rng, rng_mode, base, n_loc))
+        a_loc = ops.rejection_range(w_full, config, rng, rng_mode, base, n_loc)
+    elif alg == "multinomial":
+        a_loc = ops.multinomial_range(w_full, rng, rng_mode, base, n_loc, uniforms)
     else:
-        a_full = ops.full_ancestors(w_full, config, rng, rng_mode)
-    c_full = ops.permute(torch.as_tensor(a_full))
-    c = c_full[base: base + n_loc]
+        raise ValueError(f"unknown algorithm {alg!r}")
+    # the in-place ancestry of this rank's indices only (pfr_permute_range)
+    a_full = comm.all_gather_var(a_loc)
+    c, steps, flag = ops.permute_range(a_full, base, n_loc)
+    over = 0
+    for f in comm.all_gather_scalars(int(ops.overflowed(flag)), torch.int64):
+        over |= int(f)
+    if over:  # a chain beyond the walk bound somewhere: the replicated permute
+        c = ops.permute(a_full)[base: base + n_loc]
+        steps = None
     ops.check()
-    return (c, None) if return_max_steps else c
+    if not return_max_steps:
+        return c
+    if steps is None:
+        return c, None
+    return c, int(max(comm.all_gather_scalars(int(L.read_status(steps)), torch.int64)))
 
 
+@_on_rank_stream
 def metropolis_sharded(w_local, config_or_b, rng, *, comm, ops=None, rng_mode=None, _w_full=None, _sizes=None):
     """metropolis_ancestors (resamplers.py:204-234) with the N chains split over
     the ranks: returns this rank's slice of the ancestry (global indices)."""
@@ -391,7 +568,77 @@ def metropolis_sharded(w_local, config_or_b, rng, *, comm, ops=None, rng_mode=No
     return ops.metropolis_range(w_full, b, rng, rng_mode, int(offs[comm.rank]), sizes[comm.rank])
 
 
+# how often each systematic/stratified protocol ran (diagnostics; tests)
+protocol_counts = {"v2": 0, "general": 0}
+_count_lock = threading.Lock()
+
+
+def _count(path):
+    with _count_lock:
+        protocol_counts[path] += 1
+
+
+def halo_width(n: int) -> int:
+    """slots kept on each side of a shard boundary (protocol v2): several
+    times the typical drift between slot and parent (~sqrt(N) for i.i.d.
+    weights) so loser chains stay inside; PFR_SHARD_HALO overrides"""
+    env = os.environ.get("PFR_SHARD_HALO")
+    if env:
+        return max(int(env), 0)
+    return max(2048, 8 * math.isqrt(max(n, 1)))
+
+
 def _deliver_offspring_sharded(w_local, stratified, rng, comm, ops, rng_mode, uniforms, return_max_steps):
+    """Protocol v2: two host synchronisations in all (the shard sizes with the
+    validation bits at the start, the status bits at the end); the shard
+    totals and the boundary bands move device to device."""
+    rank, world = comm.rank, comm.world
+    w_local = torch.as_tensor(w_local)
+    ops.check_local(w_local)
+    rows = comm.all_gather_scalars(int(w_local.numel()) | (int(ops.status_bits()) << 40), torch.int64)
+    sizes = [int(r) & ((1 << 40) - 1) for r in rows]
+    bits = 0
+    for r in rows:
+        bits |= int(r) >> 40
+    L.raise_weight_errors(bits, "w", True)
+    offs, n = shard_bounds(sizes)
+    base, n_loc = int(offs[rank]), sizes[rank]
+    if min(sizes) < 1:
+        raise ValueError("every rank needs a non-empty weight shard")
+    halo = halo_width(n)
+
+    # 1. local scan; shard totals device to device; prefix and W_N on the device
+    W_loc, t_loc = ops.local_scan_dev(w_local)
+    pt = ops.prefix_total(comm.all_gather_fixed(t_loc), rank)
+    # 2. offspring in global slot numbers, the slot words of this shard's
+    #    window written into the extended array around its indices
+    offset = 0.0 if stratified else ops.systematic_offset(rng, rng_mode)
+    O, o_before = ops.offspring_dev(W_loc, w_local.dtype, pt, n, rank == world - 1, rank == 0, stratified, offset,
+                                    uniforms, rng, rng_mode)
+    ext, has = ops.ext_words(O, base, o_before, halo)
+    # 3. one fixed-size all-gather of every rank's boundary bands
+    ops.merge(ext, n_loc, halo, comm.all_gather_fixed(ops.bands(ext, n_loc, halo)), rank, world)
+    # 4. the in-place ancestry of this shard's indices
+    c, steps = ops.resolve_ext(ext, n_loc, halo, has, base)
+    rows = comm.all_gather_scalars(int(ops.status_bits()) | (int(L.read_status(steps)) << 32), torch.int64)
+    bits = 0
+    for r in rows:
+        bits |= int(r) & 0xFFFFFFFF
+    if bits & L.ST_OVERFLOW:  # a drift or chain beyond the halo somewhere: the general protocol
+        ops.reset()
+        _count("general")
+        return _deliver_offspring_general(w_local, stratified, rng, comm, ops, rng_mode, uniforms, return_max_steps)
+    _count("v2")
+    ops.check()
+    if return_max_steps:
+        return c, max(int(r) >> 32 for r in rows)
+    return c
+
+
+
+def _deliver_offspring_general(w_local, stratified, rng, comm, ops, rng_mode, uniforms, return_max_steps):
+    """the general protocol (variable slot-word all-to-all, walker rounds): the
+    fallback when a drift or a loser chain reaches beyond the halo"""
     rank, world = comm.rank, comm.world
     w_local = torch.as_tensor(w_local)
     sizes = [int(s) for s in comm.all_gather_scalars(int(w_local.numel()), torch.int64)]

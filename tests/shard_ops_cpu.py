@@ -35,8 +35,22 @@ class NumpyShardOps:
     def status_bits(self):
         return self.bits
 
+    def reset(self):
+        self.bits = 0
+
     def check(self):
         pass
+
+    def check_local(self, w_local):
+        from paper_1301_4019_b200 import _lib as L
+
+        w = _np(w_local)
+        if not np.all(np.isfinite(w)):
+            self.bits |= L.ST_NONFINITE
+        if np.any(w < 0):
+            self.bits |= L.ST_NEGATIVE
+        if np.any(w > 0):
+            self.bits |= L.ST_POSITIVE
 
     def local_scan(self, w):
         w = _np(w)
@@ -125,6 +139,100 @@ class NumpyShardOps:
         for h, v in _np(done).reshape(-1, 2).tolist():
             c[h - base] = v
 
+    # ---- protocol v2 (csrc/pfr_shard.cu: k_shard_offspring_dev, k_shard_ext_words,
+    # k_shard_merge, k_shard_resolve_ext), in NumPy
+    SENT = 0xFFFFFFFF
+
+    def local_scan_dev(self, w):
+        W, t = self.local_scan(w)
+        return W, W[-1:].clone()
+
+    def prefix_total(self, totals, rank):
+        totals = _np(totals, np.float64)
+        acc, prefix = 0.0, 0.0
+        for r, v in enumerate(totals.tolist()):
+            if r == rank:
+                prefix = acc
+            acc = acc + v
+        return torch.tensor([prefix, acc], dtype=torch.float64)
+
+    def offspring_dev(self, W, wdtype, pt, n_global, last, first, stratified, offset, uniforms, rng, mode):
+        prefix, total = _np(pt, np.float64).tolist()
+        O = self.offspring(W, wdtype, prefix, total, n_global, last, stratified, offset, uniforms, rng, mode)
+        if first:
+            ob = 0
+        else:  # the formula at W = prefix (the previous shard's last element)
+            ob = int(self.offspring(torch.zeros(1, dtype=torch.float64), wdtype, prefix, total, n_global, False,
+                                    stratified, offset, uniforms, rng, mode)[0])
+        return O, torch.tensor([ob], dtype=torch.int32)
+
+    def ext_words(self, O, base, o_before, halo):
+        from paper_1301_4019_b200 import _lib as L
+
+        O = _np(O, np.int64)
+        n = O.size
+        ext = np.full(n + 2 * halo, self.SENT, dtype=np.uint64)
+        prev = np.concatenate([[int(_np(o_before)[0])], O[:-1]])
+        o = O - prev
+        if np.any(o < 0):
+            self.bits |= L.ST_NOTMONOTONE
+        has = (o > 0).astype(np.uint8)
+        lo_slot = base - halo
+        for i in np.flatnonzero(o > 0).tolist():
+            for sl in range(int(prev[i]), int(O[i])):
+                pos = sl - lo_slot
+                if 0 <= pos < ext.size:
+                    ext[pos] = (base + i) | (FIRST if sl == prev[i] else 0)
+                else:
+                    self.bits |= L.ST_OVERFLOW
+        return torch.from_numpy(ext.astype(np.uint32).view(np.int32)), torch.from_numpy(has)
+
+    @staticmethod
+    def bands(ext, n_loc, halo):
+        return torch.cat([ext[: 2 * halo], ext[n_loc: n_loc + 2 * halo]])
+
+    def merge(self, ext, n_loc, halo, all_bands, rank, world):
+        e = ext.numpy().view(np.uint32)
+        b = _np(all_bands).view(np.uint32).reshape(world, 4 * halo)
+        if rank > 0:
+            src = b[rank - 1, 2 * halo:]
+            m = (src != self.SENT) & (e[: 2 * halo] == self.SENT)
+            e[: 2 * halo][m] = src[m]
+        if rank + 1 < world:
+            src = b[rank + 1, : 2 * halo]
+            m = (src != self.SENT) & (e[n_loc: n_loc + 2 * halo] == self.SENT)
+            e[n_loc: n_loc + 2 * halo][m] = src[m]
+
+    def resolve_ext(self, ext, n_loc, halo, has, base):
+        from paper_1301_4019_b200 import _lib as L
+
+        e = ext.numpy().view(np.uint32)
+        has = _np(has)
+        c = np.empty(n_loc, dtype=np.int32)
+        lo_slot, longest = base - halo, 0
+        for i in range(n_loc):
+            if has[i]:
+                c[i] = base + i
+                continue
+            wd = int(e[halo + i])
+            if wd == self.SENT:
+                self.bits |= L.ST_OVERFLOW
+                continue
+            st, ok = 0, True
+            while wd & FIRST:
+                pos = (wd & MASK) - lo_slot
+                st += 1
+                if st > 4096 or pos < 0 or pos >= e.size or int(e[pos]) == self.SENT:
+                    ok = False
+                    break
+                wd = int(e[pos])
+            if not ok:
+                self.bits |= L.ST_OVERFLOW
+                continue
+            c[i] = wd & MASK
+            longest = max(longest, st)
+        return torch.from_numpy(c), torch.tensor([longest], dtype=torch.int32)
+
     def metropolis_range(self, w_full, b, rng, mode, c_begin, c_count):
         a = orc.metropolis_stream(_np(w_full), b, rng.seed, rng.ids)
         return torch.from_numpy(a[c_begin: c_begin + c_count].astype(np.int32))
@@ -137,11 +245,32 @@ class NumpyShardOps:
         a = orc.rejection_stream(w, sup, rng.seed, rng.ids)[0]
         return torch.from_numpy(a[s_begin: s_begin + s_count].astype(np.int32))
 
-    def full_ancestors(self, w_full, config, rng, mode):
-        w = _np(w_full)
-        if config.algorithm == "multinomial":
-            return torch.from_numpy(orc.multinomial_stream(w, rng.seed, rng.ids).astype(np.int32))
-        raise NotImplementedError(config.algorithm)
+    def multinomial_range(self, w_full, rng, mode, s_begin, s_count, uniforms=None):
+        a = orc.multinomial_stream(_np(w_full), rng.seed, rng.ids)
+        return torch.from_numpy(a[s_begin: s_begin + s_count].astype(np.int32))
+
+    def permute_range(self, a_full, base, n_loc):
+        """the backward walks of csrc/pfr_ancestry.cu's k_permute_range, in NumPy"""
+        a = _np(a_full, np.int64)
+        n = a.size
+        d = orc.prepermute(a)
+        c = np.empty(n_loc, dtype=np.int32)
+        longest = 0
+        for t in range(n_loc):
+            x = base + t
+            if d[x] < n:
+                c[t] = x
+                continue
+            z, hops = x, 0
+            while d[a[z]] == z:
+                z = a[z]
+                hops += 1
+            c[t] = a[z]
+            longest = max(longest, hops)
+        return torch.from_numpy(c), torch.tensor([longest], dtype=torch.int32), torch.zeros(1, dtype=torch.int32)
+
+    def overflowed(self, flag):
+        return False
 
     def permute(self, a_full):
         return torch.from_numpy(orc.permute(_np(a_full)).astype(np.int32))

@@ -113,7 +113,7 @@ def test_threads_long_chains_cross_every_boundary():
     assert steps == want_steps and steps > 50
 
 
-@pytest.mark.parametrize("alg", ["metropolis", "multinomial"])
+@pytest.mark.parametrize("alg", ["metropolis", "multinomial", "rejection"])
 def test_threads_ancestry_algorithms(alg):
     w = int_weights(1024, 21)
     rs = RngStream(5, (1,))
@@ -130,6 +130,27 @@ def test_threads_rejection_slots_partitioned():
     c, _ = sharded_threads(w, 3, "rejection", rs, NumpyShardOps)
     a = orc.rejection_stream(w, float(w.max()), rs.seed, rs.ids)[0]
     np.testing.assert_array_equal(c, orc.permute(a))
+
+
+def test_threads_v2_and_general_protocols():
+    """the default halo keeps i.i.d. weights on protocol v2; a zero halo
+    forces every rank onto the general protocol together -- same result"""
+    from paper_1301_4019_b200 import sharded
+
+    w = int_weights(3000, 17)
+    rs = RngStream(2)
+    want = orc.deliver(w, "systematic", rs.seed, rs.ids)
+    before = dict(sharded.protocol_counts)
+    c, _ = sharded_threads(w, 3, "systematic", rs, NumpyShardOps)
+    np.testing.assert_array_equal(c, want)
+    assert sharded.protocol_counts["v2"] == before["v2"] + 3
+    os.environ["PFR_SHARD_HALO"] = "0"
+    try:
+        c, _ = sharded_threads(w, 3, "systematic", rs, NumpyShardOps)
+    finally:
+        del os.environ["PFR_SHARD_HALO"]
+    np.testing.assert_array_equal(c, want)
+    assert sharded.protocol_counts["general"] == before["general"] + 3
 
 
 def test_threads_errors_raise_on_every_rank():
@@ -177,7 +198,8 @@ def _gloo_worker(rank, world, port, alg, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("alg", ["systematic", "systematic-long", "stratified", "metropolis"])
+@pytest.mark.parametrize("alg", ["systematic", "systematic-long", "stratified", "metropolis", "multinomial",
+                                 "rejection"])
 def test_gloo_world2(alg):
     import torch.multiprocessing as mp
 
@@ -290,3 +312,82 @@ def test_gpu_sharded_real_processes(procs):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     assert r.stdout.count("identical") == 6 and "DIFFERENT" not in r.stdout, r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("mode", ["philox", "numpy"])
+def test_gpu_sharded_multinomial_bit_identical(world, mode):
+    """Slot-partitioned multinomial (pfr_multinomial_range: every rank merges
+    only its slots' sorted uniforms with W) plus the partitioned permute
+    (pfr_permute_range) equal the single-GPU delivery at 2/4/8 virtual ranks."""
+    import paper_1301_4019_b200 as pf
+    from paper_1301_4019_b200.sharded import CudaShardOps
+
+    g = np.random.default_rng(40 + world)
+    lw = g.normal(0, 1, 1 << 16)
+    w = np.exp(lw - lw.max())
+    rs = RngStream(21, (world,))
+    cuts = split(w.size, world, 5)
+    c, steps = sharded_threads(w, world, "multinomial", rs, CudaShardOps, cuts=cuts, rng_mode=mode)
+    single, want_steps = pf.deliver(w, ResamplerConfig("multinomial"), rs, rng_mode=mode, return_max_steps=True)
+    np.testing.assert_array_equal(c, single.cpu().numpy())
+    assert steps == int(want_steps)
+
+
+@pytest.mark.gpu
+def test_gpu_permute_range_union_is_the_permute():
+    """pfr_permute_range over any index partition reproduces permute_parallel,
+    including its longest chain (random ancestries and an adversarial chain)."""
+    import paper_1301_4019_b200 as pf
+    from paper_1301_4019_b200.sharded import CudaShardOps
+
+    g = np.random.default_rng(2)
+    n = 4000  # the adversarial chain (n - 2 hops) stays under the 4096-hop walk bound
+    cases = [g.integers(0, n, n), np.sort(g.integers(0, n, n)), np.r_[np.arange(1, n), [n - 1]]]
+    ops = CudaShardOps()
+    long_chain = np.r_[np.arange(1, 6000), [5999]].astype(np.int32)
+    _, _, flag = ops.permute_range(torch.from_numpy(long_chain), 0, 6000)
+    assert ops.overflowed(flag)  # beyond the bound: the caller falls back to the full permute
+    for a in cases:
+        want, want_steps = orc.permute(a, with_steps=True)
+        cuts = [0, 1, 1234, 2500, n]  # uneven, with a one-index part
+        parts, steps = [], 0
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            c, st, flag = ops.permute_range(torch.from_numpy(a.astype(np.int32)), lo, hi - lo)
+            assert not ops.overflowed(flag)
+            parts.append(c.cpu().numpy())
+            steps = max(steps, int(st.item()))
+        np.testing.assert_array_equal(np.concatenate(parts), want)
+        assert steps == want_steps
+        ops.check()
+
+
+@pytest.mark.gpu
+def test_gpu_sharded_zero_weight_shard():
+    """A rank whose whole shard weighs zero has an empty slot window (ADVICE:
+    it must not fail alone while the others wait in the next collective)."""
+    import paper_1301_4019_b200 as pf
+    from paper_1301_4019_b200.sharded import CudaShardOps
+
+    w = int_weights(6000, 3, zeros=0.0)
+    w[2000:4000] = 0.0
+    rs = RngStream(6)
+    for alg in ("systematic", "stratified"):
+        c, _ = sharded_threads(w, 3, alg, rs, CudaShardOps, cuts=np.array([0, 2000, 4000, 6000]))
+        want = orc.deliver(w, alg, rs.seed, rs.ids)
+        np.testing.assert_array_equal(c, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alg", ["metropolis", "rejection", "multinomial"])
+def test_gpu_sharded_bad_weights_raise_on_every_rank(alg):
+    """Negative weights on one shard raise the reference's ValueError on every
+    rank (the validation bits travel with the shard sizes)."""
+    from paper_1301_4019_b200.sharded import CudaShardOps
+
+    w = int_weights(3000, 4)
+    w[2500] = -1.0
+    mode = "philox" if alg == "rejection" else "numpy"
+    with pytest.raises(ValueError, match="non-negative"):
+        sharded_threads(w, 2, alg, RngStream(3), CudaShardOps, b=8 if alg == "metropolis" else None, rng_mode=mode)
