@@ -313,10 +313,11 @@ int pfr_shard_offspring_dev(const double* W_loc, int64_t n_loc, int dtype, const
  * window outside that range sets PFR_ST_OVERFLOW. */
 int pfr_shard_ext_words(const int32_t* O_loc, int64_t n_loc, int64_t index_base, const int32_t* o_before, int64_t halo,
                         uint32_t* ext, uint8_t* has, uint32_t* status, void* stream);
-/* Fill ext's sentinels from the neighbours' boundary bands: bands[world][4*halo]
- * holds every rank's ext[0, 2*halo) followed by its ext[n, n + 2*halo). */
-int pfr_shard_merge_bands(uint32_t* ext, int64_t n_loc, int64_t halo, const uint32_t* bands, int rank, int world,
-                          uint32_t* status, void* stream);
+/* Fill ext's sentinels from the neighbours' boundary bands: from_left = the
+ * left neighbour's ext[n, n + 2*halo), from_right = the right neighbour's
+ * ext[0, 2*halo) (null at the ends of the rank order). */
+int pfr_shard_merge_bands(uint32_t* ext, int64_t n_loc, int64_t halo, const uint32_t* from_left,
+                          const uint32_t* from_right, void* stream);
 /* The in-place ancestry of the shard's indices (ancestry.py:139-174 read
  * backwards from each hole) with every chain inside ext; a missing word or a
  * chain leaving ext sets PFR_ST_OVERFLOW (the caller reruns the general

@@ -498,12 +498,12 @@ int pfr_shard_ext_words(const int32_t* O_loc, int64_t n_loc, int64_t index_base,
   return PFR_OK;
 }
 
-int pfr_shard_merge_bands(uint32_t* ext, int64_t n_loc, int64_t halo, const uint32_t* bands, int rank, int world,
-                          uint32_t* status, void* stream) {
-  PFR_REQUIRE(valid_n(n_loc) && halo >= 0 && world >= 1 && rank >= 0 && rank < world, "bad sizes");
-  PFR_REQUIRE(ext && (bands || halo == 0) && status, "null array");
-  if (halo == 0) return PFR_OK;
-  PFR_CHECK_LAUNCH(launch_shard_merge(ext, n_loc, halo, bands, rank, world, status, (cudaStream_t)stream),
+int pfr_shard_merge_bands(uint32_t* ext, int64_t n_loc, int64_t halo, const uint32_t* from_left,
+                          const uint32_t* from_right, void* stream) {
+  PFR_REQUIRE(valid_n(n_loc) && halo >= 0, "bad sizes");
+  PFR_REQUIRE(ext, "null array");
+  if (halo == 0 || (!from_left && !from_right)) return PFR_OK;
+  PFR_CHECK_LAUNCH(launch_shard_merge(ext, n_loc, halo, from_left, from_right, (cudaStream_t)stream),
                    "pfr_shard_merge_bands");
   return PFR_OK;
 }

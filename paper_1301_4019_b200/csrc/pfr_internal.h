@@ -126,8 +126,8 @@ cudaError_t launch_shard_offspring_dev(const double* W_loc, int64_t n_loc, int d
                                        int32_t* o_before, cudaStream_t s);
 cudaError_t launch_shard_ext(const int32_t* O, int64_t n_loc, int64_t index_base, const int32_t* o_before, int64_t H,
                              uint32_t* ext, uint8_t* has, uint32_t* status, cudaStream_t s);
-cudaError_t launch_shard_merge(uint32_t* ext, int64_t n_loc, int64_t H, const uint32_t* bands, int rank, int world,
-                               uint32_t* status, cudaStream_t s);
+cudaError_t launch_shard_merge(uint32_t* ext, int64_t n_loc, int64_t H, const uint32_t* from_left,
+                               const uint32_t* from_right, cudaStream_t s);
 cudaError_t launch_shard_resolve_ext(const uint32_t* ext, int64_t n_loc, int64_t H, const uint8_t* has,
                                      int64_t index_base, int32_t* c, int32_t* max_steps, uint32_t* status,
                                      cudaStream_t s);

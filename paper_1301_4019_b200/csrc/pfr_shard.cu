@@ -268,20 +268,20 @@ __global__ void k_shard_ext_words(const int32_t* __restrict__ O, int64_t n_loc, 
   status_or_warp(status, f);
 }
 
-// fill the sentinel positions of ext from the neighbours' bands (bands:
-// [world][4H] = every rank's ext[0, 2H) then ext[n, n + 2H)); then every
-// own index must have its word
-__global__ void k_shard_merge(uint32_t* __restrict__ ext, int64_t n_loc, int64_t H, const uint32_t* __restrict__ bands,
-                              int rank, int world, uint32_t* status) {
+// fill the sentinel positions of ext from the neighbours' boundary bands:
+// from_left = the left neighbour's ext[n, n + 2H) (slots [base - H, base + H)),
+// from_right = the right neighbour's ext[0, 2H) (slots [base + n - H, base + n + H));
+// null at the ends of the rank order
+__global__ void k_shard_merge(uint32_t* __restrict__ ext, int64_t n_loc, int64_t H,
+                              const uint32_t* __restrict__ from_left, const uint32_t* __restrict__ from_right) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  for (int64_t q = t0; q < 2 * H; q += stride) {
-    if (rank > 0) {  // my [base - H, base + H) = left neighbour's right band
-      const uint32_t v = bands[(int64_t)(rank - 1) * 4 * H + 2 * H + q];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < 2 * H; q += stride) {
+    if (from_left) {
+      const uint32_t v = from_left[q];
       if (v != kSentinel && ext[q] == kSentinel) ext[q] = v;
     }
-    if (rank + 1 < world) {  // my [base + n - H, base + n + H) = right neighbour's left band
-      const uint32_t v = bands[(int64_t)(rank + 1) * 4 * H + q];
+    if (from_right) {
+      const uint32_t v = from_right[q];
       if (v != kSentinel && ext[n_loc + q] == kSentinel) ext[n_loc + q] = v;
     }
   }
@@ -416,9 +416,9 @@ cudaError_t launch_shard_ext(const int32_t* O, int64_t n_loc, int64_t index_base
   return cudaGetLastError();
 }
 
-cudaError_t launch_shard_merge(uint32_t* ext, int64_t n_loc, int64_t H, const uint32_t* bands, int rank, int world,
-                               uint32_t* status, cudaStream_t s) {
-  k_shard_merge<<<grid_for_n(2 * H), 256, 0, s>>>(ext, n_loc, H, bands, rank, world, status);
+cudaError_t launch_shard_merge(uint32_t* ext, int64_t n_loc, int64_t H, const uint32_t* from_left,
+                               const uint32_t* from_right, cudaStream_t s) {
+  k_shard_merge<<<grid_for_n(2 * H), 256, 0, s>>>(ext, n_loc, H, from_left, from_right);
   note_launch();
   return cudaGetLastError();
 }

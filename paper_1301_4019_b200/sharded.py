@@ -101,6 +101,27 @@ class DistComm:
         self.dist.all_gather_into_tensor(out, t, group=self.group)
         return out
 
+    def neighbor_exchange(self, to_left: torch.Tensor, to_right: torch.Tensor):
+        """send to_left to rank-1 and to_right to rank+1 (equal sizes), receive
+        (from_left, from_right) -- None at the ends; point to point (NCCL:
+        device to device, no host round trip)"""
+        reqs, ops = [], []
+        from_left = from_right = None
+        P2P = self.dist.P2POp
+        if self.rank > 0:
+            from_left = torch.empty_like(to_right, device=self.device)
+            ops += [P2P(self.dist.isend, to_left.contiguous().to(self.device), self.rank - 1, self.group),
+                    P2P(self.dist.irecv, from_left, self.rank - 1, self.group)]
+        if self.rank + 1 < self.world:
+            from_right = torch.empty_like(to_left, device=self.device)
+            ops += [P2P(self.dist.isend, to_right.contiguous().to(self.device), self.rank + 1, self.group),
+                    P2P(self.dist.irecv, from_right, self.rank + 1, self.group)]
+        if ops:
+            reqs = self.dist.batch_isend_irecv(ops)
+        for r in reqs:
+            r.wait()
+        return from_left, from_right
+
     def all_gather_var(self, t: torch.Tensor) -> torch.Tensor:
         sizes = [int(s) for s in self.all_gather_scalars(t.numel(), torch.int64)]
         m = max(sizes)
@@ -167,6 +188,18 @@ class ThreadComm:
 
     def all_gather_fixed(self, t: torch.Tensor) -> torch.Tensor:
         return self.all_gather_var(t.reshape(-1))
+
+    def neighbor_exchange(self, to_left: torch.Tensor, to_right: torch.Tensor):
+        if to_left.is_cuda:
+            torch.cuda.current_stream().synchronize()
+        dev = self.device or to_left.device
+
+        def pick(got):
+            left = got[self.rank - 1][1].to(dev).clone() if self.rank > 0 else None
+            right = got[self.rank + 1][0].to(dev).clone() if self.rank + 1 < self.world else None
+            return left, right
+
+        return self._exchange((to_left, to_right), pick)
 
     def all_gather_var(self, t: torch.Tensor) -> torch.Tensor:
         if t.is_cuda:
@@ -348,12 +381,15 @@ class CudaShardOps:
 
     @staticmethod
     def bands(ext, n_loc, halo):
-        return torch.cat([ext[: 2 * halo], ext[n_loc: n_loc + 2 * halo]])
+        """(this rank's ext[0, 2H), ext[n, n + 2H)): what the left and the
+        right neighbour need"""
+        return ext[: 2 * halo], ext[n_loc: n_loc + 2 * halo]
 
-    def merge(self, ext, n_loc, halo, all_bands, rank, world):
-        all_bands = self._on_dev(all_bands)
-        L.call("pfr_shard_merge_bands", ext.data_ptr(), int(n_loc), int(halo), all_bands.data_ptr(), int(rank),
-               int(world), self.status.data_ptr(), L.stream_handle())
+    def merge(self, ext, n_loc, halo, from_left, from_right):
+        fl = None if from_left is None else self._on_dev(from_left)
+        fr = None if from_right is None else self._on_dev(from_right)
+        L.call("pfr_shard_merge_bands", ext.data_ptr(), int(n_loc), int(halo), L.ptr(fl), L.ptr(fr),
+               L.stream_handle())
 
     def resolve_ext(self, ext, n_loc, halo, has, base):
         c = torch.empty(n_loc, dtype=torch.int32, device=self.dev)
@@ -579,19 +615,21 @@ def _count(path):
 
 
 def halo_width(n: int) -> int:
-    """slots kept on each side of a shard boundary (protocol v2): several
-    times the typical drift between slot and parent (~sqrt(N) for i.i.d.
-    weights) so loser chains stay inside; PFR_SHARD_HALO overrides"""
+    """slots kept on each side of a shard boundary (protocol v2): the drift
+    between slot and parent is ~sqrt(N) for i.i.d. weights and a
+    loser chain moves by it every step (p99 ~10 steps, tails ~30), so 32
+    sqrt(N) keeps nearly every chain inside; PFR_SHARD_HALO overrides"""
     env = os.environ.get("PFR_SHARD_HALO")
     if env:
         return max(int(env), 0)
-    return max(2048, 8 * math.isqrt(max(n, 1)))
+    return max(4096, 32 * math.isqrt(max(n, 1)))
 
 
 def _deliver_offspring_sharded(w_local, stratified, rng, comm, ops, rng_mode, uniforms, return_max_steps):
     """Protocol v2: two host synchronisations in all (the shard sizes with the
     validation bits at the start, the status bits at the end); the shard
-    totals and the boundary bands move device to device."""
+    totals (all-gather) and the boundary bands (to the two neighbours) move
+    device to device."""
     rank, world = comm.rank, comm.world
     w_local = torch.as_tensor(w_local)
     ops.check_local(w_local)
@@ -616,8 +654,8 @@ def _deliver_offspring_sharded(w_local, stratified, rng, comm, ops, rng_mode, un
     O, o_before = ops.offspring_dev(W_loc, w_local.dtype, pt, n, rank == world - 1, rank == 0, stratified, offset,
                                     uniforms, rng, rng_mode)
     ext, has = ops.ext_words(O, base, o_before, halo)
-    # 3. one fixed-size all-gather of every rank's boundary bands
-    ops.merge(ext, n_loc, halo, comm.all_gather_fixed(ops.bands(ext, n_loc, halo)), rank, world)
+    # 3. boundary bands to and from the two neighbours (point to point)
+    ops.merge(ext, n_loc, halo, *comm.neighbor_exchange(*ops.bands(ext, n_loc, halo)))
     # 4. the in-place ancestry of this shard's indices
     c, steps = ops.resolve_ext(ext, n_loc, halo, has, base)
     rows = comm.all_gather_scalars(int(ops.status_bits()) | (int(L.read_status(steps)) << 32), torch.int64)

@@ -189,17 +189,16 @@ class NumpyShardOps:
 
     @staticmethod
     def bands(ext, n_loc, halo):
-        return torch.cat([ext[: 2 * halo], ext[n_loc: n_loc + 2 * halo]])
+        return ext[: 2 * halo], ext[n_loc: n_loc + 2 * halo]
 
-    def merge(self, ext, n_loc, halo, all_bands, rank, world):
+    def merge(self, ext, n_loc, halo, from_left, from_right):
         e = ext.numpy().view(np.uint32)
-        b = _np(all_bands).view(np.uint32).reshape(world, 4 * halo)
-        if rank > 0:
-            src = b[rank - 1, 2 * halo:]
+        if from_left is not None:
+            src = _np(from_left).view(np.uint32)
             m = (src != self.SENT) & (e[: 2 * halo] == self.SENT)
             e[: 2 * halo][m] = src[m]
-        if rank + 1 < world:
-            src = b[rank + 1, : 2 * halo]
+        if from_right is not None:
+            src = _np(from_right).view(np.uint32)
             m = (src != self.SENT) & (e[n_loc: n_loc + 2 * halo] == self.SENT)
             e[n_loc: n_loc + 2 * halo][m] = src[m]
 
