@@ -172,6 +172,10 @@ def copy_particles(x: torch.Tensor, c) -> torch.Tensor:
     if x.dtype != torch.float64 or not x.is_contiguous() or x.device != c.device:
         raise ValueError("x must be a contiguous float64 tensor on the ancestry's device")
     n = c.numel()
+    if x.shape[0] != n:
+        raise ValueError(f"x has {x.shape[0]} particles but the ancestry vector has {n} entries")
+    if L.config.check and n and (int(c.min()) < 0 or int(c.max()) >= n):
+        raise ValueError(f"ancestry entries must lie in [0, {n})")  # an out-of-range c would read outside x
     width = x.numel() // n if n else 1
     L.call("pfr_copy_particles", x.data_ptr(), n, width, c.data_ptr(), L.stream_handle())
     return x

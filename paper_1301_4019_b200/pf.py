@@ -94,10 +94,12 @@ def pf_run(model: LinearGaussianModel, observations, n_particles: int, resampler
     ``observations``: shape (T,) (shared by every filter; ``filters``
     defaults to 1 and the result is squeezed like the reference's) or
     (filters, T).  Resampling: systematic (the batched kernels implement the
-    offspring algorithm; other algorithms raise NotImplementedError)."""
+    offspring algorithm, fused into the filter's kernels; every other
+    ResamplerConfig -- multinomial, stratified, Metropolis(B), rejection with
+    the tracked weight bound, rejection-capped with carried importance
+    weights -- runs the same filter through the library's resampling calls,
+    _pf_run_general)."""
     algorithm = resampler if isinstance(resampler, str) else resampler.algorithm
-    if algorithm != "systematic":
-        raise NotImplementedError("the batched filter resamples with the systematic algorithm")
     obs = np.asarray(observations, dtype=np.float64)
     squeeze = obs.ndim == 1 and filters is None
     if obs.ndim == 1:
@@ -109,6 +111,11 @@ def pf_run(model: LinearGaussianModel, observations, n_particles: int, resampler
     if not 0.0 <= ess_threshold <= 1.0:
         raise ValueError("ess_threshold must lie in [0, 1]")
     m_f, t_s = obs.shape
+    if algorithm != "systematic":
+        res = _pf_run_general(model, obs, int(n_particles), resampler, float(ess_threshold), seed)
+        if squeeze:
+            res = FilterResult(res.filtered_means[0], float(res.log_likelihood[0]), res.ess[0], res.resampled[0])
+        return res
     dev = L.device()
     y = torch.from_numpy(np.array(obs, dtype=np.float64, order="C")).to(dev)
     means = torch.empty((m_f, t_s), dtype=torch.float64, device=dev)
@@ -133,6 +140,78 @@ def pf_run(model: LinearGaussianModel, observations, n_particles: int, resampler
     return res
 
 
+def _pf_run_general(model, obs, n, resampler, ess_threshold, seed) -> FilterResult:
+    """pf_run (pf.py:111-204) with any ResamplerConfig, for (filters, T)
+    observations.  Propagation and weighting run on the device for every
+    filter at once; each filter whose ESS/N falls below the threshold
+    resamples through resample_ancestors + permute_parallel and the in-place
+    gather of pf_copy_step (Eq. 2).  As the reference: weights reset to 1/N
+    after resampling, except rejection-capped, whose importance weights are
+    carried; the rejection variants use the TRACKED weight bound (1/N after a
+    reset, times sup(density) / total at each weighting), ``sup_w`` read as a
+    bound on the raw observation density and ``sup_v`` as a cap on that
+    scale.  Randomness: the device Philox streams (stream (seed, filter,
+    purpose, step)); statistically the reference's filter."""
+    from dataclasses import replace
+
+    from .ancestry import copy_particles, permute_parallel
+    from .resamplers import ResamplerConfig, resample_ancestors
+
+    if isinstance(resampler, str):
+        resampler = ResamplerConfig(algorithm=resampler)
+    dev = L.device()
+    m_f, t_s = obs.shape
+    y = torch.from_numpy(np.ascontiguousarray(obs)).to(dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(int(as_stream(RngStream(seed, (1,))).key()[0] & 0x7FFFFFFFFFFFFFFF))
+    density_sup = 1.0 / (model.obs_std * math.sqrt(2.0 * math.pi))
+    raw_sup = resampler.sup_w if resampler.sup_w is not None else density_sup
+    cap_fraction = resampler.sup_v / raw_sup if resampler.sup_v is not None else 0.5
+    x = model.initial_mean + model.initial_std * torch.randn((m_f, n), generator=gen, device=dev, dtype=torch.float64)
+    w = torch.full((m_f, n), 1.0 / n, dtype=torch.float64, device=dev)
+    bound = np.full(m_f, 1.0 / n)
+    means = torch.empty((m_f, t_s), dtype=torch.float64, device=dev)
+    ess = torch.empty((m_f, t_s), dtype=torch.float64, device=dev)
+    resampled = np.zeros((m_f, t_s), dtype=bool)
+    loglik = torch.zeros(m_f, dtype=torch.float64, device=dev)
+    for t in range(t_s):
+        ess[:, t] = 1.0 / (w * w).sum(dim=1)  # compute_ess on normalised weights (diagnostics.py:54-63)
+        need = torch.nonzero(ess[:, t] / n < ess_threshold).flatten().tolist()
+        for m in need:
+            cfg = resampler
+            if resampler.algorithm == "rejection":
+                cfg = replace(resampler, sup_w=float(bound[m]))
+            elif resampler.algorithm == "rejection-capped":
+                cfg = replace(resampler, sup_v=cap_fraction * float(bound[m]))
+            out = resample_ancestors(w[m], cfg, RngStream(seed, (3, m, t)), rng_mode="philox",
+                                     index_dtype=torch.int32)
+            c = permute_parallel(out.ancestors, index_dtype=torch.int32)
+            xm = x[m].contiguous()
+            copy_particles(xm, c)
+            x[m] = xm
+            if out.weights is not None:
+                w[m] = out.weights.to(torch.float64) / n
+                bound[m] = max(1.0, 1.0 / cap_fraction) / n
+            else:
+                w[m] = 1.0 / n
+                bound[m] = 1.0 / n
+            resampled[m, t] = True
+        x = model.coeff * x + model.trans_std * torch.randn((m_f, n), generator=gen, device=dev,
+                                                            dtype=torch.float64)
+        z = (y[:, t: t + 1] - x) / model.obs_std
+        dens = torch.exp(-0.5 * z * z) * density_sup
+        unnorm = w * dens
+        total = unnorm.sum(dim=1)
+        tot = total.cpu().numpy()
+        if L.config.check and (not np.all(np.isfinite(tot)) or np.any(tot <= 0.0)):
+            raise RuntimeError(f"weight collapse at step {t}: all particle weights vanished")
+        loglik += torch.log(total)
+        w = unnorm / total[:, None]
+        bound = bound * min(raw_sup, density_sup) / tot
+        means[:, t] = (w * x).sum(dim=1)
+    return FilterResult(means.cpu().numpy(), loglik.cpu().numpy(), ess.cpu().numpy(), resampled)
+
+
 def deliver_batched(w, rng=None, *, offsets=None, index_dtype=None, return_max_steps: bool = False):
     """Systematic delivery of each row of ``w`` (filters x N): the in-place
     ancestry c[m] of filter m with indices local to the filter, i.e. row-wise
@@ -148,6 +227,15 @@ def deliver_batched(w, rng=None, *, offsets=None, index_dtype=None, return_max_s
     if wt.dim() != 2 or wt.shape[1] < 1:
         raise ValueError("w must be a (filters, N) matrix")
     m_f, n = wt.shape
+    if L.config.check:
+        # check_weights (diagnostics.py:38-51) for every filter's row: finite,
+        # non-negative, and a positive total per row (the reference raises for
+        # each filter; pfr_deliver_batched itself does not validate)
+        st = L.new_status()
+        L.call("pfr_check_weights", wt.data_ptr(), wt.numel(), L.dtype_code(wt), st.data_ptr(), L.stream_handle())
+        L.raise_weight_errors(L.read_status(st) | L.ST_POSITIVE, "w", False)
+        if not bool((wt > 0).any(dim=1).all()):
+            raise ValueError("w must contain at least one strictly positive weight (in every filter's row)")
     c = torch.empty((m_f, n), dtype=torch.int32, device=dev)
     steps = torch.zeros(1, dtype=torch.int32, device=dev) if return_max_steps else None
     off = None

@@ -330,6 +330,16 @@ def test_copy_particles():
     np.testing.assert_array_equal(np_(x)[:, 0], c.astype(np.float64))
 
 
+def test_copy_particles_rejects_bad_ancestry():
+    """an out-of-range c would read outside x; a length mismatch too."""
+    x = torch.zeros(8, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match=r"\[0, 8\)"):
+        pf.copy_particles(x, torch.tensor([0, 1, 2, 3, 4, 5, 6, 9], dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError, match="particles"):
+        pf.copy_particles(torch.zeros(7, dtype=torch.float64, device="cuda"),
+                          torch.arange(8, dtype=torch.int32, device="cuda"))
+
+
 # ---------------------------------------------------------------------------
 # large sizes: size-independent properties
 

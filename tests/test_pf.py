@@ -184,3 +184,49 @@ def test_config5_full_size_against_kalman():
     assert abs(ll.mean() - exact.log_likelihood) < 5 * se + 0.01, (ll.mean(), exact.log_likelihood, se)
     assert np.abs(res.filtered_means.mean(axis=0) - exact.means).max() < 2e-3
     assert 0.2 < res.resampled.mean() < 0.8
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bad, match", [("nan", "finite"), ("neg", "non-negative"), ("zero_row", "positive")])
+def test_deliver_batched_validates_every_row(bad, match):
+    """a row with NaN, negative or all-zero weights raises the
+    reference's ValueError instead of returning a plausible ancestry."""
+    import paper_1301_4019_b200 as pf
+
+    w = np.random.default_rng(3).random((4, 256)) + 0.1
+    if bad == "nan":
+        w[2, 7] = np.nan
+    elif bad == "neg":
+        w[1, 0] = -1.0
+    else:
+        w[3] = 0.0
+    with pytest.raises(ValueError, match=match):
+        pf.deliver_batched(w, offsets=np.full(4, 0.5))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("resampler", ["multinomial", "stratified", "metropolis", "rejection", "rejection-capped"])
+def test_pf_run_every_resampler_tracks_kalman(resampler):
+    """pf_run takes any ResamplerConfig (pf.py:111-204): Metropolis(B),
+    rejection with the tracked weight bound, rejection-capped with carried
+    importance weights, ... -- each filter's log-likelihood and filtered means
+    agree with the exact Kalman recursion within Monte Carlo error."""
+    import paper_1301_4019_b200 as pf
+    from paper_1301_4019_b200.resamplers import ResamplerConfig
+
+    model = LinearGaussianModel(coeff=0.9, trans_std=1.0, obs_std=0.8)
+    y = simulate_observations(model, 25, 11)
+    exact = exact_filter(model, y)
+    # Metropolis: B from the two-state recipe (resamplers.py:350-359); a fixed
+    # small B is biased on peaked weights (the paper's point)
+    cfg = {"rejection-capped": ResamplerConfig("rejection-capped", sup_v=0.25)}.get(resampler,
+                                                                                  ResamplerConfig(resampler))
+    filters, n = 16, 2048
+    res = pf.pf_run(model, y, n, cfg, 0.5, seed=5, filters=filters)
+    assert res.filtered_means.shape == (filters, 25)
+    assert res.resampled.any()
+    ll = res.log_likelihood
+    se = ll.std(ddof=1) / math.sqrt(filters)
+    assert abs(ll.mean() - exact.log_likelihood) < 5 * se + 0.1, (ll.mean(), exact.log_likelihood, se)
+    err = np.abs(res.filtered_means.mean(axis=0) - exact.means)
+    assert err.max() < 0.08, err.max()
