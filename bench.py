@@ -442,7 +442,7 @@ def main():
     alg, dt = dom_name.split("/")
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
             tr = json.load(fh)
         if n == N_DEFAULT and dom_name in tr:
             traffic = float(tr[dom_name]["bytes"])
@@ -595,7 +595,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": dom_name,
                          "algorithmic_bytes": alg_bytes, "kernel_ms": dom_ms, "peak_source": peak_src,
-                         "traffic_source": "profiles/r01_traffic.json (ncu --set full, per launch)",
+                         "traffic_source": "profiles/r02_traffic.json (ncu, per launch)",
                          "note": "algorithmic bytes count every proposal's weight gather (SURVEY 8(d)); the "
                                  "gathers hit L2 (N=2^20 weights are L2 resident): the kernel is bound by the "
                                  "L2 random-sector rate and Philox issue, not by HBM (DESIGN.md 3.3-3.4)"},

@@ -41,10 +41,29 @@ def body(r):
                               ops=CudaShardOps())
 
 
-ts = [threading.Thread(target=body, args=(r,)) for r in range(3)]
-for t in ts:
-    t.start()
-for t in ts:
-    t.join()
+def run3(fn):
+    ts = [threading.Thread(target=fn, args=(r,)) for r in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+
+
+run3(body)
+# the v2 protocol's general fallback (zero halo), and the slot-partitioned
+# multinomial / rejection with the partitioned permute
+os.environ["PFR_SHARD_HALO"] = "0"
+run3(body)
+del os.environ["PFR_SHARD_HALO"]
+
+
+def body2(r):
+    shard = torch.from_numpy(w[cuts[r]: cuts[r + 1]].copy())
+    for alg in ("multinomial", "rejection"):
+        outs[r] = deliver_sharded(shard, pf.ResamplerConfig(alg), pf.RngStream(6), comm=comms[r], ops=CudaShardOps(),
+                                  rng_mode="philox")
+
+
+run3(body2)
 torch.cuda.synchronize()
 print("all rare paths ran", [int(x.numel()) for x in outs])
