@@ -299,32 +299,35 @@ int pfr_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double pr
                         int last_global, int stratified, double offset, const double* uniforms, const pfr_rng* rng,
                         int32_t* O, void* stream);
 
-/* Protocol v2 of the weight-sharded systematic / stratified delivery (no
- * host round trip before the final status exchange; sharded.py):
- * pfr_shard_offspring_dev is pfr_shard_offspring with prefix_total = {weight
- * before the shard, W_N} read on the device, and o_before = the O of the
- * element before the shard (the previous shard's last O; 0 for the first). */
-int pfr_shard_offspring_dev(const double* W_loc, int64_t n_loc, int dtype, const double* prefix_total,
-                            int64_t n_global, int last_global, int first_global, int stratified, double offset,
-                            const double* uniforms, const pfr_rng* rng, int32_t* O, int32_t* o_before, void* stream);
-/* The shard's slot words (parent | FIRST) written into the EXTENDED array
- * ext[n_loc + 2*halo] covering slots [index_base - halo, index_base + n_loc +
- * halo) (sentinel 0xFFFFFFFF elsewhere), and has[i] = o_i > 0.  A slot of the
- * window outside that range sets PFR_ST_OVERFLOW. */
-int pfr_shard_ext_words(const int32_t* O_loc, int64_t n_loc, int64_t index_base, const int32_t* o_before, int64_t halo,
-                        uint32_t* ext, uint8_t* has, uint32_t* status, void* stream);
+/* Protocol v3 of the weight-sharded systematic / stratified delivery
+ * (sharded.py): the shard's local work through the single-GPU kernels.
+ * pfr_shard_local_end: the shard's float64 weight hierarchy (check_weights'
+ * flags into status) and its END value -- W at its last element in the
+ * delivery's association -- into *end (device), the value the next shard's
+ * prefix adds.  pfr_shard_produce: O of the shard's parents in global slot
+ * numbers with prefix_total = {weight before the shard (a left fold of the
+ * END values in rank order), W_N} read on the device, and their slot words
+ * (global parents) written to ext[slot - slot_lo] for slots in [slot_lo,
+ * slot_hi) (ext is set to 0xFFFFFFFF first; a slot outside sets
+ * PFR_ST_OVERFLOW).  pfr_shard_resolve_fast: the in-place ancestry of the
+ * shard's indices from ext (after the neighbours' bands are merged in,
+ * pfr_shard_merge_bands), c indexed locally, values global; a chain leaving
+ * the window sets PFR_ST_OVERFLOW.  The three share one workspace. */
+int pfr_shard_local_end(const void* w_loc, int64_t n_loc, int dtype, double* end, uint32_t* status, void* ws,
+                        size_t ws_bytes, void* stream);
+int pfr_shard_produce(const void* w_loc, int64_t n_loc, int dtype, int64_t index_base, int64_t n_global,
+                      const double* prefix_total, int first, int last, int stratified, double offset,
+                      const double* uniforms, const pfr_rng* rng, uint32_t* ext, int64_t slot_lo, int64_t slot_hi,
+                      uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+int pfr_shard_resolve_fast(int64_t n_loc, int dtype, int64_t index_base, const uint32_t* ext, int64_t slot_lo,
+                           int64_t slot_hi, int32_t* c, int32_t* max_steps, uint32_t* status, void* ws,
+                           size_t ws_bytes, void* stream);
+
 /* Fill ext's sentinels from the neighbours' boundary bands: from_left = the
  * left neighbour's ext[n, n + 2*halo), from_right = the right neighbour's
  * ext[0, 2*halo) (null at the ends of the rank order). */
 int pfr_shard_merge_bands(uint32_t* ext, int64_t n_loc, int64_t halo, const uint32_t* from_left,
                           const uint32_t* from_right, void* stream);
-/* The in-place ancestry of the shard's indices (ancestry.py:139-174 read
- * backwards from each hole) with every chain inside ext; a missing word or a
- * chain leaving ext sets PFR_ST_OVERFLOW (the caller reruns the general
- * protocol). */
-int pfr_shard_resolve_ext(const uint32_t* ext, int64_t n_loc, int64_t halo, const uint8_t* has, int64_t index_base,
-                          int32_t* c, int32_t* max_steps, uint32_t* status, void* stream);
-
 /* Slot words of the shard's slot window [o_begin, O[n_loc-1]):
  * words[s - o_begin] = parent | 0x80000000 on a parent's first slot
  * (cumulative_offspring_to_ancestors, ancestry.py:69-76, + prepermute's

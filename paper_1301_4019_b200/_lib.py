@@ -85,10 +85,11 @@ _SIGNATURES = {
     "pfr_check_predicate": ([_P, _I64, _INT, _P, _P, _P, _SZ, _P], _INT),
     "pfr_copy_particles": ([_P, _I64, _I64, _P, _P], _INT),
     "pfr_metropolis_range": ([_P, _I64, _INT, _I64, _RNGP, _I64, _I64, _P, _P, _P], _INT),
-    "pfr_shard_offspring_dev": ([_P, _I64, _INT, _P, _I64, _INT, _INT, _INT, _DBL, _P, _RNGP, _P, _P, _P], _INT),
-    "pfr_shard_ext_words": ([_P, _I64, _I64, _P, _I64, _P, _P, _P, _P], _INT),
     "pfr_shard_merge_bands": ([_P, _I64, _I64, _P, _P, _P], _INT),
-    "pfr_shard_resolve_ext": ([_P, _I64, _I64, _P, _I64, _P, _P, _P, _P], _INT),
+    "pfr_shard_local_end": ([_P, _I64, _INT, _P, _P, _P, _SZ, _P], _INT),
+    "pfr_shard_produce": ([_P, _I64, _INT, _I64, _I64, _P, _INT, _INT, _INT, _DBL, _P, _RNGP, _P, _I64, _I64, _P, _P,
+                           _SZ, _P], _INT),
+    "pfr_shard_resolve_fast": ([_I64, _INT, _I64, _P, _I64, _I64, _P, _P, _P, _P, _SZ, _P], _INT),
     "pfr_multinomial_range": ([_P, _I64, _INT, _INT, _RNGP, _P, _I64, _I64, _P, _P, _P, _SZ, _P], _INT),
     "pfr_permute_range": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _SZ, _P], _INT),
     "pfr_shard_offspring": ([_P, _I64, _INT, _DBL, _DBL, _I64, _INT, _INT, _DBL, _P, _RNGP, _P, _P], _INT),

@@ -476,25 +476,46 @@ int pfr_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double pr
   return PFR_OK;
 }
 
-int pfr_shard_offspring_dev(const double* W_loc, int64_t n_loc, int dtype, const double* prefix_total,
-                            int64_t n_global, int last_global, int first_global, int stratified, double offset,
-                            const double* uniforms, const pfr_rng* rng, int32_t* O, int32_t* o_before, void* stream) {
-  PFR_REQUIRE(valid_n(n_loc) && valid_n(n_global) && n_loc <= n_global, "bad sizes");
-  PFR_REQUIRE(W_loc && prefix_total && O && o_before, "null array");
+int pfr_shard_local_end(const void* w_loc, int64_t n_loc, int dtype, double* end, uint32_t* status, void* ws_ptr,
+                        size_t ws_bytes, void* stream) {
+  const int64_t n = n_loc;
+  PFR_REQUIRE(valid_n(n) && w_loc && end && status, "bad arguments");
   PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
-  if (stratified) PFR_REQUIRE(uniforms || rng, "stratified needs uniforms or an rng");
-  PFR_CHECK_LAUNCH(launch_shard_offspring_dev(W_loc, n_loc, dtype, prefix_total, n_global, last_global, first_global,
-                                              stratified, offset, uniforms, rng, O, o_before, (cudaStream_t)stream),
-                   "pfr_shard_offspring_dev");
+  PFR_WS(PFR_OP_DELIVER);
+  PFR_CHECK_LAUNCH(launch_shard_local_end(w_loc, n, dtype, status, end, ws, (cudaStream_t)stream),
+                   "pfr_shard_local_end");
   return PFR_OK;
 }
 
-int pfr_shard_ext_words(const int32_t* O_loc, int64_t n_loc, int64_t index_base, const int32_t* o_before, int64_t halo,
-                        uint32_t* ext, uint8_t* has, uint32_t* status, void* stream) {
-  PFR_REQUIRE(valid_n(n_loc) && index_base >= 0 && halo >= 0, "bad sizes");
-  PFR_REQUIRE(O_loc && o_before && ext && has && status, "null array");
-  PFR_CHECK_LAUNCH(launch_shard_ext(O_loc, n_loc, index_base, o_before, halo, ext, has, status, (cudaStream_t)stream),
-                   "pfr_shard_ext_words");
+int pfr_shard_produce(const void* w_loc, int64_t n_loc, int dtype, int64_t index_base, int64_t n_global,
+                      const double* prefix_total, int first, int last, int stratified, double offset,
+                      const double* uniforms, const pfr_rng* rng, uint32_t* ext, int64_t slot_lo, int64_t slot_hi,
+                      uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
+  const int64_t n = n_loc;
+  PFR_REQUIRE(valid_n(n) && valid_n(n_global) && index_base >= 0 && index_base + n <= n_global, "bad sizes");
+  PFR_REQUIRE(w_loc && prefix_total && ext && status, "null array");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(slot_hi > slot_lo && (slot_lo & 3) == 0 && slot_lo <= index_base && slot_hi >= index_base + n,
+              "the slot window must cover the shard's indices and start at a multiple of 4");
+  if (stratified) PFR_REQUIRE(uniforms || rng, "stratified needs uniforms or an rng");
+  PFR_WS(PFR_OP_DELIVER);
+  PFR_CHECK_LAUNCH(launch_shard_produce(w_loc, n, dtype, index_base, n_global, prefix_total, first, last, stratified,
+                                        offset, uniforms, rng, ext, slot_lo, slot_hi, status, ws,
+                                        (cudaStream_t)stream),
+                   "pfr_shard_produce");
+  return PFR_OK;
+}
+
+int pfr_shard_resolve_fast(int64_t n_loc, int dtype, int64_t index_base, const uint32_t* ext, int64_t slot_lo,
+                           int64_t slot_hi, int32_t* c, int32_t* max_steps, uint32_t* status, void* ws_ptr,
+                           size_t ws_bytes, void* stream) {
+  const int64_t n = n_loc;
+  PFR_REQUIRE(valid_n(n) && index_base >= 0 && ext && c && status, "bad arguments");
+  PFR_REQUIRE(slot_lo <= index_base && slot_hi >= index_base + n, "the slot window must cover the shard's indices");
+  PFR_WS(PFR_OP_DELIVER);
+  PFR_CHECK_LAUNCH(launch_shard_resolve_fast(n, dtype, index_base, ext, slot_lo, slot_hi, c, max_steps, status, ws,
+                                             (cudaStream_t)stream),
+                   "pfr_shard_resolve_fast");
   return PFR_OK;
 }
 
@@ -505,16 +526,6 @@ int pfr_shard_merge_bands(uint32_t* ext, int64_t n_loc, int64_t halo, const uint
   if (halo == 0 || (!from_left && !from_right)) return PFR_OK;
   PFR_CHECK_LAUNCH(launch_shard_merge(ext, n_loc, halo, from_left, from_right, (cudaStream_t)stream),
                    "pfr_shard_merge_bands");
-  return PFR_OK;
-}
-
-int pfr_shard_resolve_ext(const uint32_t* ext, int64_t n_loc, int64_t halo, const uint8_t* has, int64_t index_base,
-                          int32_t* c, int32_t* max_steps, uint32_t* status, void* stream) {
-  PFR_REQUIRE(valid_n(n_loc) && halo >= 0 && index_base >= 0, "bad sizes");
-  PFR_REQUIRE(ext && has && c && status, "null array");
-  PFR_CHECK_LAUNCH(launch_shard_resolve_ext(ext, n_loc, halo, has, index_base, c, max_steps, status,
-                                            (cudaStream_t)stream),
-                   "pfr_shard_resolve_ext");
   return PFR_OK;
 }
 

@@ -80,6 +80,14 @@ struct DvArgs {
   int32_t* O;        // [n]
   int64_t* tmax;     // [tiles]
   int32_t *d, *J0, *J1, *R0, *R1;
+  // one weight shard of a larger vector (sharded.py protocol v3); the single
+  // GPU path has gn = n, gpt = null, gbase = 0, words covering [0, n)
+  int64_t gn;        // N of the offspring formula (the global N)
+  const double* gpt; // non-null: {weight before this shard, W_N} on the device
+  int glast;         // the shard holds the global last particle (O[N-1] = N)
+  int gfirst;        // the shard starts at particle 0
+  int64_t gbase;     // global index of local element 0 (parents and slots are global)
+  int64_t wlo, whi;  // `words` holds slots [wlo, whi) at words[slot - wlo]; outside -> PFR_ST_OVERFLOW
 };
 
 // ---------------------------------------------------------------------------
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(kTileThreads) k_dv_reduce(DvArgs<A> p) {
 // element of subtile s-1 (0 for s = 0), uniform.  One warp, no block barrier;
 // every prefix value is fetched by one lane, all in one round trip with the
 // weights.
-template <typename T, typename A, int UM>
+template <typename T, typename A, int UM, bool kShard = false>
 __device__ __forceinline__ void subtile_offspring(const DvArgs<A>& p, int64_t s, int32_t (&o)[kTileItems],
                                                   int32_t& o_prev) {
   const int lane = threadIdx.x & 31;
@@ -348,7 +356,19 @@ __device__ __forceinline__ void subtile_offspring(const DvArgs<A>& p, int64_t s,
     for (int i = 8; i < 15; ++i) Qp = add_rn(Qp, __shfl_sync(0xffffffffu, v, i));
     wprev = add_rn(add_rn(tep, Qp), __shfl_sync(0xffffffffu, v, 15));
   }
-  const A total = __shfl_sync(0xffffffffu, v, 20);
+  // sharded: W of the global vector = (weight before the shard) + local W
+  constexpr bool shard = kShard;
+  A gp = A(0), total = __shfl_sync(0xffffffffu, v, 20);
+  if constexpr (shard) {
+    gp = (A)__ldcg(p.gpt);
+    total = (A)__ldcg(p.gpt + 1);
+  }
+  auto globalW = [&](A wl) {
+    if constexpr (shard)
+      return add_rn(gp, wl);
+    else
+      return wl;
+  };
   // the lane's serial partials and the Kogge-Stone exclusive offset; when the
   // weights are narrower than the accumulator the partials are recomputed in
   // the second loop (the same sequence) instead of being kept in registers
@@ -358,32 +378,40 @@ __device__ __forceinline__ void subtile_offspring(const DvArgs<A>& p, int64_t s,
   const A incl = warp_inclusive_scan(tot);
   A tex = __shfl_up_sync(0xffffffffu, incl, 1);
   if (lane == 0) tex = A(0);
-  const FxParams fx = fx_params<A>(p.n, total, p.u_sys, p.fx_S);
+  const int64_t gn = shard ? p.gn : p.n;
+  const FxParams fx = fx_params<A>(gn, total, p.u_sys, p.fx_S);
   const double csys = 4503599627370496.0 + (double)fx.ufx;  // 2^52 + ufx (exact)
-  const int32_t nn = (int32_t)p.n;
+  const int32_t gN = (int32_t)gn;
   A loc = A(0);
   uint32_t unsafe = 0;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
     loc = j ? add_rn(loc, (A)x[j]) : (A)x[0];
     bool u;
-    o[j] = offspring_fast<T, A, UM>(add_rn(SP, add_rn(tex, loc)), fx, csys, nn, u, p);
+    o[j] = offspring_fast<T, A, UM>(globalW(add_rn(SP, add_rn(tex, loc))), fx, csys, gN, u, p);
     unsafe |= (uint32_t)u << j;
   }
   if (__any_sync(0xffffffffu, unsafe)) {  // rare: the reference's exact IEEE sequence
     loc = A(0);
     for (int j = 0; j < kTileItems; ++j) {
       loc = j ? add_rn(loc, (A)x[j]) : (A)x[0];
-      if ((unsafe >> j) & 1u) o[j] = offspring_exact<T, A, UM>(add_rn(SP, add_rn(tex, loc)), total, p.n, p);
+      if ((unsafe >> j) & 1u)
+        o[j] = offspring_exact<T, A, UM>(globalW(add_rn(SP, add_rn(tex, loc))), total, gn, p);
     }
   }
-  if (e0 + kTileItems > p.n - 1) {  // the final subtile: O[N-1] = N, padding past N stays at N
+  // the final subtile of the global vector: O[N-1] = N, padding past N stays
+  // at N (a shard that is not last needs nothing: its zero padding repeats
+  // the last O)
+  if ((!shard || p.glast) && e0 + kTileItems > p.n - 1) {
     const int64_t lim = p.n - 1 - e0;
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j)
-      if (j >= lim) o[j] = nn;
+      if (j >= lim) o[j] = gN;
   }
-  o_prev = s > 0 ? offspring_of<T, A, UM>(wprev, total, fx, p.n, p) : 0;
+  if (s > 0)
+    o_prev = offspring_of<T, A, UM>(globalW(wprev), total, fx, gn, p);
+  else  // before the shard W is exactly the weight before it (sharded.py)
+    o_prev = (shard && !p.gfirst) ? offspring_of<T, A, UM>(gp, total, fx, gn, p) : 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -543,12 +571,18 @@ struct __align__(16) WarpSmem {
 // XOR-swizzled in 16-byte units so the per-lane vector accesses are
 // bank-conflict free.
 __device__ __forceinline__ int sw_hd(int v) { return v ^ ((v >> 3) & 3); }  // 16-byte unit swizzle
-__device__ __forceinline__ void subtile_expand(const int32_t (&o)[kTileItems], int32_t prev_l, int32_t o_prev,
+template <bool kShard = false>
+__device__ __forceinline__ bool subtile_expand(const int32_t (&o)[kTileItems], int32_t prev_l, int32_t o_prev,
                                                int32_t oend, int64_t s, int64_t n, uint32_t* __restrict__ words,
-                                               uint32_t* __restrict__ bitmap, WarpSmem& W) {
+                                               uint32_t* __restrict__ bitmap, WarpSmem& W, int64_t gbase = 0,
+                                               int64_t wlo = 0, int64_t whi = INT64_MAX) {
+  // words[slot - wlo] for slots in [wlo, whi); parents are written as global
+  // numbers gbase + local index; returns false when a slot fell outside
+  // (a shard whose window overhangs its halo: the caller falls back)
   const int lane = threadIdx.x & 31;
   const int64_t base = s * kSub;
   const int64_t e0 = base + (int64_t)lane * kTileItems;
+  bool outside = false;
   uint32_t bits = 0;
 #pragma unroll
   for (int j = 0; j < kTileItems; ++j) {
@@ -557,10 +591,10 @@ __device__ __forceinline__ void subtile_expand(const int32_t (&o)[kTileItems], i
   }
   const uint32_t hi = __shfl_down_sync(0xffffffffu, bits, 1);
   if ((lane & 1) == 0 && e0 < n) bitmap[(base >> 5) + (lane >> 1)] = bits | (hi << 16);
-  if (oend <= o_prev) return;  // uniform: no slots
+  if (oend <= o_prev) return true;  // uniform: no slots
   int32_t* hb = reinterpret_cast<int32_t*>(W.buf);
   int4* hb4 = reinterpret_cast<int4*>(W.buf);
-  const int pb = (int)e0;  // global index of the lane's first parent
+  const int pb = (int)(gbase + e0);  // global index of the lane's first parent
   int carry = -1;
   // chunks of kWBuf = 1024 positions (a typical subtile's ~512 slots fit one
   // chunk whatever their alignment), scanned as up to two rows of 512
@@ -611,23 +645,32 @@ __device__ __forceinline__ void subtile_expand(const int32_t (&o)[kTileItems], i
         }
       }
       const int s0 = c0 + kSub * row + lane * kTileItems;
-      if (s0 >= o_prev && s0 + kTileItems <= oend) {
-        uint4* dst = reinterpret_cast<uint4*>(words + s0);
+      if (s0 >= o_prev && s0 + kTileItems <= oend && (!kShard || (s0 >= wlo && s0 + kTileItems <= whi))) {
+        uint4* dst = reinterpret_cast<uint4*>(words + (s0 - wlo));
 #pragma unroll
         for (int q = 0; q < kTileItems / 4; ++q)
           dst[q] = make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
       } else if (s0 < oend && s0 + kTileItems > o_prev) {
-        for (int t = 0; t < kTileItems; ++t)
-          if (s0 + t >= o_prev && s0 + t < oend) words[s0 + t] = wv[t];
+        for (int t = 0; t < kTileItems; ++t) {
+          const int64_t sl = s0 + t;
+          if (sl >= o_prev && sl < oend) {
+            if (!kShard || (sl >= wlo && sl < whi))
+              words[sl - wlo] = wv[t];
+            else
+              outside = true;
+          }
+        }
       }
     }
     __syncwarp();
   }
+  if constexpr (kShard) return !__any_sync(0xffffffffu, outside);
+  return true;
 }
 
 // K2w: produce every subtile (grid-stride): O from the position formula,
 // the slot words of the subtile's slot range and its has-offspring bitmap.
-template <typename T, typename A, int UM>
+template <typename T, typename A, int UM, bool kShard = false>
 __global__ void __launch_bounds__(kFWarps * 32, 3) k_dv_produce(DvArgs<A> p) {
   extern __shared__ __align__(16) unsigned char fused_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -638,15 +681,19 @@ __global__ void __launch_bounds__(kFWarps * 32, 3) k_dv_produce(DvArgs<A> p) {
   for (int64_t k = blockIdx.x * (int64_t)kFWarps + warp; k < nS; k += (int64_t)gridDim.x * kFWarps) {
     int32_t o[kTileItems];
     int32_t o_prev;
-    subtile_offspring<T, A, UM>(p, k, o, o_prev);
+    subtile_offspring<T, A, UM, kShard>(p, k, o, o_prev);
     int32_t prev_l = __shfl_up_sync(0xffffffffu, o[kTileItems - 1], 1);
     if (lane == 0) prev_l = o_prev;
     const bool bad = __any_sync(0xffffffffu, o[0] < prev_l);
     const int32_t oend = __shfl_sync(0xffffffffu, o[kTileItems - 1], 31);
-    if (!bad)
-      subtile_expand(o, prev_l, o_prev, oend, k, n, p.words, p.bitmap, W);
-    else if (lane == 0)
+    if (!bad) {
+      if (!subtile_expand<kShard>(o, prev_l, o_prev, oend, k, n, p.words, p.bitmap, W, p.gbase, p.wlo, p.whi) &&
+          lane == 0)
+        status_or(p.status, PFR_ST_OVERFLOW);  // a shard's window beyond its halo (sharded.py falls back)
+    } else if (lane == 0) {
       atomicOr(&p.state->flags, kNeedsRepair);
+      if (kShard) status_or(p.status, PFR_ST_OVERFLOW);  // a shard has no repair path: the host falls back
+    }
   }
 }
 
@@ -659,9 +706,14 @@ struct ResolveQ {
 };
 
 // One step for every queued chain when every word is written: dense, eight
-// loads per lane in flight, survivors compacted to the front.
+// loads per lane in flight, survivors compacted to the front.  Entries are
+// (local hole, global slot); words are indexed by global slot and exist for
+// [wlo, whi) only (a shard's halo: a chain leaving it sets the overflow flag
+// and the host falls back).
+template <bool kShard = false>
 __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const uint32_t* __restrict__ words,
-                                         int32_t* __restrict__ c, uint32_t n, int& longest, bool& overflow) {
+                                         int32_t* __restrict__ c, int64_t wlo, int64_t whi, int64_t gbase,
+                                         int& longest, bool& overflow) {
   constexpr int K = 8;
   int out = 0;
   for (int b = 0; b < qlen; b += 32 * K) {
@@ -674,7 +726,8 @@ __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const 
       if (e < qlen) {
         xz[i] = Q.xz[e];
         st[i] = Q.st[e] + 1;
-        w[i] = __ldcg(words + xz[i].y);
+        const int64_t z = xz[i].y;
+        w[i] = (!kShard || (z >= wlo && z < whi)) ? __ldcg(words + z) : 0xFFFFFFFFu;
       }
     }
     __syncwarp();
@@ -685,10 +738,12 @@ __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const 
       bool keep = false;
       if (valid) {
         const uint32_t par = w[i] & kParentMask;
-        if (!(w[i] & kFirst)) {
+        if (kShard && w[i] == 0xFFFFFFFFu) {
+          overflow = true;  // outside the shard's halo (or an unwritten word): the host falls back
+        } else if (!(w[i] & kFirst)) {
           c[xz[i].x] = (int32_t)par;
           longest = max(longest, st[i]);
-        } else if (st[i] >= kBackBound || par >= n) {
+        } else if (st[i] >= kBackBound || (kShard && (int64_t)par >= whi)) {
           overflow = true;  // abandoned: the rare-path kernel resolves every chain
         } else {
           keep = true;
@@ -704,6 +759,7 @@ __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const 
     }
     __syncwarp();
   }
+  (void)gbase;
   return out;
 }
 
@@ -715,7 +771,7 @@ __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const 
 // pass, a pass running once enough chains wait -- so a pass costs one L2
 // round trip for several subtiles' chains, overlapped with the next
 // subtile's prefetched loads.
-template <typename T, typename A, int UM>
+template <typename T, typename A, int UM, bool kShard = false>
 __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
   extern __shared__ __align__(16) unsigned char fused_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -727,8 +783,13 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
   const int64_t nS = (n + kSub - 1) / kSub;
   int qlen = 0, longest = 0;
   bool overflow = false;
-  auto pass = [&]() { return lean_pass(Q, lane, qlen, p.words, p.c, nn, longest, overflow); };
-  const uint4* __restrict__ words4 = reinterpret_cast<const uint4*>(p.words);
+  // slot / parent numbers are global (gbase + local index) and words[slot -
+  // wlo] covers [wlo, whi): the single-GPU call has gbase = wlo = 0, whi = n
+  const int64_t gbase = kShard ? p.gbase : 0, wlo = kShard ? p.wlo : 0, whi = kShard ? p.whi : p.n;
+  const uint32_t* __restrict__ wds = p.words - wlo;  // indexed by global slot (only inside [wlo, whi))
+  auto pass = [&]() { return lean_pass<kShard>(Q, lane, qlen, wds, p.c, wlo, whi, gbase, longest, overflow); };
+  const bool vec_ok = !kShard || ((gbase - wlo) & 3) == 0;  // 16-byte word loads need a 4-aligned offset
+  const uint4* __restrict__ words4 = reinterpret_cast<const uint4*>(p.words + (gbase - wlo));
   int4* __restrict__ c4 = reinterpret_cast<int4*>(p.c);
   const int64_t stride = (int64_t)gridDim.x * kFWarps;
   auto load = [&](int64_t rr, uint4 (&wv)[4], uint32_t (&bm)[4]) {
@@ -736,13 +797,14 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint32_t x0 = xb + 128 * q + 4 * lane;
-      if (xb + kSub <= nn) {
+      if (xb + kSub <= nn && vec_ok) {
         wv[q] = __ldg(words4 + (x0 >> 2));
       } else {
-        wv[q].x = x0 < nn ? __ldg(p.words + x0) : 0u;
-        wv[q].y = x0 + 1 < nn ? __ldg(p.words + x0 + 1) : 0u;
-        wv[q].z = x0 + 2 < nn ? __ldg(p.words + x0 + 2) : 0u;
-        wv[q].w = x0 + 3 < nn ? __ldg(p.words + x0 + 3) : 0u;
+        const uint32_t* wx = p.words + (gbase - wlo) + x0;
+        wv[q].x = x0 < nn ? __ldg(wx) : 0u;
+        wv[q].y = x0 + 1 < nn ? __ldg(wx + 1) : 0u;
+        wv[q].z = x0 + 2 < nn ? __ldg(wx + 2) : 0u;
+        wv[q].w = x0 + 3 < nn ? __ldg(wx + 3) : 0u;
       }
       bm[q] = x0 < nn ? __ldg(p.bitmap + (x0 >> 5)) >> (x0 & 31) : 0u;
     }
@@ -753,7 +815,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
   if (rr < nS) load(rr, nwv, nbm);
   for (; rr < nS; rr += stride) {
     const uint32_t xb = (uint32_t)rr * kSub;
-    const bool full = xb + kSub <= nn;
+    const bool full = xb + kSub <= nn && vec_ok;
     uint4 wv[4];
     uint32_t bm[4];
 #pragma unroll
@@ -771,7 +833,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const bool has = (bm[q] >> t) & 1u;
-        o[t] = has ? (int32_t)(x0 + t) : (int32_t)(e[t] & kParentMask);
+        o[t] = has ? (int32_t)(gbase + x0 + t) : (int32_t)(e[t] & kParentMask);
         if (!has && (e[t] & kFirst) && x0 + t < nn) pend |= 1u << (4 * q + t);
       }
       // pending holes get a placeholder, overwritten when their chain
@@ -801,7 +863,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         if ((pend >> (4 * q + t)) & 1u) {
-          Q.xz[pos] = make_uint2(xb + 128 * q + 4 * lane + t, e[t] & kParentMask);
+          Q.xz[pos] = make_uint2(xb + 128 * q + 4 * lane + t, e[t] & kParentMask);  // (local hole, global slot)
           Q.st[pos] = 0;
           ++pos;
         }
@@ -1127,10 +1189,153 @@ DvArgs<A> make_args(const void* w, int64_t n, double offset, const double* unifo
   p.R0 = ws.r0;
   p.R1 = ws.r1;
   p.sub = reinterpret_cast<A*>(ws.sub_cells);
+  p.gn = n;
+  p.gpt = nullptr;
+  p.glast = 1;
+  p.gfirst = 1;
+  p.gbase = 0;
+  p.wlo = 0;
+  p.whi = n;
   return p;
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// Weight-sharded delivery, protocol v3 (sharded.py): the shard's local work
+// through the single-GPU kernels.  K1 builds the shard's hierarchy; the
+// shard's END value (W at its last element in the subtile association,
+// SP(last) + sub(last)) is what the next shard's prefix adds, so the previous
+// shard's last O and this shard's O(before) are computed from the same IEEE
+// sum.  K2w writes the slot words of the shard's window into the extended
+// array words[slot - wlo], K3w resolves the shard's indices from it.
+
+template <typename A>
+__global__ void k_shard_end(DvArgs<A> p, double* out) {
+  const int64_t nS = (p.n + kSub - 1) / kSub;
+  const int64_t s = nS - 1;
+  const int64_t b = s >> 3;
+  const int q = (int)(s & 7);
+  const Hier<A> h = hier_of(p);
+  if (threadIdx.x != 0) return;
+  A Q = A(0);
+  for (int i = 0; i < q; ++i) Q = add_rn(Q, __ldcg(p.sub + b * kSubPerTile + i));
+  const A SP = add_rn(h.tile_excl(b), Q);
+  *out = (double)add_rn(SP, __ldcg(p.sub + s));
+}
+
+namespace {
+template <typename T>
+cudaError_t shard_local_end_t(const void* w, int64_t n, uint32_t* status, double* end, const Workspace& ws,
+                              cudaStream_t s) {
+  auto p = make_args<T, double>(w, n, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, status, ws);
+  k_dv_reduce<T, double, 1, false><<<(unsigned)p.tiles, kTileThreads, 0, s>>>(p);
+  note_launch();
+  k_shard_end<double><<<1, 32, 0, s>>>(p, end);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <typename T, int UM>
+cudaError_t shard_produce_t(DvArgs<double> p, cudaStream_t s) {
+  const int smem = (int)(sizeof(WarpSmem) * kFWarps);
+  static int occ = -1;
+  if (occ < 0) {
+    cudaError_t e = cudaFuncSetAttribute(k_dv_produce<T, double, UM, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dv_produce<T, double, UM, true>, kFWarps * 32, smem);
+    occ = max(occ, 1);
+  }
+  const int64_t subs = (p.n + kSub - 1) / kSub;
+  const int64_t g = max((int64_t)1, min((int64_t)num_sms() * occ, (subs + kFWarps - 1) / kFWarps));
+  k_dv_produce<T, double, UM, true><<<(unsigned)g, kFWarps * 32, smem, s>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t shard_resolve_t(DvArgs<double> p, cudaStream_t s) {
+  const int smem = (int)(sizeof(ResolveQ) * kFWarps);
+  static int occ = -1;
+  if (occ < 0) {
+    cudaError_t e = cudaFuncSetAttribute(k_dv_resolve<T, double, kUSys, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dv_resolve<T, double, kUSys, true>, kFWarps * 32, smem);
+    occ = max(occ, 1);
+  }
+  const int64_t subs = (p.n + kSub - 1) / kSub;
+  const int64_t g = max((int64_t)1, min((int64_t)num_sms() * occ, (subs + kFWarps - 1) / kFWarps));
+  k_dv_resolve<T, double, kUSys, true><<<(unsigned)g, kFWarps * 32, smem, s>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <typename T>
+DvArgs<double> shard_args(const void* w, int64_t n_loc, int64_t base, int64_t n_global, const double* pt, int first,
+                          int last, double offset, const double* uniforms, const pfr_rng* rng, uint32_t* ext,
+                          int64_t wlo, int64_t whi, int32_t* c, int32_t* max_steps, uint32_t* status,
+                          const Workspace& ws) {
+  auto p = make_args<T, double>(w, n_loc, offset, uniforms, rng, c, nullptr, max_steps, status, ws);
+  p.gn = n_global;
+  p.fx_S = fx_bits(n_global);
+  p.gpt = pt;
+  p.gfirst = first;
+  p.glast = last;
+  p.gbase = base;
+  p.wlo = wlo;
+  p.whi = whi;
+  p.words = ext;
+  return p;
+}
+}  // namespace
+
+cudaError_t launch_shard_local_end(const void* w, int64_t n, int dtype, uint32_t* status, double* end,
+                                   const Workspace& ws, cudaStream_t s) {
+  if (dtype == PFR_F64) return shard_local_end_t<double>(w, n, status, end, ws, s);
+  return shard_local_end_t<float>(w, n, status, end, ws, s);
+}
+
+cudaError_t launch_shard_produce(const void* w, int64_t n_loc, int dtype, int64_t base, int64_t n_global,
+                                 const double* pt, int first, int last, int stratified, double offset,
+                                 const double* uniforms, const pfr_rng* rng, uint32_t* ext, int64_t wlo, int64_t whi,
+                                 uint32_t* status, const Workspace& ws, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(ext, 0xFF, (size_t)(whi - wlo) * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  const int mode = !stratified ? kUSys : uniforms ? kUArr : (rng && rng->mode == PFR_RNG_NUMPY) ? kUNp : kUPh;
+  auto run = [&](auto tag) -> cudaError_t {
+    using T = decltype(tag);
+    auto p = shard_args<T>(w, n_loc, base, n_global, pt, first, last, offset, uniforms, rng, ext, wlo, whi, nullptr,
+                           nullptr, status, ws);
+    switch (mode) {
+      case kUSys: return shard_produce_t<T, kUSys>(p, s);
+      case kUArr: return shard_produce_t<T, kUArr>(p, s);
+      case kUNp: return shard_produce_t<T, kUNp>(p, s);
+      default: return shard_produce_t<T, kUPh>(p, s);
+    }
+  };
+  return dtype == PFR_F64 ? run(double(0)) : run(float(0));
+}
+
+cudaError_t launch_shard_resolve_fast(int64_t n_loc, int dtype, int64_t base, const uint32_t* ext, int64_t wlo,
+                                      int64_t whi, int32_t* c, int32_t* max_steps, uint32_t* status,
+                                      const Workspace& ws, cudaStream_t s) {
+  if (max_steps) {
+    cudaError_t e = cudaMemsetAsync(max_steps, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+  }
+  // the state flags must not carry a repair request into the resolve (K1 of
+  // this shard cleared them; a shard needing repair already reported overflow)
+  if (dtype == PFR_F64)
+    return shard_resolve_t<double>(shard_args<double>(nullptr, n_loc, base, 0, nullptr, 0, 0, 0.0, nullptr, nullptr,
+                                                      const_cast<uint32_t*>(ext), wlo, whi, c, max_steps, status,
+                                                      ws),
+                                   s);
+  return shard_resolve_t<float>(shard_args<float>(nullptr, n_loc, base, 0, nullptr, 0, 0, 0.0, nullptr, nullptr,
+                                                   const_cast<uint32_t*>(ext), wlo, whi, c, max_steps, status, ws),
+                                s);
+}
 
 // K3 on its own, for callers that wrote slot words and the has-offspring
 // bitmap themselves (the batched filter: global parent numbers, so one pass

@@ -120,17 +120,17 @@ cudaError_t launch_rejection_replay(const void* w, int64_t n, int dtype, double 
 cudaError_t launch_shard_offspring(const double* W_loc, int64_t n_loc, int dtype, double prefix, double total,
                                    int64_t n_global, int last_global, int stratified, double offset,
                                    const double* uniforms, const pfr_rng* rng, int32_t* O, cudaStream_t s);
-cudaError_t launch_shard_offspring_dev(const double* W_loc, int64_t n_loc, int dtype, const double* prefix_total,
-                                       int64_t n_global, int last_global, int first_global, int stratified,
-                                       double offset, const double* uniforms, const pfr_rng* rng, int32_t* O,
-                                       int32_t* o_before, cudaStream_t s);
-cudaError_t launch_shard_ext(const int32_t* O, int64_t n_loc, int64_t index_base, const int32_t* o_before, int64_t H,
-                             uint32_t* ext, uint8_t* has, uint32_t* status, cudaStream_t s);
 cudaError_t launch_shard_merge(uint32_t* ext, int64_t n_loc, int64_t H, const uint32_t* from_left,
                                const uint32_t* from_right, cudaStream_t s);
-cudaError_t launch_shard_resolve_ext(const uint32_t* ext, int64_t n_loc, int64_t H, const uint8_t* has,
-                                     int64_t index_base, int32_t* c, int32_t* max_steps, uint32_t* status,
-                                     cudaStream_t s);
+cudaError_t launch_shard_local_end(const void* w, int64_t n, int dtype, uint32_t* status, double* end,
+                                   const Workspace& ws, cudaStream_t s);
+cudaError_t launch_shard_produce(const void* w, int64_t n_loc, int dtype, int64_t base, int64_t n_global,
+                                 const double* pt, int first, int last, int stratified, double offset,
+                                 const double* uniforms, const pfr_rng* rng, uint32_t* ext, int64_t wlo, int64_t whi,
+                                 uint32_t* status, const Workspace& ws, cudaStream_t s);
+cudaError_t launch_shard_resolve_fast(int64_t n_loc, int dtype, int64_t base, const uint32_t* ext, int64_t wlo,
+                                      int64_t whi, int32_t* c, int32_t* max_steps, uint32_t* status,
+                                      const Workspace& ws, cudaStream_t s);
 cudaError_t launch_shard_words(const int32_t* O, int64_t n_loc, int64_t index_base, int32_t o_begin, uint32_t* words,
                                uint8_t* has, uint32_t* status, cudaStream_t s);
 cudaError_t launch_shard_resolve(const uint32_t* words, const uint8_t* has, int64_t n_loc, int64_t index_base,

@@ -200,73 +200,11 @@ __global__ void k_shard_scatter(const int32_t* __restrict__ done, int64_t count,
 }
 
 // ---------------------------------------------------------------------------
-// Protocol v2 (sharded.py): device-resident prefix / total, fixed-size
-// boundary bands instead of a variable all-to-all, no host round trip until
-// the final status exchange.
-//
-// The rank's EXTENDED word array covers slots [base - H, base + n_loc + H):
-// its own slot window is written there directly, the neighbours' windows
-// reach it through the all-gathered boundary bands (ext[0, 2H) and
-// ext[n_loc, n_loc + 2H) of every rank), and loser chains are walked inside
-// it.  Anything outside (a drift or chain beyond H) sets PFR_ST_OVERFLOW and
-// the host reruns the general protocol.
+// Boundary bands of the sharded protocol (sharded.py): a rank's slot words
+// live in an EXTENDED array covering slots [base - H, base + n_loc + H)
+// (sentinel 0xFFFFFFFF where no word was written); the neighbours' windows
+// reach it through their boundary bands.
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // FIRST | parent 2^31-1: no word has it (N < 2^31 - 1)
-constexpr int kExtBound = 4096;              // chain hops walked inside the extended array
-
-__device__ __forceinline__ int32_t shard_O(double W, double total, int64_t n_global, const ShardU& U) {
-  const double r = __ddiv_rn(__dmul_rn(W, (double)n_global), total);
-  int64_t k = (int64_t)floor(r) + 1;
-  if (k > n_global) k = n_global;
-  if (k < 1) k = 1;
-  int64_t o = (int64_t)floor(__dadd_rn(r, stratum_u_global(U, k - 1)));
-  if (o > n_global) o = n_global;
-  if (o < 0) o = 0;
-  return (int32_t)o;
-}
-
-// pt = {prefix, total} on the device; o_before = O of the element before the
-// shard (the previous shard's last O: W there is exactly `prefix`)
-__global__ void k_shard_offspring_dev(const double* __restrict__ W_loc, int64_t n_loc, const double* pt,
-                                      int64_t n_global, int last_global, int first_global, ShardU U,
-                                      int32_t* __restrict__ O, int32_t* o_before) {
-  const double prefix = pt[0], total = pt[1];
-  if (blockIdx.x == 0 && threadIdx.x == 0) *o_before = first_global ? 0 : shard_O(prefix, total, n_global, U);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_loc; i += stride) {
-    int32_t o = shard_O(__dadd_rn(prefix, W_loc[i]), total, n_global, U);
-    if (last_global && i == n_loc - 1) o = (int32_t)n_global;  // O[N-1] = N (resamplers.py:151)
-    O[i] = o;
-  }
-}
-
-// words of the shard's slot window, written at their extended positions
-__global__ void k_shard_ext_words(const int32_t* __restrict__ O, int64_t n_loc, int64_t index_base,
-                                  const int32_t* o_before, int64_t H, uint32_t* __restrict__ ext,
-                                  uint8_t* __restrict__ has, uint32_t* status) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t lo_slot = index_base - H, ext_n = n_loc + 2 * H;
-  uint32_t f = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_loc; i += stride) {
-    const int32_t lo = i ? O[i - 1] : *o_before;
-    const int32_t hi = O[i];
-    if (hi < lo) {
-      f |= PFR_ST_NOTMONOTONE;
-      has[i] = 0;
-      continue;
-    }
-    has[i] = hi > lo;
-    const uint32_t p = (uint32_t)(index_base + i);
-    for (int32_t s = lo; s < hi; ++s) {
-      const int64_t pos = (int64_t)s - lo_slot;
-      if (pos < 0 || pos >= ext_n) {
-        f |= PFR_ST_OVERFLOW;
-        continue;
-      }
-      ext[pos] = p | (s == lo ? kFirst : 0u);
-    }
-  }
-  status_or_warp(status, f);
-}
 
 // fill the sentinel positions of ext from the neighbours' boundary bands:
 // from_left = the left neighbour's ext[n, n + 2H) (slots [base - H, base + H)),
@@ -284,52 +222,6 @@ __global__ void k_shard_merge(uint32_t* __restrict__ ext, int64_t n_loc, int64_t
       const uint32_t v = from_right[q];
       if (v != kSentinel && ext[n_loc + q] == kSentinel) ext[n_loc + q] = v;
     }
-  }
-}
-
-__global__ void k_shard_resolve_ext(const uint32_t* __restrict__ ext, int64_t n_loc, int64_t H,
-                                    const uint8_t* __restrict__ has, int64_t index_base, int32_t* __restrict__ c,
-                                    int32_t* max_steps, uint32_t* status) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t lo_slot = index_base - H, ext_n = n_loc + 2 * H;
-  int longest = 0;
-  uint32_t f = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_loc; i += stride) {
-    const int64_t x = index_base + i;
-    if (has[i]) {
-      c[i] = (int32_t)x;
-      continue;
-    }
-    uint32_t wd = __ldg(ext + H + i);
-    if (wd == kSentinel) {  // this index's word never arrived
-      f |= PFR_ST_OVERFLOW;
-      continue;
-    }
-    int st = 0;
-    bool ok = true;
-    while (wd & kFirst) {
-      const int64_t pos = (int64_t)(wd & kParentMask) - lo_slot;
-      if (++st > kExtBound || pos < 0 || pos >= ext_n) {
-        ok = false;
-        break;
-      }
-      wd = __ldg(ext + pos);
-      if (wd == kSentinel) {
-        ok = false;
-        break;
-      }
-    }
-    if (!ok) {
-      f |= PFR_ST_OVERFLOW;
-      continue;
-    }
-    c[i] = (int32_t)(wd & kParentMask);
-    longest = max(longest, st);
-  }
-  status_or_warp(status, f);
-  if (max_steps) {
-    longest = __reduce_max_sync(__activemask(), longest);
-    if ((threadIdx.x & 31) == 0 && longest) atomicMax(max_steps, longest);
   }
 }
 
@@ -390,43 +282,9 @@ cudaError_t launch_shard_scatter(const int32_t* done, int64_t count, int64_t ind
   return cudaGetLastError();
 }
 
-cudaError_t launch_shard_offspring_dev(const double* W_loc, int64_t n_loc, int dtype, const double* prefix_total,
-                                       int64_t n_global, int last_global, int first_global, int stratified,
-                                       double offset, const double* uniforms, const pfr_rng* rng, int32_t* O,
-                                       int32_t* o_before, cudaStream_t s) {
-  ShardU U;
-  U.stratified = stratified;
-  U.f32 = dtype == PFR_F32;
-  U.u_sys = U.f32 ? (double)(float)offset : offset;
-  U.uniforms = uniforms;
-  U.mode = rng ? rng->mode : PFR_RNG_ARRAYS;
-  U.key = Key2x64{rng ? rng->key0 : 0, rng ? rng->key1 : 0};
-  k_shard_offspring_dev<<<grid_for_n(n_loc), 256, 0, s>>>(W_loc, n_loc, prefix_total, n_global, last_global,
-                                                          first_global, U, O, o_before);
-  note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_shard_ext(const int32_t* O, int64_t n_loc, int64_t index_base, const int32_t* o_before, int64_t H,
-                             uint32_t* ext, uint8_t* has, uint32_t* status, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(ext, 0xFF, (size_t)(n_loc + 2 * H) * sizeof(uint32_t), s);
-  if (e != cudaSuccess) return e;
-  k_shard_ext_words<<<grid_for_n(n_loc), 256, 0, s>>>(O, n_loc, index_base, o_before, H, ext, has, status);
-  note_launch();
-  return cudaGetLastError();
-}
-
 cudaError_t launch_shard_merge(uint32_t* ext, int64_t n_loc, int64_t H, const uint32_t* from_left,
                                const uint32_t* from_right, cudaStream_t s) {
   k_shard_merge<<<grid_for_n(2 * H), 256, 0, s>>>(ext, n_loc, H, from_left, from_right);
-  note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_shard_resolve_ext(const uint32_t* ext, int64_t n_loc, int64_t H, const uint8_t* has,
-                                     int64_t index_base, int32_t* c, int32_t* max_steps, uint32_t* status,
-                                     cudaStream_t s) {
-  k_shard_resolve_ext<<<grid_for_n(n_loc), 256, 0, s>>>(ext, n_loc, H, has, index_base, c, max_steps, status);
   note_launch();
   return cudaGetLastError();
 }

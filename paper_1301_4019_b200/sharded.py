@@ -335,20 +335,44 @@ class CudaShardOps:
             L.call("pfr_shard_scatter", done.data_ptr(), k, int(base), c.numel(), c.data_ptr(),
                    self.status.data_ptr(), L.stream_handle())
 
-    # ---- protocol v2 (device-resident scalars, boundary bands) ----
-    def local_scan_dev(self, w: torch.Tensor):
-        """the shard's float64 inclusive scan and its total, both on the device"""
+    # ---- protocol v3: the shard's local work through the single-GPU kernels ----
+    def local_end(self, w: torch.Tensor) -> torch.Tensor:
+        """K1 over the shard (check_weights' flags into the status word) and the
+        shard's END value (W at its last element in the delivery's
+        association) as a 1-element device tensor"""
         w = L.as_weights(w)
         n = w.numel()
-        W = torch.empty(n, dtype=torch.float64, device=self.dev)
+        end = torch.empty(1, dtype=torch.float64, device=self.dev)
         ws, wsb = self._workspace(n)
-        L.call("pfr_scan", w.data_ptr(), W.data_ptr(), n, L.dtype_code(w), L.F64, L.ACC_F64 | L.SCAN_MONOTONE, 0, None,
-               self.status.data_ptr(), ws, wsb, L.stream_handle())
-        return W, W[-1:]
+        L.call("pfr_shard_local_end", w.data_ptr(), n, L.dtype_code(w), end.data_ptr(), self.status.data_ptr(), ws, wsb,
+               L.stream_handle())
+        return end
+
+    def shard_produce(self, w, base, n_global, pt, first, last, stratified, offset, uniforms, rng, mode, ext, slot_lo,
+                      slot_hi):
+        w = L.as_weights(w)
+        n = w.numel()
+        k0, k1 = as_stream(rng).key() if rng is not None else (0, 0)
+        r = L.PfrRng(k0, k1, L.rng_mode_code(mode), 0)
+        uni = None if uniforms is None else torch.as_tensor(uniforms, dtype=torch.float64).to(self.dev).contiguous()
+        pt = self._on_dev(pt)
+        ws, wsb = self._workspace(n)
+        L.call("pfr_shard_produce", w.data_ptr(), n, L.dtype_code(w), int(base), int(n_global), pt.data_ptr(),
+               int(first), int(last), int(stratified), float(offset), L.ptr(uni), r, ext.data_ptr(), int(slot_lo),
+               int(slot_hi), self.status.data_ptr(), ws, wsb, L.stream_handle())
+
+    def shard_resolve_fast(self, ext, slot_lo, slot_hi, base, n_loc, wdtype):
+        c = torch.empty(n_loc, dtype=torch.int32, device=self.dev)
+        st = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        ws, wsb = self._workspace(n_loc)
+        L.call("pfr_shard_resolve_fast", int(n_loc), L.F32 if wdtype == torch.float32 else L.F64, int(base),
+               ext.data_ptr(), int(slot_lo), int(slot_hi), c.data_ptr(), st.data_ptr(), self.status.data_ptr(), ws, wsb,
+               L.stream_handle())
+        return c, st
 
     def prefix_total(self, totals: torch.Tensor, rank: int) -> torch.Tensor:
-        """{weight before this shard, W_N}: left folds of the shard totals in
-        rank order (the same IEEE additions on every rank), on the device"""
+        """{weight before this shard, W_N}: left folds of the shard END values
+        in rank order (the same IEEE additions on every rank), on the device"""
         totals = self._on_dev(totals).to(torch.float64)
         acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
         prefix = acc
@@ -357,27 +381,6 @@ class CudaShardOps:
                 prefix = acc.clone()
             acc = acc + totals[r: r + 1]
         return torch.cat([prefix, acc])
-
-    def offspring_dev(self, W, wdtype, pt, n_global, last, first, stratified, offset, uniforms, rng, mode):
-        n = W.numel()
-        O = torch.empty(n, dtype=torch.int32, device=self.dev)
-        ob = torch.empty(1, dtype=torch.int32, device=self.dev)
-        k0, k1 = as_stream(rng).key() if rng is not None else (0, 0)
-        r = L.PfrRng(k0, k1, L.rng_mode_code(mode), 0)
-        uni = None if uniforms is None else torch.as_tensor(uniforms, dtype=torch.float64).to(self.dev).contiguous()
-        pt = self._on_dev(pt)
-        L.call("pfr_shard_offspring_dev", W.data_ptr(), n, L.F32 if wdtype == torch.float32 else L.F64, pt.data_ptr(),
-               int(n_global), int(last), int(first), int(stratified), float(offset), L.ptr(uni), r, O.data_ptr(),
-               ob.data_ptr(), L.stream_handle())
-        return O, ob
-
-    def ext_words(self, O, base, o_before, halo):
-        n = O.numel()
-        ext = torch.empty(n + 2 * halo, dtype=torch.int32, device=self.dev)
-        has = torch.empty(n, dtype=torch.uint8, device=self.dev)
-        L.call("pfr_shard_ext_words", O.data_ptr(), n, int(base), o_before.data_ptr(), int(halo), ext.data_ptr(),
-               has.data_ptr(), self.status.data_ptr(), L.stream_handle())
-        return ext, has
 
     @staticmethod
     def bands(ext, n_loc, halo):
@@ -390,13 +393,6 @@ class CudaShardOps:
         fr = None if from_right is None else self._on_dev(from_right)
         L.call("pfr_shard_merge_bands", ext.data_ptr(), int(n_loc), int(halo), L.ptr(fl), L.ptr(fr),
                L.stream_handle())
-
-    def resolve_ext(self, ext, n_loc, halo, has, base):
-        c = torch.empty(n_loc, dtype=torch.int32, device=self.dev)
-        st = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        L.call("pfr_shard_resolve_ext", ext.data_ptr(), int(n_loc), int(halo), has.data_ptr(), int(base), c.data_ptr(),
-               st.data_ptr(), self.status.data_ptr(), L.stream_handle())
-        return c, st
 
     def metropolis_range(self, w_full, b, rng, mode, c_begin, c_count):
         w_full = L.as_weights(w_full)
@@ -605,7 +601,7 @@ def metropolis_sharded(w_local, config_or_b, rng, *, comm, ops=None, rng_mode=No
 
 
 # how often each systematic/stratified protocol ran (diagnostics; tests)
-protocol_counts = {"v2": 0, "general": 0}
+protocol_counts = {"v2": 0, "general": 0}  # "v2": the halo protocol (v3 kernels)
 _count_lock = threading.Lock()
 
 
@@ -626,38 +622,43 @@ def halo_width(n: int) -> int:
 
 
 def _deliver_offspring_sharded(w_local, stratified, rng, comm, ops, rng_mode, uniforms, return_max_steps):
-    """Protocol v2: two host synchronisations in all (the shard sizes with the
-    validation bits at the start, the status bits at the end); the shard
-    totals (all-gather) and the boundary bands (to the two neighbours) move
-    device to device."""
+    """Protocol v3: the shard's local work through the single-GPU kernels
+    (K1, K2w, K3w of pfr_deliver.cu), two host synchronisations in all (the
+    shard sizes with the validation bits after K1, the status bits at the
+    end); the shard END values (all-gather) and the boundary bands (to the
+    two neighbours) move device to device."""
     rank, world = comm.rank, comm.world
     w_local = torch.as_tensor(w_local)
-    ops.check_local(w_local)
-    rows = comm.all_gather_scalars(int(w_local.numel()) | (int(ops.status_bits()) << 40), torch.int64)
+    n_loc = int(w_local.numel())
+    if n_loc < 1:
+        raise ValueError("every rank needs a non-empty weight shard")
+    # 1. K1 over the shard: hierarchy, validation bits, END value (device)
+    end = ops.local_end(w_local)
+    rows = comm.all_gather_scalars(n_loc | (int(ops.status_bits()) << 40), torch.int64)
     sizes = [int(r) & ((1 << 40) - 1) for r in rows]
     bits = 0
     for r in rows:
         bits |= int(r) >> 40
     L.raise_weight_errors(bits, "w", True)
     offs, n = shard_bounds(sizes)
-    base, n_loc = int(offs[rank]), sizes[rank]
-    if min(sizes) < 1:
-        raise ValueError("every rank needs a non-empty weight shard")
+    base = int(offs[rank])
     halo = halo_width(n)
-
-    # 1. local scan; shard totals device to device; prefix and W_N on the device
-    W_loc, t_loc = ops.local_scan_dev(w_local)
-    pt = ops.prefix_total(comm.all_gather_fixed(t_loc), rank)
-    # 2. offspring in global slot numbers, the slot words of this shard's
-    #    window written into the extended array around its indices
+    slot_lo = ((base - halo) // 4) * 4  # 16-byte aligned window start
+    slot_hi = base + n_loc + halo
+    shift = (base - halo) - slot_lo
+    # 2. END values device to device; weight before the shard and W_N as left
+    #    folds in rank order (the same IEEE additions on every rank)
+    pt = ops.prefix_total(comm.all_gather_fixed(end), rank)
+    # 3. K2w: O in global slot numbers and the slot words of this shard's window
     offset = 0.0 if stratified else ops.systematic_offset(rng, rng_mode)
-    O, o_before = ops.offspring_dev(W_loc, w_local.dtype, pt, n, rank == world - 1, rank == 0, stratified, offset,
-                                    uniforms, rng, rng_mode)
-    ext, has = ops.ext_words(O, base, o_before, halo)
-    # 3. boundary bands to and from the two neighbours (point to point)
-    ops.merge(ext, n_loc, halo, *comm.neighbor_exchange(*ops.bands(ext, n_loc, halo)))
-    # 4. the in-place ancestry of this shard's indices
-    c, steps = ops.resolve_ext(ext, n_loc, halo, has, base)
+    ext = torch.empty(slot_hi - slot_lo, dtype=torch.int32, device=end.device)
+    ops.shard_produce(w_local, base, n, pt, rank == 0, rank == world - 1, stratified, offset, uniforms, rng, rng_mode,
+                      ext, slot_lo, slot_hi)
+    # 4. boundary bands to and from the two neighbours (point to point)
+    view = ext[shift:]
+    ops.merge(view, n_loc, halo, *comm.neighbor_exchange(*ops.bands(view, n_loc, halo)))
+    # 5. K3w: the in-place ancestry of this shard's indices
+    c, steps = ops.shard_resolve_fast(ext, slot_lo, slot_hi, base, n_loc, w_local.dtype)
     rows = comm.all_gather_scalars(int(ops.status_bits()) | (int(L.read_status(steps)) << 32), torch.int64)
     bits = 0
     for r in rows:
@@ -671,7 +672,6 @@ def _deliver_offspring_sharded(w_local, stratified, rng, comm, ops, rng_mode, un
     if return_max_steps:
         return c, max(int(r) >> 32 for r in rows)
     return c
-
 
 
 def _deliver_offspring_general(w_local, stratified, rng, comm, ops, rng_mode, uniforms, return_max_steps):

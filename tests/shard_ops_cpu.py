@@ -139,6 +139,39 @@ class NumpyShardOps:
         for h, v in _np(done).reshape(-1, 2).tolist():
             c[h - base] = v
 
+    # ---- protocol v3 (pfr_shard_local_end / _produce / _resolve_fast), in NumPy
+    def local_end(self, w):
+        self.check_local(w)  # K1 reports check_weights' flags, the positive one included
+        W, _ = self.local_scan(w)
+        return W[-1:].clone()
+
+    def shard_produce(self, w, base, n_global, pt, first, last, stratified, offset, uniforms, rng, mode, ext, slot_lo,
+                      slot_hi):
+        from paper_1301_4019_b200 import _lib as L
+
+        W, _ = self.local_scan(w)
+        wdtype = torch.as_tensor(w).dtype
+        O, ob = self.offspring_dev(W, wdtype, pt, n_global, last, first, stratified, offset, uniforms, rng, mode)
+        O = _np(O, np.int64)
+        prev = np.concatenate([[int(_np(ob)[0])], O[:-1]])
+        o = O - prev
+        if np.any(o < 0):
+            self.bits |= L.ST_OVERFLOW
+        e = ext.numpy().view(np.uint32)
+        e[:] = self.SENT
+        self._has = (o > 0).astype(np.uint8)
+        for i in np.flatnonzero(o > 0).tolist():
+            for sl in range(int(prev[i]), int(O[i])):
+                if slot_lo <= sl < slot_hi:
+                    e[sl - slot_lo] = (base + i) | (FIRST if sl == prev[i] else 0)
+                else:
+                    self.bits |= L.ST_OVERFLOW
+
+    def shard_resolve_fast(self, ext, slot_lo, slot_hi, base, n_loc, wdtype):
+        halo = base - slot_lo  # resolve_ext's extended array starts at base - halo
+        c, st = self.resolve_ext(ext, n_loc, halo, torch.from_numpy(self._has), base)
+        return c, st
+
     # ---- protocol v2 (csrc/pfr_shard.cu: k_shard_offspring_dev, k_shard_ext_words,
     # k_shard_merge, k_shard_resolve_ext), in NumPy
     SENT = 0xFFFFFFFF
