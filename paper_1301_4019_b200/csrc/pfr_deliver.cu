@@ -596,6 +596,7 @@ __device__ __forceinline__ bool subtile_expand(const int32_t (&o)[kTileItems], i
   int4* hb4 = reinterpret_cast<int4*>(W.buf);
   const int pb = (int)(gbase + e0);  // global index of the lane's first parent
   int carry = -1;
+  const bool single = oend - (o_prev & ~3) <= kWBuf;
   // chunks of kWBuf = 1024 positions (a typical subtile's ~512 slots fit one
   // chunk whatever their alignment), scanned as up to two rows of 512
   for (int c0 = o_prev & ~3; c0 < oend; c0 += kWBuf) {
@@ -607,11 +608,23 @@ __device__ __forceinline__ bool subtile_expand(const int32_t (&o)[kTileItems], i
       for (int q = 0; q < 4; ++q) hb4[sw_hd(128 + 4 * lane + q)] = make_int4(-1, -1, -1, -1);
     }
     __syncwarp();
-    {
-      int r = prev_l - c0;  // first slot of parent j = O[j-1], relative
+    // head of parent j at its first slot O[j-1] - c0; the swizzle
+    // (sw_hd(r >> 2) << 2) | (r & 3) folds to r ^ ((r >> 3) & 12).  In the
+    // usual single-chunk case (the whole range fits one chunk) every head
+    // lies in [0, oend - c0) within the buffer, so the range test is dropped
+    // (uniform branch; later chunks of a long range see heads below c0)
+    if (single) {
+      int r = prev_l - c0;
 #pragma unroll
       for (int j = 0; j < kTileItems; ++j) {
-        if (((bits >> j) & 1u) && (unsigned)r < (unsigned)kWBuf) hb[(sw_hd(r >> 2) << 2) | (r & 3)] = pb + j;
+        if ((bits >> j) & 1u) hb[r ^ ((r >> 3) & 12)] = pb + j;
+        r = o[j] - c0;
+      }
+    } else {
+      int r = prev_l - c0;
+#pragma unroll
+      for (int j = 0; j < kTileItems; ++j) {
+        if (((bits >> j) & 1u) && (unsigned)r < (unsigned)kWBuf) hb[r ^ ((r >> 3) & 12)] = pb + j;
         r = o[j] - c0;
       }
     }
@@ -651,13 +664,24 @@ __device__ __forceinline__ bool subtile_expand(const int32_t (&o)[kTileItems], i
         for (int q = 0; q < kTileItems / 4; ++q)
           dst[q] = make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
       } else if (s0 < oend && s0 + kTileItems > o_prev) {
-        for (int t = 0; t < kTileItems; ++t) {
-          const int64_t sl = s0 + t;
-          if (sl >= o_prev && sl < oend) {
-            if (!kShard || (sl >= wlo && sl < whi))
-              words[sl - wlo] = wv[t];
-            else
-              outside = true;
+        // an edge row: whole 16-byte groups as vectors, element stores only
+        // in the (at most two) groups the range cuts
+#pragma unroll
+        for (int q = 0; q < kTileItems / 4; ++q) {
+          const int v0 = s0 + 4 * q;
+          if (v0 >= o_prev && v0 + 4 <= oend && (!kShard || (v0 >= wlo && v0 + 4 <= whi))) {
+            *reinterpret_cast<uint4*>(words + (v0 - wlo)) = make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
+          } else if (v0 < oend && v0 + 4 > o_prev) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int64_t sl = v0 + t;
+              if (sl >= o_prev && sl < oend) {
+                if (!kShard || (sl >= wlo && sl < whi))
+                  words[sl - wlo] = wv[4 * q + t];
+                else
+                  outside = true;
+              }
+            }
           }
         }
       }
