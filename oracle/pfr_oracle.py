@@ -429,6 +429,84 @@ def rejection_stream(w, bound: float, seed: int, ids=(), cap=None):
 
 
 # ---------------------------------------------------------------------------
+# the GPU's own Philox stream (rng_mode='philox'): a model of its rejection
+
+
+def philox4x32_10_vec(c0, c1, c2, c3, k0: int, k1: int):
+    """philox4x32_10 over numpy arrays of 32-bit counters (uint64 lanes)."""
+    x0, x1, x2, x3 = (np.asarray(c, dtype=np.uint64) & MASK32 for c in (c0, c1, c2, c3))
+    x0, x1, x2, x3 = (np.broadcast_to(v, np.broadcast(x0, x1, x2, x3).shape).copy() for v in (x0, x1, x2, x3))
+    m0, m1 = np.uint64(_PH32_M[0]), np.uint64(_PH32_M[1])
+    sh, lo = np.uint64(32), np.uint64(MASK32)
+    for rnd in range(10):
+        if rnd:
+            k0 = (k0 + _PH32_W[0]) & MASK32
+            k1 = (k1 + _PH32_W[1]) & MASK32
+        p0 = m0 * x0  # < 2^64: no wrap
+        p1 = m1 * x2
+        x0, x1, x2, x3 = ((p1 >> sh) ^ x1 ^ np.uint64(k0), p1 & lo, (p0 >> sh) ^ x3 ^ np.uint64(k1), p0 & lo)
+    return x0, x1, x2, x3
+
+
+TAG_REJECTION = 0x524A  # csrc/pfr_rng.cuh kTagRejection
+
+
+def own_rejection(w, bound: float, key0: int, cap=None):
+    """The GPU's own-stream rejection (csrc/pfr_resample.cu rej_draws,
+    k_rejection_philox) for a power-of-two N: trip t of slot i uses Philox
+    counter (i, t // 2, tag, 0) keyed (key0 low, key0 high), words 2(t&1) /
+    2(t&1)+1 = proposal (umulhi(x, N)) / open uniform; trip 0 proposes i;
+    accept when beta * bound <= v[j] in the weights' precision (the
+    semantics of resamplers.py:237-310 on this stream).  Returns (a, trips[,
+    out_w]).  Test model of the product's stream, not of the reference's."""
+    w = np.asarray(w)
+    n = w.size
+    if n & (n - 1):
+        raise ValueError("the model covers power-of-two N (no Lemire redraws)")
+    T = w.dtype.type
+    capv = T(cap) if cap is not None else None
+    v = w if cap is None else np.where(w < capv, w, capv)
+    bnd = T(cap if cap is not None else bound)
+    k0, k1 = int(key0) & MASK32, (int(key0) >> 32) & MASK32
+    a = np.full(n, -1, dtype=np.int64)
+    trips = np.zeros(n, dtype=np.int64)
+    active = np.arange(n, dtype=np.int64)
+    t = 0
+    while active.size:
+        if t > 1 << 20:
+            raise RuntimeError("no progress")
+        o = philox4x32_10_vec(active, t // 2, TAG_REJECTION, 0, k0, k1)
+        for h in (0, 1):
+            if not active.size:
+                break
+            if len(o[0]) != active.size:  # slots accepted on the first half
+                o = tuple(x[keep] for x in o)
+            xj, xu = o[2 * h], o[2 * h + 1]
+            j = ((xj * np.uint64(n)) >> np.uint64(32)).astype(np.int64)
+            if t == 0:
+                j = active.copy()
+            if T is np.float32:
+                u = ((((xu >> np.uint64(9)) << np.uint64(1)) | np.uint64(1)).astype(np.float32)
+                     * np.float32(1.0 / 16777216.0))
+            else:
+                u = xu.astype(np.float64) * 2.0 ** -32 + 2.0 ** -33
+            ok = u * bnd <= v[j]
+            a[active[ok]] = j[ok]
+            trips[active[ok]] = t + 1
+            keep = ~ok
+            active = active[keep]
+            t += 1
+        if t % 2:  # odd: the loop broke after the first half
+            t += 1
+    if cap is None:
+        return a, trips
+    va = v[a]
+    with np.errstate(invalid="ignore", divide="ignore"):
+        out_w = np.where(va == 0, T(1), w[a] / va).astype(w.dtype)
+    return a, trips, out_w
+
+
+# ---------------------------------------------------------------------------
 # ancestry (ancestry.py)
 
 

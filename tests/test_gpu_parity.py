@@ -661,3 +661,43 @@ def test_config4_full_size_properties(alg):
     assert pf.satisfies_inplace_predicate(c)
     del c, w
     torch.cuda.empty_cache()
+
+
+def _rej_weights(kind, n, dtype, seed):
+    g = np.random.default_rng(seed)
+    if kind == "lognormal1":
+        w = np.exp(g.normal(0, 1, n))
+    elif kind == "lognormal2":
+        w = np.exp(g.normal(0, 2, n))
+    elif kind == "uniform":
+        w = g.random(n)
+    elif kind == "spikes":  # a few large weights, the rest tiny or zero
+        w = g.random(n) * 1e-3
+        w[g.integers(0, n, 5)] = 1.0
+        w[g.random(n) < 0.3] = 0.0
+    else:
+        raise KeyError(kind)
+    return w.astype(dtype)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [4096, 1 << 16])
+@pytest.mark.parametrize("kind", ["lognormal1", "lognormal2", "uniform", "spikes"])
+@pytest.mark.parametrize("capped", [False, True])
+def test_rejection_own_stream_matches_model(dtype, n, kind, capped):
+    """Own-stream rejection, bit for bit against the oracle's model of the
+    stream (ancestors, trip counts, capped importance weights)."""
+    w = _rej_weights(kind, n, dtype, n + len(kind))
+    rs = pf.RngStream(31, (n, int(capped)))
+    key0 = rs.key()[0]
+    if capped:
+        cap = float(np.quantile(w, 0.9))
+        a, ow, trips = pf.rejection_ancestors_capped(w, cap, rs, return_trips=True)
+        wa, wt, wo = O.own_rejection(w, cap, key0, cap=cap)
+        np.testing.assert_array_equal(np_(ow), wo)
+    else:
+        bound = float(w.max()) * (1.5 if kind == "lognormal2" else 1.0)
+        a, trips = pf.rejection_ancestors(w, bound, rs, return_trips=True)
+        wa, wt = O.own_rejection(w, bound, key0)
+    np.testing.assert_array_equal(np_(a), wa)
+    np.testing.assert_array_equal(np_(trips), wt)

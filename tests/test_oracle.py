@@ -203,3 +203,26 @@ def test_rejection_rounds_on_stream_model():
         pending = pending[~ok]
     np.testing.assert_array_equal(a, a_ref)
     np.testing.assert_array_equal(trips, trips_ref)
+
+
+def test_philox4x32_vectorised_matches_scalar():
+    """The vectorised Philox4x32-10 of the own-stream model equals the scalar
+    restatement of csrc/pfr_rng.cuh word for word."""
+    g = np.random.default_rng(5)
+    c = g.integers(0, 1 << 32, (4, 64), dtype=np.uint64)
+    k0, k1 = 0x9A3B1C2D, 0x01F2E3D4
+    vec = O.philox4x32_10_vec(c[0], c[1], c[2], c[3], k0, k1)
+    for i in range(64):
+        assert [int(v[i]) for v in vec] == O.philox4x32_10([int(x) for x in c[:, i]], (k0, k1))
+
+
+def test_own_rejection_model_statistics():
+    """The own-stream rejection model: trip 0 proposes the slot itself, mean
+    trips ~ bound / mean(v), capped weights w[a] / min(w[a], cap)."""
+    g = np.random.default_rng(2)
+    w = g.random(4096) + 0.5
+    a, trips = O.own_rejection(w, float(w.max()), 12345)
+    assert np.all(trips >= 1) and np.all(a[trips == 1] == np.flatnonzero(trips == 1))
+    assert abs(trips.mean() - w.max() / w.mean()) < 0.05 * w.max() / w.mean()
+    a, trips, ow = O.own_rejection(w.astype(np.float32), 1.0, 7, cap=1.0)
+    np.testing.assert_array_equal(ow, np.maximum(w.astype(np.float32)[a], np.float32(1.0)) / np.float32(1.0))
