@@ -227,7 +227,6 @@ struct RejArgs {
   T* out_w;
   unsigned long long* next_chunk;
   uint32_t* status;
-  int pack_k;  // log2 N for the packed 3-trips-per-call draws (N = 2^k, k <= 21), else -1
 };
 
 constexpr int kRejChunk = 256;
@@ -270,57 +269,26 @@ __device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, ui
   if (trip == 0) d.j[0] = slot;
 }
 
-// Packed draws (power-of-two N = 2^k, k <= 21): THREE trips per
-// Philox4x32-10 call instead of two.  The 128 output bits are cut into three
-// 42-bit fields; trip t of `slot` uses call (slot, t/3) and field t%3: the low
-// k bits are the proposal (exact: N is a power of two), the remaining 42-k >=
-// 21 bits the uniform, taken at the midpoint of its cell, (bits + 1/2) *
-// 2^-(42-k), so it is never 0 (a zero weight can never be accepted) and its
-// quantisation moves an acceptance probability by at most 2^-(43-k) <= 2^-22
-// (float32: the top 22 bits).  Philox is ~46% of the rejection kernel's
-// instructions, so a third fewer calls per trip -- yet measured slower on
-// B200 (launcher), so opt-in only.
-template <typename T, int B>
-__device__ __forceinline__ void rej_draws3(const RejArgs<T>& A, uint32_t slot, uint32_t trip, int k,
-                                           RejBatch<T, B>& d) {
-  static_assert(B % 3 == 0, "packed batches hold whole Philox calls");
-  const uint32_t nmask = (uint32_t)A.n - 1u;
-  const int m = 42 - k;  // uniform bits
-#pragma unroll
-  for (int q = 0; q < B / 3; ++q) {
-    uint32_t o[4];
-    philox4x32_10(slot, trip / 3 + q, kTagRejection, 0, A.k0, A.k1, o);
-    const uint64_t f[3] = {((uint64_t)o[1] << 32 | o[0]) & 0x3FFFFFFFFFFull,
-                           (((uint64_t)o[2] << 32 | o[1]) >> 10) & 0x3FFFFFFFFFFull,
-                           (((uint64_t)o[3] << 32 | o[2]) >> 20) & 0x3FFFFFFFFFFull};
-#pragma unroll
-    for (int h = 0; h < 3; ++h) {
-      d.j[3 * q + h] = (uint32_t)f[h] & nmask;
-      const uint64_t ub = f[h] >> k;  // m bits
-      if constexpr (sizeof(T) == 4) {
-        // top 22 bits, then the midpoint bit: 23 mantissa bits
-        const uint32_t t22 = m >= 22 ? (uint32_t)(ub >> (m - 22)) : (uint32_t)(ub << (22 - m));
-        d.u[3 * q + h] = __uint_as_float(0x3F800000u | (t22 << 1) | 1u) - 1.0f;
-      } else {
-        d.u[3 * q + h] = __longlong_as_double((long long)(0x3FF0000000000000ull | ((2 * ub + 1) << (51 - m)))) - 1.0;
-      }
-    }
-  }
-  if (trip == 0) d.j[0] = slot;
-}
-
-// Software pipelined: the gathers of batch k are issued, then the draws of
-// batch k+1 are computed while they are in flight, then batch k is resolved.
-// A lane whose slot finishes discards its precomputed batch (one per slot).
-template <typename T, bool kCapped, int kRejBatch, int kMinBlocks = 1, bool kPack = false>
-__global__ void __launch_bounds__(256, kMinBlocks) k_rejection_philox(RejArgs<T> A) {
-  auto draws = [&](uint32_t slot, uint32_t trip, RejBatch<T, kRejBatch>& d) {
-    if constexpr (kPack)
-      rej_draws3<T, kRejBatch>(A, slot, trip, A.pack_k, d);
-    else
-      rej_draws<T, kRejBatch>(A, slot, trip, d);
-  };
-  const int lane = threadIdx.x & 31;
+// Steady state: every lane owns a slot; the gathers of batch k are issued,
+// then the draws of batch k+1 are computed while they are in flight, then
+// batch k is resolved (two batch buffers used in turn: no copies).  A lane
+// whose slot finishes discards its precomputed batch and takes the next slot
+// of the warp's chunk (one atomic per 256 slots).
+//
+// Tail: once the chunks are exhausted, lanes without a slot HELP the slots
+// still running instead of idling -- trip t of a slot depends only on (slot,
+// t), so helper h of a slot evaluates trips t + hB .. t + hB + B - 1 in the
+// same pass and the first accepting trip over the owner and its helpers wins
+// (a shared-memory atomicMin on (trip, proposal)).  Results, trip counts and
+// the stream mapping are exactly those of a one-trip-at-a-time loop; the
+// geometric tail (a warp's last slot runs ~4x the mean trips) no longer
+// leaves 31 lanes idle.
+template <typename T, bool kCapped, int kRejBatch>
+__global__ void __launch_bounds__(256, 1) k_rejection_philox(RejArgs<T> A) {
+  constexpr int B = kRejBatch;
+  __shared__ unsigned long long s_best[8][32];  // per warp, per owner lane
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
   const T bound = (T)A.bound;
   const T capv = (T)A.cap;
   int64_t chunk_next = 0, chunk_end = 0;  // warp-uniform local queue
@@ -329,9 +297,36 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_rejection_philox(RejArgs<T>
   uint32_t trip = 0;
   uint32_t flags = 0;
   int iter = 0;
-  RejBatch<T, kRejBatch> cur;
-  while (true) {
-    // refill idle lanes (a new slot starts with its first batch of draws)
+  RejBatch<T, B> buf0, buf1;
+
+  auto finish = [&](uint32_t jd, T wd, uint32_t ntrips) {
+    A.a[slot] = (int32_t)jd;
+    if (A.trips) A.trips[slot] = (int32_t)ntrips;
+    if (kCapped) {
+      const T vd = wd < capv ? wd : capv;
+      A.out_w[slot] = (vd == T(0)) ? T(1) : div_rn_t(wd, vd);
+    }
+    slot = -1;
+  };
+  auto no_progress = [&]() {
+    flags |= PFR_ST_NOPROGRESS;
+    A.a[slot] = (int32_t)(A.s0 + slot);
+    if (A.trips) A.trips[slot] = (int32_t)A.max_trips;
+    if (kCapped) A.out_w[slot] = T(1);
+    slot = -1;
+  };
+  // give up early once any slot reported no progress (reference raises)
+  auto give_up = [&]() {
+    if (((++iter) & 63) == 0) {
+      if (__ballot_sync(0xffffffffu, flags != 0) || (*(volatile uint32_t*)A.status & PFR_ST_NOPROGRESS)) {
+        flags |= PFR_ST_NOPROGRESS;
+        return true;
+      }
+    }
+    return false;
+  };
+  // 0: continue, 1: warp done, 2: chunks exhausted with idle lanes (tail)
+  auto step = [&](RejBatch<T, B>& cur, RejBatch<T, B>& nxt) -> int {
     unsigned idle = __ballot_sync(0xffffffffu, slot < 0);
     while (idle) {
       if (chunk_next >= chunk_end) {
@@ -346,67 +341,99 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_rejection_philox(RejArgs<T>
         chunk_next = (int64_t)base;
         chunk_end = min((int64_t)base + kRejChunk, A.count);
       }
-      const int rank = __popc(idle & ((1u << lane) - 1));
+      const int rank = __popc(idle & lt_mask);
       const int take = min((int64_t)__popc(idle), chunk_end - chunk_next);
       if (slot < 0 && rank < take) {
         slot = chunk_next + rank;
         trip = 0;
-        draws((uint32_t)(A.s0 + slot), 0u, cur);
+        rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), 0u, cur);
       }
       chunk_next += take;
       idle = __ballot_sync(0xffffffffu, slot < 0);
     }
-    if (__ballot_sync(0xffffffffu, slot >= 0) == 0) break;
-    if (slot >= 0) {
-      T wj[kRejBatch];
+    if (idle) return __ballot_sync(0xffffffffu, slot >= 0) ? 2 : 1;
+    T wj[B];
 #pragma unroll
-      for (int q = 0; q < kRejBatch; ++q) wj[q] = ldg(A.w + cur.j[q]);
-      // next batch's draws overlap the gathers' latency
-      RejBatch<T, kRejBatch> nxt;
-      draws((uint32_t)(A.s0 + slot), trip + kRejBatch, nxt);
-      int done = -1;  // batch position of the first accepting trip
+    for (int q = 0; q < B; ++q) wj[q] = ldg(A.w + cur.j[q]);
+    rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), trip + B, nxt);
+    int done = -1;  // batch position of the first accepting trip
+    uint32_t jd = 0;
+    T wd = T(0);
 #pragma unroll
-      for (int q = kRejBatch - 1; q >= 0; --q) {
-        const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
-        // beta <= v[j] / bound  <=>  beta * bound <= v[j]
-        if (cur.u[q] * bound <= vj) done = q;
-      }
-      // round cap: the trips past max_trips do not exist
-      const bool near_cap = trip + (uint32_t)kRejBatch >= A.max_trips;
-      if (near_cap && (done < 0 || trip + (uint32_t)done + 1 > A.max_trips)) done = -2;
-      if (done >= 0) {
-        T wd = wj[0];
-        uint32_t jd = cur.j[0];
-#pragma unroll
-        for (int q = 1; q < kRejBatch; ++q)
-          if (done == q) {
-            wd = wj[q];
-            jd = cur.j[q];
-          }
-        A.a[slot] = (int32_t)jd;
-        if (A.trips) A.trips[slot] = (int32_t)(trip + done + 1);
-        if (kCapped) {
-          const T vd = wd < capv ? wd : capv;
-          A.out_w[slot] = (vd == T(0)) ? T(1) : div_rn_t(wd, vd);
-        }
-        slot = -1;
-      } else if (done == -2) {
-        flags |= PFR_ST_NOPROGRESS;
-        A.a[slot] = (int32_t)(A.s0 + slot);
-        if (A.trips) A.trips[slot] = (int32_t)A.max_trips;
-        if (kCapped) A.out_w[slot] = T(1);
-        slot = -1;
-      } else {
-        trip += kRejBatch;
-        cur = nxt;
+    for (int q = B - 1; q >= 0; --q) {
+      const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
+      // beta <= v[j] / bound  <=>  beta * bound <= v[j]
+      if (cur.u[q] * bound <= vj) {
+        done = q;
+        jd = cur.j[q];
+        wd = wj[q];
       }
     }
-    if (((++iter) & 63) == 0) {
-      // give up early once any slot reported no progress (reference raises)
-      if (__ballot_sync(0xffffffffu, flags != 0) || (*(volatile uint32_t*)A.status & PFR_ST_NOPROGRESS)) {
-        flags |= PFR_ST_NOPROGRESS;
-        break;
+    // round cap: the trips past max_trips do not exist
+    if (trip + (uint32_t)B >= A.max_trips && (done < 0 || trip + (uint32_t)done + 1 > A.max_trips))
+      no_progress();
+    else if (done >= 0)
+      finish(jd, wd, trip + done + 1);
+    else
+      trip += B;
+    return give_up() ? 1 : 0;
+  };
+  int st;
+  while (true) {
+    if ((st = step(buf0, buf1)) != 0) break;
+    if ((st = step(buf1, buf0)) != 0) break;
+  }
+  if (st == 2) {
+    // tail: owners and helpers
+    while (true) {
+      const unsigned act = __ballot_sync(0xffffffffu, slot >= 0);
+      if (!act) break;
+      const int na = __popc(act), ni = 32 - na;
+      int owner, h;
+      if (slot >= 0) {
+        owner = lane;
+        h = 0;
+      } else {
+        const int r = __popc(~act & lt_mask);  // rank among the idle lanes
+        unsigned m = act;                      // owner = the (r % na)-th owner lane
+        for (int i = r % na; i > 0; --i) m &= m - 1u;
+        owner = __ffs(m) - 1;
+        h = r / na + 1;
       }
+      const int k_own = __popc(act & ((1u << owner) - 1u));  // owner's rank among the owners
+      const int helpers = ni / na + (k_own < ni % na ? 1 : 0);
+      const int64_t oslot = __shfl_sync(0xffffffffu, slot, owner);
+      const uint32_t otrip = __shfl_sync(0xffffffffu, trip, owner);
+      if (slot >= 0) s_best[warp][lane] = ~0ull;
+      __syncwarp();
+      const uint32_t t0 = otrip + (uint32_t)(h * B);
+      if (t0 < A.max_trips) {
+        rej_draws<T, B>(A, (uint32_t)(A.s0 + oslot), t0, buf0);
+        T wj[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) wj[q] = ldg(A.w + buf0.j[q]);
+        unsigned long long key = ~0ull;
+#pragma unroll
+        for (int q = B - 1; q >= 0; --q) {
+          const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
+          if (t0 + (uint32_t)q < A.max_trips && buf0.u[q] * bound <= vj)
+            key = ((unsigned long long)(t0 + (uint32_t)q) << 32) | buf0.j[q];
+        }
+        if (key != ~0ull) atomicMin(&s_best[warp][owner], key);
+      }
+      __syncwarp();
+      if (slot >= 0) {
+        const unsigned long long best = s_best[warp][lane];
+        if (best != ~0ull) {
+          const uint32_t jd = (uint32_t)best;
+          finish(jd, kCapped ? ldg(A.w + jd) : T(0), (uint32_t)(best >> 32) + 1);
+        } else {
+          trip += (uint32_t)((helpers + 1) * B);
+          if (trip >= A.max_trips) no_progress();
+        }
+      }
+      __syncwarp();
+      if (give_up()) break;
     }
   }
   status_or_warp(A.status, flags);
@@ -692,53 +719,36 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0) != cudaSuccess || occ < 1) occ = 1;
     return num_sms() * occ;
   };
-  // trips evaluated per lane and iteration (PFR_REJ_BATCH: profiling aid)
+  // trips evaluated per lane and iteration (PFR_REJ_BATCH: profiling aid);
+  // measured on B200 (N=2^20, sigma=1, sup = max w): float32 8, float64 4.
+  // Packed draws (three trips per Philox call from 42-bit fields) measured
+  // slower in round 2 (the 64-bit field extraction costs more issue slots
+  // than the saved rounds) and were removed.
   static const int batch = [] {
     const char* v = getenv("PFR_REJ_BATCH");
     return v ? atoi(v) : 0;
   }();
-  // measured on B200 (N=2^20, sigma=1, sup = max w): float32 8 trips/lane
-  // (475 us), float64 4 trips/lane (483 us); more CTAs per SM lose.  The
-  // packed draws (3 trips per Philox call, PFR_REJ_PACK=1, batches 9 / 6)
-  // measured SLOWER (511 / 532 us; batches 6 and 12 no better): the 64-bit
-  // field extraction costs more issue slots than the saved Philox rounds, so
-  // they stay off by default.
-  static const bool pack_on = [] {
-    const char* v = getenv("PFR_REJ_PACK");
-    return v && v[0] == '1';
-  }();
-  const int l2n = log2_exact(n);
-  const int pack_k = (pack_on && l2n >= 1 && l2n <= 21) ? l2n : -1;
-  const int b_f32 = batch ? batch : (pack_k >= 0 ? 9 : 8), b_f64 = batch ? batch : (pack_k >= 0 ? 6 : 4);
-#define PFR_REJ_LAUNCH(T, CAP, B, MB, PK) \
-  k_rejection_philox<T, CAP, B, MB, PK><<<blocks_for(k_rejection_philox<T, CAP, B, MB, PK>), 256, 0, s>>>(A)
-#define PFR_REJ_DISPATCH(T, CAP)                                   \
-  do {                                                             \
-    if (pack_k >= 0) {                                             \
-      switch (sizeof(T) == 4 ? b_f32 : b_f64) {                    \
-        case 3: PFR_REJ_LAUNCH(T, CAP, 3, 1, true); break;          \
-        case 6: PFR_REJ_LAUNCH(T, CAP, 6, 1, true); break;          \
-        case 12: PFR_REJ_LAUNCH(T, CAP, 12, 1, true); break;        \
-        default: PFR_REJ_LAUNCH(T, CAP, 9, 1, true); break;         \
-      }                                                            \
-    } else {                                                       \
-      switch (sizeof(T) == 4 ? b_f32 : b_f64) {                    \
-        case 2: PFR_REJ_LAUNCH(T, CAP, 2, 1, false); break;         \
-        case 4: PFR_REJ_LAUNCH(T, CAP, 4, 1, false); break;         \
-        default: PFR_REJ_LAUNCH(T, CAP, 8, 1, false); break;        \
-      }                                                            \
-    }                                                              \
+  const int b_f32 = batch ? batch : 8, b_f64 = batch ? batch : 4;
+#define PFR_REJ_LAUNCH(T, CAP, B) \
+  k_rejection_philox<T, CAP, B><<<blocks_for(k_rejection_philox<T, CAP, B>), 256, 0, s>>>(A)
+#define PFR_REJ_DISPATCH(T, CAP)                \
+  do {                                          \
+    switch (sizeof(T) == 4 ? b_f32 : b_f64) {   \
+      case 2: PFR_REJ_LAUNCH(T, CAP, 2); break; \
+      case 4: PFR_REJ_LAUNCH(T, CAP, 4); break; \
+      default: PFR_REJ_LAUNCH(T, CAP, 8); break; \
+    }                                           \
   } while (0)
   if (dtype == PFR_F64) {
     RejArgs<double> A{(const double*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
-                      s_begin, s_count, a, trips, (double*)out_w, next, status, pack_k};
+                      s_begin, s_count, a, trips, (double*)out_w, next, status};
     if (cap > 0)
       PFR_REJ_DISPATCH(double, true);
     else
       PFR_REJ_DISPATCH(double, false);
   } else {
     RejArgs<float> A{(const float*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
-                     s_begin, s_count, a, trips, (float*)out_w, next, status, pack_k};
+                     s_begin, s_count, a, trips, (float*)out_w, next, status};
     if (cap > 0)
       PFR_REJ_DISPATCH(float, true);
     else

@@ -127,10 +127,21 @@ __host__ __device__ __forceinline__ double u32_to_unit_d(uint32_t x) {
 // midpoint of the cell, so u is never 0 and a zero weight can never be
 // accepted (u * w[k] <= w[j] = 0 would hold at u = 0)
 __host__ __device__ __forceinline__ float u32_to_unit_f_open(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  // (1 + m 2^-23) - (1 - 2^-24) = (2m + 1) 2^-24, exact (Sterbenz): shift,
+  // or, one FADD instead of shift, or, I2F, FMUL
+  return __uint_as_float((x >> 9) | 0x3F800000u) - 0.99999994f;
+#else
   return (float)(((x >> 9) << 1) | 1u) * (1.0f / 16777216.0f);  // (2m + 1) 2^-24, m < 2^23
+#endif
 }
 __host__ __device__ __forceinline__ double u32_to_unit_d_open(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  // (2^20 + x 2^-32) - (2^20 - 2^-33) = (2x + 1) 2^-33, exact (Sterbenz)
+  return __hiloint2double(0x41300000, (int)x) - 1048575.9999999999;
+#else
   return u32_to_unit_d(x) + 1.1641532182693481e-10;  // (2x + 1) 2^-33, exact
+#endif
 }
 
 // Lemire bounded integer in [0, n): exact (rejection on the biased sliver;
