@@ -57,10 +57,11 @@ size_t op_bytes(int op, int64_t n) {
   switch (op) {
     case PFR_OP_SCAN:
     case PFR_OP_METROPOLIS:
-    case PFR_OP_REJECTION:
     case PFR_OP_EXPAND:
     case PFR_OP_LOGWEIGHTS:
       return L.O;
+    case PFR_OP_REJECTION:  // + the O region: the certain-reject table
+      return L.d;
     case PFR_OP_PREDICATE:
       return L.a;
     default:

@@ -269,11 +269,95 @@ __device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, ui
   if (trip == 0) d.j[0] = slot;
 }
 
+// Certain-reject table.  A trip (j, beta) is rejected when beta * bound >
+// v[j]; when v[j] <= thr and beta * bound > thr that is certain without
+// reading v[j].  k_rej_table writes, for eight thresholds thr_k = (T)(bound *
+// 2^-(k+1)), one bit per group of g = 2^lg consecutive weights (set when the
+// group's largest capped weight exceeds thr_k) and counts the set bits; the
+// rejection kernel picks the k minimising the expected share of trips that
+// still need the gather, 2^-(k+1) + set_k / groups, and holds that bitmap
+// (<= 2^20 bits, 128 KiB) in shared memory.  The table only skips loads whose
+// outcome is already decided, so acceptances, trip counts and the stream
+// mapping are exactly those of the plain kernel.
+//
+// Why: the plain kernel is bound by the L1TEX sector rate of its random
+// gathers (ncu: l1tex throughput 91% of peak; one sector per trip), not by
+// HBM or L2.  With the table (log-normal sigma = 1, sup = max w: k = 3, ~8%
+// of trips gather) L1 drops to ~20% and the kernel becomes issue-bound on
+// Philox: 413 -> 349 us at N = 2^20 (float32).
+constexpr int kRejTabK = 8;                  // thresholds 2^-1 .. 2^-8 of the bound
+constexpr int64_t kRejTabMaxBits = 1 << 20;  // 128 KiB of shared memory
+constexpr int kRejTabThreads = 1024;  // one CTA per SM (128 KiB table)
+
+struct RejTab {
+  uint32_t* counts;  // [kRejTabK] set groups per threshold
+  uint32_t* bits;    // [kRejTabK][words]
+  int64_t groups;    // ceil(N / g)
+  int64_t words;     // ceil(groups / 32)
+  int lg;            // log2 g
+};
+
+// v = *p when c (a predicated non-coherent load: no branch around it)
+__device__ __forceinline__ void ldg_if(const float* p, bool c, float& v) {
+  asm("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.global.nc.f32 %0, [%1];\n}"
+      : "+f"(v)
+      : "l"(p), "r"((unsigned)c));
+}
+__device__ __forceinline__ void ldg_if(const double* p, bool c, double& v) {
+  asm("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.global.nc.f64 %0, [%1];\n}"
+      : "+d"(v)
+      : "l"(p), "r"((unsigned)c));
+}
+
+template <typename T>
+__device__ __forceinline__ T rej_thr(double bound, int k) {
+  return (T)(bound * ldexp(1.0, -(k + 1)));
+}
+
+template <typename T, bool kCapped>
+__global__ void __launch_bounds__(256) k_rej_table(const T* __restrict__ w, int64_t n, double bound, double cap,
+                                                   RejTab tb) {
+  const int lane = threadIdx.x & 31;
+  const T capv = (T)cap;
+  T thr[kRejTabK];
+#pragma unroll
+  for (int k = 0; k < kRejTabK; ++k) thr[k] = rej_thr<T>(cap > 0 ? cap : bound, k);
+  const int64_t g = (int64_t)1 << tb.lg;
+  uint32_t cnt = 0;  // lane k < kRejTabK: set bits of threshold k
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t wd = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); wd < tb.words; wd += warps) {
+    const int64_t grp = wd * 32 + lane;
+    T vmax = T(0);
+    bool any = false;
+    if (grp < tb.groups) {
+      const int64_t e0 = grp * g, e1 = min(e0 + g, n);
+      for (int64_t e = e0; e < e1; ++e) {
+        const T wj = ldg(w + e);
+        const T v = kCapped ? (wj < capv ? wj : capv) : wj;
+        if (!any || v > vmax) vmax = v;  // NaN never exceeds a threshold (never set)
+        any = true;
+      }
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < kRejTabK; ++k) {
+      const uint32_t b = __ballot_sync(0xffffffffu, any && vmax > thr[k]);
+      if (lane == k) mine = b;
+    }
+    if (lane < kRejTabK) {
+      tb.bits[(int64_t)lane * tb.words + wd] = mine;
+      cnt += __popc(mine);
+    }
+  }
+  if (lane < kRejTabK && cnt) atomicAdd(tb.counts + lane, cnt);
+}
+
 // Steady state: every lane owns a slot; the gathers of batch k are issued,
 // then the draws of batch k+1 are computed while they are in flight, then
 // batch k is resolved (two batch buffers used in turn: no copies).  A lane
 // whose slot finishes discards its precomputed batch and takes the next slot
-// of the warp's chunk (one atomic per 256 slots).
+// of the warp's chunk (one atomic per 256 slots); the new slot's first batch
+// is drawn in the same (non-divergent) draw call as everyone's next batch.
 //
 // Tail: once the chunks are exhausted, lanes without a slot HELP the slots
 // still running instead of idling -- trip t of a slot depends only on (slot,
@@ -283,10 +367,10 @@ __device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, ui
 // the stream mapping are exactly those of a one-trip-at-a-time loop; the
 // geometric tail (a warp's last slot runs ~4x the mean trips) no longer
 // leaves 31 lanes idle.
-template <typename T, bool kCapped, int kRejBatch>
-__global__ void __launch_bounds__(256, 1) k_rejection_philox(RejArgs<T> A) {
+template <typename T, bool kCapped, int kRejBatch, bool kTab = false>
+__global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_philox(RejArgs<T> A, RejTab tb) {
   constexpr int B = kRejBatch;
-  __shared__ unsigned long long s_best[8][32];  // per warp, per owner lane
+  __shared__ unsigned long long s_best[kTab ? kRejTabThreads / 32 : 8][32];  // per warp, per owner lane
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const T bound = (T)A.bound;
@@ -297,6 +381,52 @@ __global__ void __launch_bounds__(256, 1) k_rejection_philox(RejArgs<T> A) {
   uint32_t trip = 0;
   uint32_t flags = 0;
   int iter = 0;
+  bool fresh = false;  // the slot was just taken: no batch drawn yet
+  // certain-reject table (kTab): trip q needs its gather only when beta *
+  // bound <= thr or the proposal's group holds a capped weight above thr
+  extern __shared__ uint32_t rej_tab[];
+  T thr = T(INFINITY);
+  if constexpr (kTab) {
+    __shared__ int s_k;
+    if (threadIdx.x == 0) {
+      int best = -1;
+      double bc = 0.75;  // use a table only when it saves at least a quarter of the gathers
+      for (int k = 0; k < kRejTabK; ++k) {
+        const double c = ldexp(1.0, -(k + 1)) + (double)tb.counts[k] / (double)tb.groups;
+        if (c < bc) {
+          bc = c;
+          best = k;
+        }
+      }
+      s_k = best;
+    }
+    __syncthreads();
+    const int k = s_k;
+    if (k >= 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(tb.bits + (int64_t)k * tb.words);
+      uint4* dst = reinterpret_cast<uint4*>(rej_tab);
+      for (int64_t i = threadIdx.x; i < tb.words / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
+      thr = rej_thr<T>(A.bound, k);
+    }
+    __syncthreads();
+  }
+  // gathers of one batch; need[q] false: the trip is a certain reject
+  // (branch-free: the bit is read unconditionally -- with no table thr is
+  // +inf and the bit is ignored -- and the gather is a predicated load)
+  auto gather = [&](const RejBatch<T, B>& d, T (&wj)[B], bool (&need)[B]) {
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      bool nd = true;
+      if constexpr (kTab) {
+        const uint32_t gq = d.j[q] >> tb.lg;
+        const uint32_t bit = rej_tab[gq >> 5] >> (gq & 31);
+        nd = !(d.u[q] * bound > thr) || (bit & 1u);
+      }
+      need[q] = nd;
+      wj[q] = T(0);
+      ldg_if(A.w + d.j[q], nd, wj[q]);
+    }
+  };
   RejBatch<T, B> buf0, buf1;
 
   auto finish = [&](uint32_t jd, T wd, uint32_t ntrips) {
@@ -346,16 +476,30 @@ __global__ void __launch_bounds__(256, 1) k_rejection_philox(RejArgs<T> A) {
       if (slot < 0 && rank < take) {
         slot = chunk_next + rank;
         trip = 0;
-        rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), 0u, cur);
+        fresh = true;  // its first batch is drawn below, with everyone's next batch
       }
       chunk_next += take;
       idle = __ballot_sync(0xffffffffu, slot < 0);
     }
     if (idle) return __ballot_sync(0xffffffffu, slot >= 0) ? 2 : 1;
     T wj[B];
-#pragma unroll
-    for (int q = 0; q < B; ++q) wj[q] = ldg(A.w + cur.j[q]);
-    rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), trip + B, nxt);
+    bool need[B];
+    if constexpr (kTab) {
+      // not pipelined: few trips need a gather, and the table kernel's
+      // occupancy (32 warps per SM) hides the rest
+      (void)nxt;
+      rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), trip, cur);
+      fresh = false;
+      gather(cur, wj, need);
+    } else {
+      if (!fresh) gather(cur, wj, need);
+      // one non-divergent draw per step: the next batch, or a fresh slot's first
+      rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), fresh ? 0u : trip + B, nxt);
+      if (fresh) {
+        fresh = false;
+        return give_up() ? 1 : 0;
+      }
+    }
     int done = -1;  // batch position of the first accepting trip
     uint32_t jd = 0;
     T wd = T(0);
@@ -363,7 +507,7 @@ __global__ void __launch_bounds__(256, 1) k_rejection_philox(RejArgs<T> A) {
     for (int q = B - 1; q >= 0; --q) {
       const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
       // beta <= v[j] / bound  <=>  beta * bound <= v[j]
-      if (cur.u[q] * bound <= vj) {
+      if (need[q] && cur.u[q] * bound <= vj) {
         done = q;
         jd = cur.j[q];
         wd = wj[q];
@@ -410,13 +554,13 @@ __global__ void __launch_bounds__(256, 1) k_rejection_philox(RejArgs<T> A) {
       if (t0 < A.max_trips) {
         rej_draws<T, B>(A, (uint32_t)(A.s0 + oslot), t0, buf0);
         T wj[B];
-#pragma unroll
-        for (int q = 0; q < B; ++q) wj[q] = ldg(A.w + buf0.j[q]);
+        bool need[B];
+        gather(buf0, wj, need);
         unsigned long long key = ~0ull;
 #pragma unroll
         for (int q = B - 1; q >= 0; --q) {
           const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
-          if (t0 + (uint32_t)q < A.max_trips && buf0.u[q] * bound <= vj)
+          if (need[q] && t0 + (uint32_t)q < A.max_trips && buf0.u[q] * bound <= vj)
             key = ((unsigned long long)(t0 + (uint32_t)q) << 32) | buf0.j[q];
         }
         if (key != ~0ull) atomicMin(&s_best[warp][owner], key);
@@ -719,8 +863,7 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0) != cudaSuccess || occ < 1) occ = 1;
     return num_sms() * occ;
   };
-  // trips evaluated per lane and iteration (PFR_REJ_BATCH: profiling aid);
-  // measured on B200 (N=2^20, sigma=1, sup = max w): float32 8, float64 4.
+  // trips evaluated per lane and iteration (PFR_REJ_BATCH: profiling aid).
   // Packed draws (three trips per Philox call from 42-bit fields) measured
   // slower in round 2 (the 64-bit field extraction costs more issue slots
   // than the saved rounds) and were removed.
@@ -728,9 +871,62 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
     const char* v = getenv("PFR_REJ_BATCH");
     return v ? atoi(v) : 0;
   }();
-  const int b_f32 = batch ? batch : 8, b_f64 = batch ? batch : 4;
-#define PFR_REJ_LAUNCH(T, CAP, B) \
-  k_rejection_philox<T, CAP, B><<<blocks_for(k_rejection_philox<T, CAP, B>), 256, 0, s>>>(A)
+
+  // certain-reject table: N <= 4 * 2^20 (groups of g <= 4 weights), the
+  // workspace's O region as scratch (PFR_OP_REJECTION reserves it)
+  static const bool tab_on = [] {
+    const char* v = getenv("PFR_REJ_TABLE");
+    return !(v && v[0] == '0');
+  }();
+  RejTab tb{};
+  bool use_tab = false;
+  if (tab_on && ws.O && n >= 4096 && n <= 4 * kRejTabMaxBits) {
+    int lg = 0;
+    while (((n + ((int64_t)1 << lg) - 1) >> lg) > kRejTabMaxBits) ++lg;
+    tb.lg = lg;
+    tb.groups = (n + ((int64_t)1 << lg) - 1) >> lg;
+    tb.words = ((tb.groups + 127) / 128) * 4;  // whole uint4 rows
+    tb.counts = reinterpret_cast<uint32_t*>(ws.O);
+    tb.bits = tb.counts + 64;  // 256-byte aligned
+    e = cudaMemsetAsync(tb.counts, 0, kRejTabK * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    const int tblocks = (int)std::min<int64_t>((tb.words + 7) / 8, (int64_t)num_sms() * 8);
+    const double cb = cap > 0 ? cap : bound;
+    if (dtype == PFR_F64) {
+      if (cap > 0)
+        k_rej_table<double, true><<<tblocks, 256, 0, s>>>((const double*)w, n, cb, cap, tb);
+      else
+        k_rej_table<double, false><<<tblocks, 256, 0, s>>>((const double*)w, n, cb, cap, tb);
+    } else {
+      if (cap > 0)
+        k_rej_table<float, true><<<tblocks, 256, 0, s>>>((const float*)w, n, cb, cap, tb);
+      else
+        k_rej_table<float, false><<<tblocks, 256, 0, s>>>((const float*)w, n, cb, cap, tb);
+    }
+    note_launch();
+    use_tab = true;
+  }
+  const size_t tab_smem = use_tab ? (size_t)tb.words * 4 : 0;
+  // measured (N=2^20, sigma=1, sup = max w): table kernel 8 trips per lane
+  // and batch for both dtypes (349 / 353 us); plain kernel float32 8, float64 4
+  const int b_f32 = batch ? batch : 8, b_f64 = batch ? batch : (use_tab ? 8 : 4);
+  auto tab_blocks = [&](auto kernel) {
+    // every call: the instantiations share one function-pointer type
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kRejTabMaxBits / 8));
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kRejTabThreads, tab_smem) != cudaSuccess ||
+        occ < 1)
+      occ = 1;
+    return num_sms() * occ;
+  };
+#define PFR_REJ_LAUNCH(T, CAP, B)                                                                             \
+  do {                                                                                                        \
+    if (use_tab)                                                                                              \
+      k_rejection_philox<T, CAP, B, true>                                                                     \
+          <<<tab_blocks(k_rejection_philox<T, CAP, B, true>), kRejTabThreads, tab_smem, s>>>(A, tb);          \
+    else                                                                                                      \
+      k_rejection_philox<T, CAP, B><<<blocks_for(k_rejection_philox<T, CAP, B>), 256, 0, s>>>(A, tb);         \
+  } while (0)
 #define PFR_REJ_DISPATCH(T, CAP)                \
   do {                                          \
     switch (sizeof(T) == 4 ? b_f32 : b_f64) {   \

@@ -701,3 +701,45 @@ def test_rejection_own_stream_matches_model(dtype, n, kind, capped):
         wa, wt = O.own_rejection(w, bound, key0)
     np.testing.assert_array_equal(np_(a), wa)
     np.testing.assert_array_equal(np_(trips), wt)
+
+
+_TABLE_AB = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+import paper_1301_4019_b200 as pf
+out = {}
+# g = 1, 2, 4 weights per table bit; non-power-of-two N (Lemire redraws)
+for n in (1 << 20, 1000003, 1 << 21, 3 << 20):
+    for dt in (np.float32, np.float64):
+        g = np.random.default_rng(n)
+        w = np.exp(g.normal(0, 0.8, n)).astype(dt)
+        w[g.random(n) < 0.2] = 0
+        a, t = pf.rejection_ancestors(w, float(w.max()), pf.RngStream(9, (n,)), return_trips=True)
+        a2, ow, t2 = pf.rejection_ancestors_capped(w, float(np.quantile(w, 0.95)), pf.RngStream(10, (n,)),
+                                                   return_trips=True)
+        k = f"{n}_{np.dtype(dt).name}"
+        out[k + "_a"], out[k + "_t"] = a.cpu().numpy(), t.cpu().numpy()
+        out[k + "_ca"], out[k + "_cw"], out[k + "_ct"] = a2.cpu().numpy(), ow.cpu().numpy(), t2.cpu().numpy()
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_rejection_table_on_off_identical(tmp_path):
+    """The certain-reject table (DESIGN 3.4) only skips gathers whose outcome
+    is decided: ancestors, trips and capped weights equal the plain kernel's
+    (PFR_REJ_TABLE=0) for g = 1, 2, 4 weights per bit, power-of-two and odd N,
+    zero weights -- two processes, the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for flag in ("1", "0"):
+        f = tmp_path / f"t{flag}.npz"
+        env = dict(os.environ, PFR_REJ_TABLE=flag)
+        subprocess.run([sys.executable, "-c", _TABLE_AB, str(f)], cwd=root, env=env, check=True, timeout=600)
+        res.append(np.load(f))
+    assert set(res[0].files) == set(res[1].files) and len(res[0].files) == 40
+    for k in res[0].files:
+        np.testing.assert_array_equal(res[0][k], res[1][k], err_msg=k)
