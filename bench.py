@@ -459,7 +459,7 @@ def main():
     # deliveries' weights upload while earlier ones compute; results download
     # while later deliveries compute) -- the B200-native way to feed the API;
     # the device-only number is `value`.  The host link is the floor here:
-    # the same uploads and downloads with no compute take ~2.0 ms per step
+    # the same uploads and downloads with no compute take ~1.4 ms per step
     # (H2D and D2H share the link; reported as `link_only_ms`).
     host_w = {dt: weights[dt].cpu().pin_memory() for dt in DTYPES}
     host_c = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in jobs]
@@ -473,9 +473,21 @@ def main():
     h2d = sum(host_w[dt].numel() * host_w[dt].element_size() for (_, _, _, dt) in jobs)
     d2h = len(jobs) * n * 4
     e2e_ms = 0.0
-    # upload the weights of the longest deliveries first, so their compute
-    # overlaps the remaining uploads (device times of the sequential leg)
-    order = sorted(range(len(jobs)), key=lambda k: -statistics.mean(per_delivery[f"{jobs[k][1]}/{jobs[k][3]}"]))
+    # Schedule (measured on B200, N = 2^20): uploads take ~1.3 ms, the ten
+    # deliveries ~1.2 ms of concurrent compute, downloads ~0.8 ms, so the
+    # three must overlap.  The long deliveries (rejection, Metropolis) run
+    # one after another on one compute stream, the short ones on a second,
+    # and the upload order interleaves the two classes (f32 first: smaller
+    # uploads start compute sooner) so results start downloading while
+    # later weights still upload: 1.68 ms per step, against 1.9-2.0 ms with
+    # every delivery on its own stream (longest upload first) and 1.80 ms
+    # round-robin over two streams; stream priorities did not help.
+    names = [f"{jobs[k][1]}/{jobs[k][3]}" for k in range(len(jobs))]
+    seq = ["rejection/f32", "rejection/f64", "systematic/f32", "metropolis/f32", "stratified/f32",
+           "metropolis/f64", "multinomial/f32", "stratified/f64", "multinomial/f64", "systematic/f64"]
+    order = [names.index(x) for x in seq]
+    e2e_streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+    stream_of = {k: e2e_streams[0 if jobs[k][1] in ("rejection", "metropolis") else 1] for k in order}
 
     for s in range(args.warmup + args.steps):
         flush.zero_()
@@ -486,26 +498,32 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(copy_stream)
         up = {}
+        dbg = os.environ.get("PFR_BENCH_DEBUG") == "2"
+        tl = {}
         for k in order:
             dt = jobs[k][3]
             with torch.cuda.stream(copy_stream):
                 dev_w[k].copy_(host_w[dt], non_blocking=True)
-                ev = torch.cuda.Event()
+                ev = torch.cuda.Event(enable_timing=dbg)
                 ev.record(copy_stream)
             up[k] = ev
         for k in order:
             i, alg, j, dt = jobs[k]
-            sk = conc_streams[k]
+            sk = stream_of[k]
             sk.wait_event(up[k])
             with torch.cuda.stream(sk):
                 c = run_delivery(alg, dt, dev_w[k], pf.RngStream(50_000 + s, (rank, i, j)), dev_c[k])
-                done = torch.cuda.Event()
+                done = torch.cuda.Event(enable_timing=dbg)
                 done.record(sk)
             dk = down_streams[k]
             c.record_stream(dk)
             dk.wait_event(done)
             with torch.cuda.stream(dk):
                 host_c[k].copy_(c, non_blocking=True)
+                if dbg:
+                    fin = torch.cuda.Event(enable_timing=True)
+                    fin.record(dk)
+                    tl[k] = (up[k], done, fin)
         down_stream.wait_stream(copy_stream)
         for dk in down_streams:
             down_stream.wait_stream(dk)
@@ -513,6 +531,10 @@ def main():
         torch.cuda.synchronize()
         if os.environ.get("PFR_BENCH_DEBUG"):
             print(f"e2e step {s}: {e0.elapsed_time(e1):.3f} ms", file=sys.stderr, flush=True)
+            for k in (order if dbg else []):
+                u_, d_, f_ = tl[k]
+                print(f"   {jobs[k][1]:12s}/{jobs[k][3]}: uploaded {e0.elapsed_time(u_):.3f} computed "
+                      f"{e0.elapsed_time(d_):.3f} downloaded {e0.elapsed_time(f_):.3f}", file=sys.stderr, flush=True)
         if s >= args.warmup:
             e2e_ms += e0.elapsed_time(e1)
     # the link floor: the step's copies alone (uploads and downloads issued
@@ -597,18 +619,20 @@ def main():
                          "algorithmic_bytes": alg_bytes, "kernel_ms": dom_ms, "peak_source": peak_src,
                          "traffic_source": "profiles/r02_traffic.json (ncu, per launch)",
                          "note": "algorithmic bytes count every proposal's weight gather (SURVEY 8(d)); the "
-                                 "gathers hit L2 (N=2^20 weights are L2 resident): the kernel is bound by the "
-                                 "L2 random-sector rate and Philox issue, not by HBM (DESIGN.md 3.3-3.4)"},
+                                 "weights are L2 resident at N=2^20 and random gathers are bound by the L1TEX "
+                                 "sector rate, not HBM; rejection skips the gathers whose outcome a shared-memory "
+                                 "certain-reject table decides and is then bound by Philox issue (DESIGN.md 3.4)"},
             "sequential": {"ms_per_step": seq_ms_per_step, "value": seq_value, "gpu_launches": seq_launches,
                            "note": "the same ten deliveries one at a time, L2 flushed before each"},
             "gather_probes": probes,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "particles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms / args.steps, "link_only_ms": link_only_ms,
-                    "note": "pinned host buffers; uploads (longest delivery first) on one copy stream, each "
-                            "result downloaded on its own stream as soon as its delivery is done, pipelined with "
-                            "the ten deliveries (each on its own stream); link_only_ms = the same copies with no "
-                            "compute (the host-link floor)"},
+                    "note": "pinned host buffers; uploads on one copy stream in an order interleaving long "
+                            "and short deliveries, the long ones (rejection, Metropolis) computed in sequence on "
+                            "one stream and the short ones on another, each result downloaded on its own stream "
+                            "as soon as its delivery is done; link_only_ms = the same copies with no compute "
+                            "(the host-link floor)"},
             "gpu_launches": launches,
             "clocks": clocks,
             "per_delivery_ms": {k: sum(v) / len(v) for k, v in per_delivery.items()},
@@ -623,7 +647,9 @@ def main():
             line["roofline"]["gather_floor"] = {
                 "achieved_ggather_per_s": g, "peak_ggather_per_s": peak, "frac": g / peak,
                 "gathers_per_launch": gathers,
-                "peak_source": f"pfr_probe_gather on the same-size ({key}) L2-resident vector, this run"}
+                "peak_source": f"pfr_probe_gather on the same-size ({key}) L2-resident vector, this run",
+                "note": "gathers = proposals (trips) evaluated; frac > 1 means decided gathers were skipped "
+                        "(rejection's certain-reject table)" if alg == "rejection" else "gathers = N x B steps"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
