@@ -317,6 +317,7 @@ __device__ __forceinline__ T rej_thr(double bound, int k) {
 template <typename T, bool kCapped>
 __global__ void __launch_bounds__(256) k_rej_table(const T* __restrict__ w, int64_t n, double bound, double cap,
                                                    RejTab tb) {
+  constexpr int kW = 4;  // words per warp and pass: four independent loads in flight per lane
   const int lane = threadIdx.x & 31;
   const T capv = (T)cap;
   T thr[kRejTabK];
@@ -325,28 +326,48 @@ __global__ void __launch_bounds__(256) k_rej_table(const T* __restrict__ w, int6
   const int64_t g = (int64_t)1 << tb.lg;
   uint32_t cnt = 0;  // lane k < kRejTabK: set bits of threshold k
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t wd = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); wd < tb.words; wd += warps) {
-    const int64_t grp = wd * 32 + lane;
-    T vmax = T(0);
-    bool any = false;
-    if (grp < tb.groups) {
-      const int64_t e0 = grp * g, e1 = min(e0 + g, n);
-      for (int64_t e = e0; e < e1; ++e) {
-        const T wj = ldg(w + e);
-        const T v = kCapped ? (wj < capv ? wj : capv) : wj;
-        if (!any || v > vmax) vmax = v;  // NaN never exceeds a threshold (never set)
-        any = true;
+  for (int64_t w0 = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * kW; w0 < tb.words;
+       w0 += warps * kW) {
+    // group maximum of the capped weights; NaN never exceeds a threshold and
+    // is skipped (the plain kernel never accepts a NaN proposal either)
+    T vmax[kW];
+    if (tb.lg == 0) {  // one weight per bit: the four loads first
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        const int64_t e = (w0 + q) * 32 + lane;
+        vmax[q] = e < n ? ldg(w + e) : T(0);
+      }
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        const T v = kCapped ? (vmax[q] < capv ? vmax[q] : capv) : vmax[q];
+        vmax[q] = v > T(0) ? v : T(0);  // NaN -> 0
+      }
+    } else
+#pragma unroll
+    for (int q = 0; q < kW; ++q) {
+      vmax[q] = T(0);
+      const int64_t grp = (w0 + q) * 32 + lane;
+      if (grp < tb.groups) {
+        const int64_t e0 = grp * g, e1 = min(e0 + g, n);
+        for (int64_t e = e0; e < e1; ++e) {
+          const T wj = ldg(w + e);
+          const T v = kCapped ? (wj < capv ? wj : capv) : wj;
+          if (v > vmax[q]) vmax[q] = v;
+        }
       }
     }
-    uint32_t mine = 0;
 #pragma unroll
-    for (int k = 0; k < kRejTabK; ++k) {
-      const uint32_t b = __ballot_sync(0xffffffffu, any && vmax > thr[k]);
-      if (lane == k) mine = b;
-    }
-    if (lane < kRejTabK) {
-      tb.bits[(int64_t)lane * tb.words + wd] = mine;
-      cnt += __popc(mine);
+    for (int q = 0; q < kW; ++q) {
+      uint32_t mine = 0;
+#pragma unroll
+      for (int k = 0; k < kRejTabK; ++k) {
+        const uint32_t bk = __ballot_sync(0xffffffffu, vmax[q] > thr[k]);
+        if (lane == k) mine = bk;
+      }
+      if (lane < kRejTabK && w0 + q < tb.words) {
+        tb.bits[(int64_t)lane * tb.words + w0 + q] = mine;
+        cnt += __popc(mine);
+      }
     }
   }
   if (lane < kRejTabK && cnt) atomicAdd(tb.counts + lane, cnt);
@@ -890,7 +911,7 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
     tb.bits = tb.counts + 64;  // 256-byte aligned
     e = cudaMemsetAsync(tb.counts, 0, kRejTabK * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
-    const int tblocks = (int)std::min<int64_t>((tb.words + 7) / 8, (int64_t)num_sms() * 8);
+    const int tblocks = (int)std::min<int64_t>((tb.words + 31) / 32, (int64_t)num_sms() * 8);
     const double cb = cap > 0 ? cap : bound;
     if (dtype == PFR_F64) {
       if (cap > 0)

@@ -1,4 +1,4 @@
-"""Launch the north-star paths at N=2^24 f32 for ncu (a few reps each)."""
+"""Launch the north-star paths at N=2^24 f32 (DT=f64: float64 weights) for ncu (a few reps each)."""
 import os
 import sys
 
@@ -14,7 +14,7 @@ n = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 24
 pf.config.check = False
 g = np.random.default_rng(1)
 lw = g.normal(0, 1, n)
-w = torch.from_numpy(np.exp(lw - lw.max()).astype(np.float32)).cuda()
+w = torch.from_numpy(np.exp(lw - lw.max()).astype(np.float64 if os.environ.get("DT") == "f64" else np.float32)).cuda()
 c = torch.empty(n, dtype=torch.int32, device="cuda")
 for r in range(reps):
     if which in ("all", "systematic"):
