@@ -245,11 +245,14 @@ template <typename T, int B>
 struct RejBatch {
   uint32_t j[B];
   T u[B];
+  uint32_t big;  // bit q: trip q's uniform exceeds the table's 2^-(k+1) (raw word >= 2^(31-k))
 };
 
 template <typename T, int B>
-__device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, uint32_t trip, RejBatch<T, B>& d) {
+__device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, uint32_t trip, RejBatch<T, B>& d,
+                                          uint32_t ubig = 0) {
   const uint32_t nn = (uint32_t)A.n;
+  d.big = 0;
 #pragma unroll
   for (int q = 0; q < B / 2; ++q) {
     uint32_t o[4];
@@ -264,16 +267,22 @@ __device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, ui
         d.u[2 * q + h] = u32_to_unit_f_open(o[2 * h + 1]);
       else
         d.u[2 * q + h] = u32_to_unit_d_open(o[2 * h + 1]);
+      // u = (2m+1) 2^-24 (f32, m = x >> 9) or (2x+1) 2^-33 (f64) exceeds
+      // 2^-(k+1) exactly when x >= 2^(31-k): one integer compare
+      if (ubig && o[2 * h + 1] >= ubig) d.big |= 1u << (2 * q + h);
     }
   }
   if (trip == 0) d.j[0] = slot;
 }
 
 // Certain-reject table.  A trip (j, beta) is rejected when beta * bound >
-// v[j]; when v[j] <= thr and beta * bound > thr that is certain without
-// reading v[j].  k_rej_table writes, for eight thresholds thr_k = (T)(bound *
-// 2^-(k+1)), one bit per group of g = 2^lg consecutive weights (set when the
-// group's largest capped weight exceeds thr_k) and counts the set bits; the
+// v[j]; when v[j] < thr and beta > 2^-(k+1) that is certain without reading
+// v[j] (thr = (T)(bound 2^-(k+1)) = (T)bound 2^-(k+1) exactly, so the exact
+// product beta * bound exceeds thr and its rounding is >= thr > v[j]; beta >
+// 2^-(k+1) is one integer compare on the raw Philox word).  k_rej_table
+// writes, for eight thresholds thr_k, one bit per group of g = 2^lg
+// consecutive weights (set when the group's largest capped weight is >=
+// thr_k) and counts the set bits; the
 // rejection kernel picks the k minimising the expected share of trips that
 // still need the gather, 2^-(k+1) + set_k / groups, and holds that bitmap
 // (<= 2^20 bits, 128 KiB) in shared memory.  The table only skips loads whose
@@ -311,7 +320,9 @@ __device__ __forceinline__ void ldg_if(const double* p, bool c, double& v) {
 
 template <typename T>
 __device__ __forceinline__ T rej_thr(double bound, int k) {
-  return (T)(bound * ldexp(1.0, -(k + 1)));
+  // in T, like the kernel's product u * (T)bound: rounding is monotone, so
+  // u > 2^-(k+1) gives fl(u * (T)bound) >= fl((T)bound * 2^-(k+1)) = thr
+  return (T)bound * (T)ldexp(1.0, -(k + 1));
 }
 
 template <typename T, bool kCapped>
@@ -361,7 +372,7 @@ __global__ void __launch_bounds__(256) k_rej_table(const T* __restrict__ w, int6
       uint32_t mine = 0;
 #pragma unroll
       for (int k = 0; k < kRejTabK; ++k) {
-        const uint32_t bk = __ballot_sync(0xffffffffu, vmax[q] > thr[k]);
+        const uint32_t bk = __ballot_sync(0xffffffffu, vmax[q] >= thr[k]);
         if (lane == k) mine = bk;
       }
       if (lane < kRejTabK && w0 + q < tb.words) {
@@ -406,7 +417,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
   // certain-reject table (kTab): trip q needs its gather only when beta *
   // bound <= thr or the proposal's group holds a capped weight above thr
   extern __shared__ uint32_t rej_tab[];
-  T thr = T(INFINITY);
+  uint32_t ubig = 0;  // 2^(31-k) with a table, 0: none
   if constexpr (kTab) {
     __shared__ int s_k;
     if (threadIdx.x == 0) {
@@ -427,13 +438,13 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
       const uint4* src = reinterpret_cast<const uint4*>(tb.bits + (int64_t)k * tb.words);
       uint4* dst = reinterpret_cast<uint4*>(rej_tab);
       for (int64_t i = threadIdx.x; i < tb.words / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
-      thr = rej_thr<T>(A.bound, k);
+      ubig = 1u << (31 - k);
     }
     __syncthreads();
   }
   // gathers of one batch; need[q] false: the trip is a certain reject
-  // (branch-free: the bit is read unconditionally -- with no table thr is
-  // +inf and the bit is ignored -- and the gather is a predicated load)
+  // (branch-free: the bit is read unconditionally -- with no table `big` is
+  // 0 and the bit is ignored -- and the gather is a predicated load)
   auto gather = [&](const RejBatch<T, B>& d, T (&wj)[B], bool (&need)[B]) {
 #pragma unroll
     for (int q = 0; q < B; ++q) {
@@ -441,7 +452,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
       if constexpr (kTab) {
         const uint32_t gq = d.j[q] >> tb.lg;
         const uint32_t bit = rej_tab[gq >> 5] >> (gq & 31);
-        nd = !(d.u[q] * bound > thr) || (bit & 1u);
+        nd = ((~d.big >> q) | bit) & 1u;
       }
       need[q] = nd;
       wj[q] = T(0);
@@ -509,7 +520,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
       // not pipelined: few trips need a gather, and the table kernel's
       // occupancy (32 warps per SM) hides the rest
       (void)nxt;
-      rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), trip, cur);
+      rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), trip, cur, ubig);
       fresh = false;
       gather(cur, wj, need);
     } else {
@@ -573,7 +584,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
       __syncwarp();
       const uint32_t t0 = otrip + (uint32_t)(h * B);
       if (t0 < A.max_trips) {
-        rej_draws<T, B>(A, (uint32_t)(A.s0 + oslot), t0, buf0);
+        rej_draws<T, B>(A, (uint32_t)(A.s0 + oslot), t0, buf0, ubig);
         T wj[B];
         bool need[B];
         gather(buf0, wj, need);
