@@ -244,15 +244,21 @@ constexpr int kRejChunk = 256;
 template <typename T, int B>
 struct RejBatch {
   uint32_t j[B];
-  T u[B];
-  uint32_t big;  // bit q: trip q's uniform exceeds the table's 2^-(k+1) (raw word >= 2^(31-k))
+  uint32_t x[B];  // raw uniform words: u = unit(x) (rej_u), and u > 2^-(k+1) iff x >= 2^(31-k)
 };
 
+// the acceptance uniform of a raw word (open interval, cell midpoints)
+template <typename T>
+__device__ __forceinline__ T rej_u(uint32_t x) {
+  if constexpr (sizeof(T) == 4)
+    return u32_to_unit_f_open(x);
+  else
+    return u32_to_unit_d_open(x);
+}
+
 template <typename T, int B>
-__device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, uint32_t trip, RejBatch<T, B>& d,
-                                          uint32_t ubig = 0) {
+__device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, uint32_t trip, RejBatch<T, B>& d) {
   const uint32_t nn = (uint32_t)A.n;
-  d.big = 0;
 #pragma unroll
   for (int q = 0; q < B / 2; ++q) {
     uint32_t o[4];
@@ -263,13 +269,7 @@ __device__ __forceinline__ void rej_draws(const RejArgs<T>& A, uint32_t slot, ui
       d.j[2 * q + h] = A.threshold == 0 ? __umulhi(o[2 * h], nn)
                                         : bounded_u32(o[2 * h], nn, A.threshold, slot, trip + 2 * q + h,
                                                       kTagRejection, A.k0, A.k1);
-      if constexpr (sizeof(T) == 4)
-        d.u[2 * q + h] = u32_to_unit_f_open(o[2 * h + 1]);
-      else
-        d.u[2 * q + h] = u32_to_unit_d_open(o[2 * h + 1]);
-      // u = (2m+1) 2^-24 (f32, m = x >> 9) or (2x+1) 2^-33 (f64) exceeds
-      // 2^-(k+1) exactly when x >= 2^(31-k): one integer compare
-      if (ubig && o[2 * h + 1] >= ubig) d.big |= 1u << (2 * q + h);
+      d.x[2 * q + h] = o[2 * h + 1];
     }
   }
   if (trip == 0) d.j[0] = slot;
@@ -417,7 +417,8 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
   // certain-reject table (kTab): trip q needs its gather only when beta *
   // bound <= thr or the proposal's group holds a capped weight above thr
   extern __shared__ uint32_t rej_tab[];
-  uint32_t ubig = 0;  // 2^(31-k) with a table, 0: none
+  uint32_t ubig = 0;   // 2^(31-k) with a table
+  uint32_t notab = 1;  // 1: no table chosen (every trip gathers)
   if constexpr (kTab) {
     __shared__ int s_k;
     if (threadIdx.x == 0) {
@@ -439,6 +440,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
       uint4* dst = reinterpret_cast<uint4*>(rej_tab);
       for (int64_t i = threadIdx.x; i < tb.words / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
       ubig = 1u << (31 - k);
+      notab = 0;
     }
     __syncthreads();
   }
@@ -452,7 +454,9 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
       if constexpr (kTab) {
         const uint32_t gq = d.j[q] >> tb.lg;
         const uint32_t bit = rej_tab[gq >> 5] >> (gq & 31);
-        nd = ((~d.big >> q) | bit) & 1u;
+        // u = (2m+1) 2^-24 (f32, m = x >> 9) or (2x+1) 2^-33 (f64) exceeds
+        // 2^-(k+1) exactly when x >= 2^(31-k) (ubig)
+        nd = (d.x[q] < ubig) | (bit & 1u) | notab;
       }
       need[q] = nd;
       wj[q] = T(0);
@@ -520,7 +524,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
       // not pipelined: few trips need a gather, and the table kernel's
       // occupancy (32 warps per SM) hides the rest
       (void)nxt;
-      rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), trip, cur, ubig);
+      rej_draws<T, B>(A, (uint32_t)(A.s0 + slot), trip, cur);
       fresh = false;
       gather(cur, wj, need);
     } else {
@@ -539,7 +543,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
     for (int q = B - 1; q >= 0; --q) {
       const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
       // beta <= v[j] / bound  <=>  beta * bound <= v[j]
-      if (need[q] && cur.u[q] * bound <= vj) {
+      if (need[q] && rej_u<T>(cur.x[q]) * bound <= vj) {
         done = q;
         jd = cur.j[q];
         wd = wj[q];
@@ -584,7 +588,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
       __syncwarp();
       const uint32_t t0 = otrip + (uint32_t)(h * B);
       if (t0 < A.max_trips) {
-        rej_draws<T, B>(A, (uint32_t)(A.s0 + oslot), t0, buf0, ubig);
+        rej_draws<T, B>(A, (uint32_t)(A.s0 + oslot), t0, buf0);
         T wj[B];
         bool need[B];
         gather(buf0, wj, need);
@@ -592,7 +596,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
 #pragma unroll
         for (int q = B - 1; q >= 0; --q) {
           const T vj = kCapped ? (wj[q] < capv ? wj[q] : capv) : wj[q];
-          if (need[q] && t0 + (uint32_t)q < A.max_trips && buf0.u[q] * bound <= vj)
+          if (need[q] && t0 + (uint32_t)q < A.max_trips && rej_u<T>(buf0.x[q]) * bound <= vj)
             key = ((unsigned long long)(t0 + (uint32_t)q) << 32) | buf0.j[q];
         }
         if (key != ~0ull) atomicMin(&s_best[warp][owner], key);
