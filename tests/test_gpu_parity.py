@@ -631,6 +631,25 @@ def test_fused_metropolis_delivery_equals_two_calls(dtype, n):
     assert s == s2
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n, sigma, b, zeros", [(1 << 22, 1.0, 32, 0.0), (70001, 1.0, 7, 0.3), (1 << 20, 0.3, 5, 0.0),
+                                                (4096, 2.0, 32, 0.5)])
+def test_fused_metropolis_delivery_more_cases(dtype, n, sigma, b, zeros):
+    """The fused Metropolis delivery (claims made by the chains) against the
+    plain chains + permute at more shapes: 2^22, odd N and odd B, zero
+    weights, flat and peaked weights."""
+    g = np.random.default_rng(n + b)
+    wn = np.exp(g.normal(0, sigma, n))
+    wn[g.random(n) < zeros] = 0.0
+    w = torch.from_numpy(wn.astype(dtype)).cuda()
+    cfg = pf.ResamplerConfig("metropolis", b=b)
+    c, s = pf.deliver(w, cfg, pf.RngStream(21, (n,)), return_max_steps=True, index_dtype=torch.int32)
+    a = pf.metropolis_ancestors(w, b, pf.RngStream(21, (n,)), index_dtype=torch.int32)
+    c2, s2 = pf.permute_parallel(a, return_max_steps=True, index_dtype=torch.int32)
+    np.testing.assert_array_equal(np_(c), np_(c2))
+    assert s == s2
+
+
 @pytest.mark.parametrize("alg", ["systematic", "metropolis"])
 def test_config4_full_size_properties(alg):
     """BASELINE config 4 at its full size, N = 2^28 float32 on one GPU:
