@@ -652,67 +652,128 @@ __global__ void k_multinomial_numpy(const T* __restrict__ W, int64_t n, Key2x64 
   }
 }
 
-// own stream sorted multinomial: exponential spacings E_k = -log(U_k), k in [0, N]
-__global__ void k_exponentials(int64_t n, uint32_t k0, uint32_t k1, double* __restrict__ E) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= n; k += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t o[4];
-    philox4x32_10((uint32_t)k, (uint32_t)(k >> 32), kTagMultinomial, 0, k0, k1, o);
-    const uint64_t x = ((uint64_t)o[0] << 32) | o[1];
-    const double u = ((double)(x >> 11) + 1.0) * (1.0 / 9007199254740992.0);  // (0, 1]
-    E[k] = -log(u);
+// ---------------------------------------------------------------------------
+// Own-stream multinomial without materialised spacings.  U_k = S_k / S_N *
+// W[N-1] with S_k = E_0 + ... + E_k, E_k = -log(u_k) from Philox counter k
+// (the k_exponentials draws).  The spacings are never stored: pass 1 sums
+// each 4096-element tile of E (regenerated), one CTA scans the tile sums,
+// and the merge regenerates its tile's E, scans it with the SAME code as
+// pass 1 and adds the tile prefix.  S_k = max(P_t + L_k, S_last(t-1)): the
+// clamp keeps U sorted across a tile boundary where the tile-prefix scan
+// rounds an ulp below the previous tile's last value (a tile adds ~4096, so
+// one clamp never reaches past one boundary).  CTA t then writes a[k] =
+// min(N-1, #{j : W[j] < U_k}) for its own U tile: binary searches over W
+// staged in shared memory when the tile's W run fits.
+constexpr int kMnTile = 4096;  // 256 threads x 16 spacings
+
+__device__ __forceinline__ double mn_spacing(int64_t k, uint32_t k0, uint32_t k1) {
+  uint32_t o[4];
+  philox4x32_10((uint32_t)k, (uint32_t)(k >> 32), kTagMultinomial, 0, k0, k1, o);
+  const uint64_t x = ((uint64_t)o[0] << 32) | o[1];
+  const double u = ((double)(x >> 11) + 1.0) * (1.0 / 9007199254740992.0);  // (0, 1]
+  return -log(u);
+}
+
+// inclusive scan of one tile's 4096 spacings e (thread tid holds indices
+// 16 tid .. 16 tid + 15; past N: 0), fixed association: thread-serial over
+// 16, Kogge-Stone over the warp's thread totals, serial fold of the 8 warp
+// totals.  L[i] = inclusive value; returns the tile's last inclusive value.
+__device__ double mn_tile_scan(const double (&e)[16], double (&L)[16], double* s_warp) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double run = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    run += e[i];
+    L[i] = run;
+  }
+  double incl = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = 0.0;
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  double wex = 0.0, tot = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q == warp) wex = tot;
+    tot += s_warp[q];
+  }
+  const double base = wex + excl;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) L[i] = base + L[i];
+  __syncthreads();  // s_warp reused below
+  if (tid == 255) s_warp[8] = L[15];
+  __syncthreads();
+  const double last = s_warp[8];
+  __syncthreads();
+  return last;
+}
+
+// pass 1: the spacings E_k (k <= N) into E, and each tile's scan total
+__global__ void __launch_bounds__(256) k_mn_tilesum(int64_t n, uint32_t k0, uint32_t k1, int64_t tiles,
+                                                    double* __restrict__ E, double* __restrict__ tsum) {
+  __shared__ double s_warp[9];
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t e0 = t * kMnTile + (int64_t)threadIdx.x * 16;
+    double e[16], L[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) e[i] = e0 + i <= n ? mn_spacing(e0 + i, k0, k1) : 0.0;
+    if (e0 + 16 <= n + 1) {
+      double2* dst = reinterpret_cast<double2*>(E + e0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[i] = make_double2(e[2 * i], e[2 * i + 1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (e0 + i <= n) E[e0 + i] = e[i];
+    }
+    const double tot = mn_tile_scan(e, L, s_warp);
+    if (threadIdx.x == 0) tsum[t] = tot;
   }
 }
 
-// sorted uniforms U_(k) = S_k / S_N times W[N-1]; a[k] = lower_bound(W, .)
-template <typename T>
-__global__ void k_multinomial_sorted(const T* __restrict__ W, int64_t n, const double* __restrict__ S,
-                                     int32_t* __restrict__ out) {
-  const double total = (double)W[n - 1];
-  const double norm = S[n];
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const double u = S[k] / norm * total;
-    out[k] = (int32_t)lower_bound_dev(W, n, u);
+// exclusive prefix of the tile sums, one CTA (1024 threads, fixed
+// association): P[t], and P[tiles] = S_N = P[last] + tsum[last]
+__global__ void __launch_bounds__(1024) k_mn_tileprefix(const double* __restrict__ tsum, int64_t tiles,
+                                                        double* __restrict__ P) {
+  __shared__ double s_w[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t per = (tiles + 1023) / 1024;
+  const int64_t t0 = (int64_t)tid * per, t1 = min(t0 + per, tiles);
+  double run = 0.0;
+  for (int64_t t = t0; t < t1; ++t) run += tsum[t];
+  double incl = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
   }
-}
-
-// Merge path of the sorted uniforms U[k] = S[k]/S[N] * W[N-1] against W:
-// a[k] = min(N-1, #{j : W[j] < U[k]}) (searchsorted left, float64 compare as
-// numpy promotes, primitives.py:91-106).  CTA c owns merge diagonals
-// [c*D, (c+1)*D) of the 2N-long merge of W and U (W first on ties only when
-// strictly smaller), stages its W and U runs in shared memory, and every
-// thread merges 16 consecutive positions: O(N) coalesced work instead of N
-// binary searches.
-constexpr int kMergeD = 4096;
-
-template <typename T>
-__device__ __forceinline__ double mm_u(const double* __restrict__ S, int64_t k, double norm, double total) {
-  return S[k] / norm * total;
-}
-
-// number of W elements among the first d merge positions
-template <typename T>
-__device__ int64_t mm_split(const T* __restrict__ W, const double* __restrict__ S, int64_t n, int64_t d, double norm,
-                            double total) {
-  int64_t lo = d > n ? d - n : 0, hi = d < n ? d : n;
-  while (lo < hi) {
-    const int64_t i = (lo + hi + 1) >> 1;  // try taking i W elements: needs W[i-1] < U[d-i]
-    const int64_t jj = d - i;
-    if (jj >= n || (double)W[i - 1] < mm_u<T>(S, jj, norm, total))
-      lo = i;
-    else
-      hi = i - 1;
+  double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = 0.0;
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  double wex = 0.0, tot = 0.0;
+  for (int q = 0; q < 32; ++q) {
+    if (q == warp) wex = tot;
+    tot += s_w[q];
   }
-  return lo;
+  double acc = wex + excl;
+  for (int64_t t = t0; t < t1; ++t) {
+    P[t] = acc;
+    acc += tsum[t];
+  }
+  if (t1 == tiles && t0 < t1) P[tiles] = P[tiles - 1] + tsum[tiles - 1];
 }
 
-// number of W elements strictly below u (the merge takes W first only when
-// W[i] < U[j]: ties go to the uniform, as lower_bound)
 template <typename T>
-__device__ int64_t mm_below(const T* __restrict__ W, int64_t n, double u) {
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
+__device__ __forceinline__ int64_t mn_below_range(const T* __restrict__ W, int64_t lo, int64_t hi, double u) {
+  while (lo < hi) {  // first j in [lo, hi) with W[j] >= u
     const int64_t mid = (lo + hi) >> 1;
-    if ((double)W[mid] < u)
+    if ((double)ldg(W + mid) < u)
       lo = mid + 1;
     else
       hi = mid;
@@ -720,64 +781,133 @@ __device__ int64_t mm_below(const T* __restrict__ W, int64_t n, double u) {
   return lo;
 }
 
-// Merge of W with the sorted uniforms U[j] = S[j] / S[N] * W[N-1] along the
-// merge path; out[j - s0] = parent of slot j for the slots [s0, s1) (a
-// rank's share: the union over ranks is the full result).  The slots' merge
-// diagonals are [s0 + below(U[s0]), s1 + below(U[s1])) (2N for s1 = N);
-// CTAs stride over kMergeD-diagonal chunks of that range.
+// U at a tile's first index (S clamped to the previous tile's last value),
+// exactly as k_mn_merge computes it: thread 0's L[0] = (0 + 0) + (0 + e0)
+__device__ __forceinline__ double mn_first_u(const double* __restrict__ E, const double* __restrict__ P,
+                                             const double* __restrict__ tsum, int64_t t, double scale) {
+  const double l0 = (0.0 + 0.0) + (0.0 + E[t * kMnTile]);
+  const double sk = P[t] + l0;
+  const double prev = t > 0 ? P[t - 1] + tsum[t - 1] : 0.0;
+  return (sk > prev ? sk : prev) * scale;
+}
+
+// U = S * (W[N-1] / S_N): one multiply per uniform (monotone in S)
 template <typename T>
-__global__ void __launch_bounds__(256) k_multinomial_merge(const T* __restrict__ W, int64_t n,
-                                                           const double* __restrict__ S, int64_t s0, int64_t s1,
-                                                           int32_t* __restrict__ out) {
-  __shared__ double sbuf[kMergeD];  // the CTA's W run, then its U run (nw + nu = D)
-  __shared__ int64_t split[2];
-  __shared__ int64_t range[2];
-  const double total = (double)W[n - 1];
-  const double norm = S[n];
-  if (threadIdx.x < 2) {
-    const int64_t sj = threadIdx.x ? s1 : s0;
-    range[threadIdx.x] = sj >= n ? 2 * n : sj + mm_below<T>(W, n, mm_u<T>(S, sj, norm, total));
+__device__ __forceinline__ double mn_scale(const T* __restrict__ W, int64_t n, const double* __restrict__ P,
+                                           int64_t tiles) {
+  return (double)ldg(W + n - 1) / P[tiles];
+}
+
+// every tile's W run start: lo[t - tb] = #{W < U_first(t)} for t in [tb, te]
+// (one thread each: all the binary searches in flight together)
+template <typename T>
+__global__ void __launch_bounds__(256) k_mn_search(const T* __restrict__ W, int64_t n, const double* __restrict__ E,
+                                                   const double* __restrict__ P, const double* __restrict__ tsum,
+                                                   int64_t tiles, int64_t tb, int64_t te, int64_t* __restrict__ lo) {
+  const int64_t t = tb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > te) return;
+  if (t * kMnTile >= n) {
+    lo[t - tb] = n;
+    return;
   }
-  __syncthreads();
-  const int64_t D0 = range[0], D1 = range[1];
-  for (int64_t d0 = D0 + (int64_t)blockIdx.x * kMergeD; d0 < D1; d0 += (int64_t)gridDim.x * kMergeD) {
-    const int64_t d1 = min(d0 + kMergeD, D1);
-    __syncthreads();
-    if (threadIdx.x < 2) split[threadIdx.x] = mm_split<T>(W, S, n, threadIdx.x ? d1 : d0, norm, total);
-    __syncthreads();
-    const int64_t i0 = split[0], i1 = split[1];
-    const int64_t j0 = d0 - i0, j1 = d1 - i1;
-    const int nw = (int)(i1 - i0), nu = (int)(j1 - j0);
-    double* sw = sbuf;
-    double* su = sbuf + nw;
-    for (int t = threadIdx.x; t < nw; t += blockDim.x) sw[t] = (double)W[i0 + t];
-    for (int t = threadIdx.x; t < nu; t += blockDim.x) su[t] = mm_u<T>(S, j0 + t, norm, total);
-    __syncthreads();
-    // per-thread split inside the CTA's run
-    const int per = kMergeD / 256;
-    const int td = threadIdx.x * per;
-    if (td < nw + nu) {
-      int lo = td > nu ? td - nu : 0, hi = td < nw ? td : nw;
-      while (lo < hi) {
-        const int i = (lo + hi + 1) >> 1;
-        const int jj = td - i;
-        if (jj >= nu || sw[i - 1] < su[jj])
-          lo = i;
-        else
-          hi = i - 1;
+  lo[t - tb] = mn_below_range<T>(W, 0, n, mn_first_u(E, P, tsum, t, mn_scale<T>(W, n, P, tiles)));
+}
+
+constexpr int kMnStage = 5632;  // W run staged in shared memory (elements; static smem < 48 KiB)
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_mn_merge(const T* __restrict__ W, int64_t n, const double* __restrict__ E,
+                                                  const double* __restrict__ P, const double* __restrict__ tsum,
+                                                  const int64_t* __restrict__ lo_t, int64_t tiles, int64_t s0,
+                                                  int64_t s1, int32_t* __restrict__ out) {
+  __shared__ double s_warp[9];
+  __shared__ T sw[kMnStage];
+  const double scale = mn_scale<T>(W, n, P, tiles);
+  const int64_t tb = s0 / kMnTile, te = (s1 + kMnTile - 1) / kMnTile;  // U tiles covering [s0, s1)
+  for (int64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
+    const int64_t k0i = t * kMnTile + (int64_t)threadIdx.x * 16;  // this thread's first index
+    double e[16], L[16];
+    if (k0i + 16 <= n + 1) {
+      const double2* src = reinterpret_cast<const double2*>(E + k0i);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double2 v = __ldcs(src + i);
+        e[2 * i] = v.x;
+        e[2 * i + 1] = v.y;
       }
-      int i = lo, j = td - lo;
-      const int te = min(td + per, nw + nu);
-      for (int pos = td; pos < te; ++pos) {
-        if (j >= nu || (i < nw && sw[i] < su[j])) {
-          ++i;  // a W element: strictly below the next uniform
-        } else {
-          const int64_t a = i0 + i;
-          out[j0 + j - s0] = (int32_t)(a < n ? a : n - 1);
-          ++j;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) e[i] = k0i + i <= n ? E[k0i + i] : 0.0;
+    }
+    mn_tile_scan(e, L, s_warp);
+    const double pt = P[t];
+    const double prev_last = t > 0 ? P[t - 1] + tsum[t - 1] : 0.0;
+    double u[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double sk = pt + L[i];
+      u[i] = (sk > prev_last ? sk : prev_last) * scale;
+    }
+    // the tile's W run [lo(t), lo(t+1) + 1): U_last(t) <= U_first(t+1)
+    const int64_t lo = lo_t[t - tb], hi = max(lo, min(n, lo_t[t - tb + 1] + 1));
+    const bool staged = hi - lo <= kMnStage;  // CTA-uniform
+    if (staged) {
+      // eight independent loads in flight per thread, then the stores
+      for (int64_t j0 = lo + threadIdx.x; j0 < hi; j0 += 8 * (int64_t)blockDim.x) {
+        T v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int64_t j = j0 + r * (int64_t)blockDim.x;
+          v[r] = j < hi ? ldg(W + j) : T(0);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int64_t j = j0 + r * (int64_t)blockDim.x;
+          if (j < hi) sw[j - lo] = v[r];
         }
       }
     }
+    __syncthreads();
+    if (staged) {
+      // 32-bit positions inside the staged run
+      const int m = (int)(hi - lo);
+      int a = 0, b = m;
+      while (a < b) {
+        const int mid = (a + b) >> 1;
+        if ((double)sw[mid] < u[0])
+          a = mid + 1;
+        else
+          b = mid;
+      }
+      const int kmax = (int)min((int64_t)16, n - k0i);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i >= kmax) break;
+        // the walk advances ~1 W per uniform: test four positions at once
+        // (independent loads), repeat only when all four are below u
+        while (true) {
+          int adv = 0;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) adv += (a + r < m && (double)sw[a + r] < u[i]) ? 1 : 0;
+          a += adv;
+          if (adv < 4) break;
+        }
+        const int64_t k = k0i + i;
+        const int64_t pos = lo + a;
+        if (k >= s0 && k < s1) out[k - s0] = (int32_t)(pos < n ? pos : n - 1);
+      }
+      __syncthreads();
+      continue;
+    }
+    int64_t pos = mn_below_range<T>(W, lo, hi, u[0]);  // #{W < u[0]}
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t k = k0i + i;
+      if (k >= n) break;
+      while (pos < hi && (double)ldg(W + pos) < u[i]) ++pos;
+      if (k >= s0 && k < s1) out[k - s0] = (int32_t)(pos < n ? pos : n - 1);
+    }
+    __syncthreads();
   }
 }
 
@@ -1037,19 +1167,37 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
     note_launch();
   } else {
     const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
-    k_exponentials<<<grid_for(n + 1, 256), 256, 0, s>>>(n, k0, k1, ws.f0);
-    note_launch();
-    // in-place scan of the N+1 spacings (non-negative: monotone repair)
-    e = launch_scan(ws.f0, ws.f0, n + 1, PFR_F64, PFR_F64, PFR_ACC_F64 | PFR_SCAN_MONOTONE, 0, nullptr, -1, status,
-                    ws, s);
-    if (e != cudaSuccess) return e;
-    // the slots' diagonals number about 2 * s_count (+ the drift)
-    const unsigned gm = (unsigned)((2 * s_count + kMergeD - 1) / kMergeD);
+    // the N+1 spacings and their tile sums, the tile prefixes (and S_N),
+    // every tile's W run start, the merge (scratch: f0 = E, O = the rest)
+    if (!ws.O) return cudaErrorNotSupported;
+    const int64_t tiles = (n + 1 + kMnTile - 1) / kMnTile;
+    double* E = ws.f0;
+    double* tsum = reinterpret_cast<double*>(ws.O);
+    double* P = tsum + ((tiles + 31) / 32) * 32;
+    int64_t* lo = reinterpret_cast<int64_t*>(P + ((tiles + 1 + 31) / 32) * 32);
+    const int gt = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 8);
+    k_mn_tilesum<<<gt, 256, 0, s>>>(n, k0, k1, tiles, E, tsum);
+    k_mn_tileprefix<<<1, 1024, 0, s>>>(tsum, tiles, P);
     const int64_t s1 = s_begin + s_count;
-    if (dtype == PFR_F64)
-      k_multinomial_merge<double><<<gm, 256, 0, s>>>((const double*)W, n, ws.f0, s_begin, s1, a);
-    else
-      k_multinomial_merge<float><<<gm, 256, 0, s>>>((const float*)W, n, ws.f0, s_begin, s1, a);
+    const int64_t tb = s_begin / kMnTile, te = (s1 + kMnTile - 1) / kMnTile;
+    const unsigned gs = (unsigned)((te - tb + 1 + 255) / 256);
+    const int gm = (int)std::min<int64_t>(te - tb, (int64_t)num_sms() * 8);
+    static const bool carve = [] {
+      cudaFuncSetAttribute(k_mn_merge<double>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+      cudaFuncSetAttribute(k_mn_merge<float>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+      return true;
+    }();
+    (void)carve;
+    if (dtype == PFR_F64) {
+      k_mn_search<double><<<gs, 256, 0, s>>>((const double*)W, n, ws.f0, P, tsum, tiles, tb, te, lo);
+      k_mn_merge<double><<<gm, 256, 0, s>>>((const double*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a);
+    } else {
+      k_mn_search<float><<<gs, 256, 0, s>>>((const float*)W, n, ws.f0, P, tsum, tiles, tb, te, lo);
+      k_mn_merge<float><<<gm, 256, 0, s>>>((const float*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a);
+    }
+    note_launch(4);
     note_launch();
   }
   return cudaGetLastError();
