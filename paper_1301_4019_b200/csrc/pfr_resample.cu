@@ -664,7 +664,8 @@ __global__ void k_multinomial_numpy(const T* __restrict__ W, int64_t n, Key2x64 
 // one clamp never reaches past one boundary).  CTA t then writes a[k] =
 // min(N-1, #{j : W[j] < U_k}) for its own U tile: binary searches over W
 // staged in shared memory when the tile's W run fits.
-constexpr int kMnTile = 4096;  // 256 threads x 16 spacings
+constexpr int kMnThreads = 128, kMnPer = 8, kMnWarps = kMnThreads / 32;
+constexpr int kMnTile = kMnThreads * kMnPer;  // 1024 spacings per tile: more CTAs in flight
 
 __device__ __forceinline__ double mn_spacing(int64_t k, uint32_t k0, uint32_t k1) {
   uint32_t o[4];
@@ -674,15 +675,15 @@ __device__ __forceinline__ double mn_spacing(int64_t k, uint32_t k0, uint32_t k1
   return -log(u);
 }
 
-// inclusive scan of one tile's 4096 spacings e (thread tid holds indices
-// 16 tid .. 16 tid + 15; past N: 0), fixed association: thread-serial over
-// 16, Kogge-Stone over the warp's thread totals, serial fold of the 8 warp
-// totals.  L[i] = inclusive value; returns the tile's last inclusive value.
-__device__ double mn_tile_scan(const double (&e)[16], double (&L)[16], double* s_warp) {
+// inclusive scan of one tile's kMnTile spacings e (thread tid holds indices
+// kMnPer tid .. kMnPer (tid + 1) - 1; past N: 0), fixed association:
+// thread-serial, Kogge-Stone over the warp's thread totals, serial fold of
+// the warp totals.  L[i] = inclusive value; returns the tile's last inclusive value.
+__device__ double mn_tile_scan(const double (&e)[kMnPer], double (&L)[kMnPer], double* s_warp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double run = 0.0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < kMnPer; ++i) {
     run += e[i];
     L[i] = run;
   }
@@ -698,37 +699,37 @@ __device__ double mn_tile_scan(const double (&e)[16], double (&L)[16], double* s
   __syncthreads();
   double wex = 0.0, tot = 0.0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < kMnWarps; ++q) {
     if (q == warp) wex = tot;
     tot += s_warp[q];
   }
   const double base = wex + excl;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) L[i] = base + L[i];
+  for (int i = 0; i < kMnPer; ++i) L[i] = base + L[i];
   __syncthreads();  // s_warp reused below
-  if (tid == 255) s_warp[8] = L[15];
+  if (tid == kMnThreads - 1) s_warp[kMnWarps] = L[kMnPer - 1];
   __syncthreads();
-  const double last = s_warp[8];
+  const double last = s_warp[kMnWarps];
   __syncthreads();
   return last;
 }
 
 // pass 1: the spacings E_k (k <= N) into E, and each tile's scan total
-__global__ void __launch_bounds__(256) k_mn_tilesum(int64_t n, uint32_t k0, uint32_t k1, int64_t tiles,
+__global__ void __launch_bounds__(kMnThreads) k_mn_tilesum(int64_t n, uint32_t k0, uint32_t k1, int64_t tiles,
                                                     double* __restrict__ E, double* __restrict__ tsum) {
-  __shared__ double s_warp[9];
+  __shared__ double s_warp[kMnWarps + 1];
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const int64_t e0 = t * kMnTile + (int64_t)threadIdx.x * 16;
-    double e[16], L[16];
+    const int64_t e0 = t * kMnTile + (int64_t)threadIdx.x * kMnPer;
+    double e[kMnPer], L[kMnPer];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) e[i] = e0 + i <= n ? mn_spacing(e0 + i, k0, k1) : 0.0;
-    if (e0 + 16 <= n + 1) {
+    for (int i = 0; i < kMnPer; ++i) e[i] = e0 + i <= n ? mn_spacing(e0 + i, k0, k1) : 0.0;
+    if (e0 + kMnPer <= n + 1) {
       double2* dst = reinterpret_cast<double2*>(E + e0);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) dst[i] = make_double2(e[2 * i], e[2 * i + 1]);
+      for (int i = 0; i < kMnPer / 2; ++i) dst[i] = make_double2(e[2 * i], e[2 * i + 1]);
     } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
+      for (int i = 0; i < kMnPer; ++i)
         if (e0 + i <= n) E[e0 + i] = e[i];
     }
     const double tot = mn_tile_scan(e, L, s_warp);
@@ -798,58 +799,67 @@ __device__ __forceinline__ double mn_scale(const T* __restrict__ W, int64_t n, c
   return (double)ldg(W + n - 1) / P[tiles];
 }
 
-// every tile's W run start: lo[t - tb] = #{W < U_first(t)} for t in [tb, te]
-// (one thread each: all the binary searches in flight together)
+constexpr int kMnStage = 2048;  // W run staged in shared memory (a tile's run: ~1024 +- 3 sigma)
+
+// every tile's W run start lo[t - tb] = #{W < U_first(t)}, t in [tb, te]:
+// one thread each, all the binary searches in flight together (used when
+// the merge CTAs loop over several tiles each)
 template <typename T>
 __global__ void __launch_bounds__(256) k_mn_search(const T* __restrict__ W, int64_t n, const double* __restrict__ E,
                                                    const double* __restrict__ P, const double* __restrict__ tsum,
                                                    int64_t tiles, int64_t tb, int64_t te, int64_t* __restrict__ lo) {
   const int64_t t = tb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t > te) return;
-  if (t * kMnTile >= n) {
-    lo[t - tb] = n;
-    return;
-  }
-  lo[t - tb] = mn_below_range<T>(W, 0, n, mn_first_u(E, P, tsum, t, mn_scale<T>(W, n, P, tiles)));
+  lo[t - tb] = t * kMnTile >= n ? n : mn_below_range<T>(W, 0, n, mn_first_u(E, P, tsum, t, mn_scale<T>(W, n, P, tiles)));
 }
 
-constexpr int kMnStage = 5632;  // W run staged in shared memory (elements; static smem < 48 KiB)
-
+// lo_t == nullptr: one tile per CTA, which searches its own run bounds
+// while its spacings load and scan; else the bounds come from k_mn_search
 template <typename T>
-__global__ void __launch_bounds__(256) k_mn_merge(const T* __restrict__ W, int64_t n, const double* __restrict__ E,
+__global__ void __launch_bounds__(kMnThreads) k_mn_merge(const T* __restrict__ W, int64_t n, const double* __restrict__ E,
                                                   const double* __restrict__ P, const double* __restrict__ tsum,
                                                   const int64_t* __restrict__ lo_t, int64_t tiles, int64_t s0,
                                                   int64_t s1, int32_t* __restrict__ out) {
-  __shared__ double s_warp[9];
+  __shared__ double s_warp[kMnWarps + 1];
   __shared__ T sw[kMnStage];
+  __shared__ int64_t s_lohi[2];
   const double scale = mn_scale<T>(W, n, P, tiles);
   const int64_t tb = s0 / kMnTile, te = (s1 + kMnTile - 1) / kMnTile;  // U tiles covering [s0, s1)
   for (int64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
-    const int64_t k0i = t * kMnTile + (int64_t)threadIdx.x * 16;  // this thread's first index
-    double e[16], L[16];
-    if (k0i + 16 <= n + 1) {
+    // the tile's W run [lo(t), lo(t+1) + 1) with lo(t) = #{W < U_first(t)}
+    // (U_last(t) <= U_first(t+1)): two binary searches, in flight while
+    // the spacings load and scan
+    if (threadIdx.x < 2) {
+      const int64_t tt = t + threadIdx.x;
+      s_lohi[threadIdx.x] = lo_t ? lo_t[tt - tb]
+                            : tt * kMnTile >= n ? n
+                                                : mn_below_range<T>(W, 0, n, mn_first_u(E, P, tsum, tt, scale));
+    }
+    const int64_t k0i = t * kMnTile + (int64_t)threadIdx.x * kMnPer;  // this thread's first index
+    double e[kMnPer], L[kMnPer];
+    if (k0i + kMnPer <= n + 1) {
       const double2* src = reinterpret_cast<const double2*>(E + k0i);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < kMnPer / 2; ++i) {
         const double2 v = __ldcs(src + i);
         e[2 * i] = v.x;
         e[2 * i + 1] = v.y;
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) e[i] = k0i + i <= n ? E[k0i + i] : 0.0;
+      for (int i = 0; i < kMnPer; ++i) e[i] = k0i + i <= n ? E[k0i + i] : 0.0;
     }
     mn_tile_scan(e, L, s_warp);
     const double pt = P[t];
     const double prev_last = t > 0 ? P[t - 1] + tsum[t - 1] : 0.0;
-    double u[16];
+    double u[kMnPer];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < kMnPer; ++i) {
       const double sk = pt + L[i];
       u[i] = (sk > prev_last ? sk : prev_last) * scale;
     }
     // the tile's W run [lo(t), lo(t+1) + 1): U_last(t) <= U_first(t+1)
-    const int64_t lo = lo_t[t - tb], hi = max(lo, min(n, lo_t[t - tb + 1] + 1));
+    const int64_t lo = s_lohi[0], hi = max(lo, min(n, s_lohi[1] + 1));  // after mn_tile_scan's barriers
     const bool staged = hi - lo <= kMnStage;  // CTA-uniform
     if (staged) {
       // eight independent loads in flight per thread, then the stores
@@ -869,26 +879,37 @@ __global__ void __launch_bounds__(256) k_mn_merge(const T* __restrict__ W, int64
     }
     __syncthreads();
     if (staged) {
-      // 32-bit positions inside the staged run
+      // 32-bit positions inside the staged run.  Float W: (double)w < u iff
+      // w < u rounded up to float (no float lies strictly between), so the
+      // compares stay in float
+      float uf[kMnPer];
+#pragma unroll
+      for (int i = 0; i < kMnPer; ++i) uf[i] = __double2float_ru(u[i]);
+      auto below = [&](int x, int i) -> bool {
+        if constexpr (sizeof(T) == 4)
+          return sw[x] < uf[i];
+        else
+          return sw[x] < u[i];
+      };
       const int m = (int)(hi - lo);
       int a = 0, b = m;
       while (a < b) {
         const int mid = (a + b) >> 1;
-        if ((double)sw[mid] < u[0])
+        if (below(mid, 0))
           a = mid + 1;
         else
           b = mid;
       }
-      const int kmax = (int)min((int64_t)16, n - k0i);
+      const int kmax = (int)min((int64_t)kMnPer, n - k0i);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < kMnPer; ++i) {
         if (i >= kmax) break;
         // the walk advances ~1 W per uniform: test four positions at once
         // (independent loads), repeat only when all four are below u
         while (true) {
           int adv = 0;
 #pragma unroll
-          for (int r = 0; r < 4; ++r) adv += (a + r < m && (double)sw[a + r] < u[i]) ? 1 : 0;
+          for (int r = 0; r < 4; ++r) adv += (a + r < m && below(a + r, i)) ? 1 : 0;
           a += adv;
           if (adv < 4) break;
         }
@@ -901,7 +922,7 @@ __global__ void __launch_bounds__(256) k_mn_merge(const T* __restrict__ W, int64
     }
     int64_t pos = mn_below_range<T>(W, lo, hi, u[0]);  // #{W < u[0]}
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < kMnPer; ++i) {
       const int64_t k = k0i + i;
       if (k >= n) break;
       while (pos < hi && (double)ldg(W + pos) < u[i]) ++pos;
@@ -1168,20 +1189,18 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
   } else {
     const uint32_t k0 = (uint32_t)rng->key0, k1 = (uint32_t)(rng->key0 >> 32);
     // the N+1 spacings and their tile sums, the tile prefixes (and S_N),
-    // every tile's W run start, the merge (scratch: f0 = E, O = the rest)
+    // the merge (scratch: f0 = E, O = the tile sums and prefixes)
     if (!ws.O) return cudaErrorNotSupported;
     const int64_t tiles = (n + 1 + kMnTile - 1) / kMnTile;
     double* E = ws.f0;
     double* tsum = reinterpret_cast<double*>(ws.O);
     double* P = tsum + ((tiles + 31) / 32) * 32;
-    int64_t* lo = reinterpret_cast<int64_t*>(P + ((tiles + 1 + 31) / 32) * 32);
-    const int gt = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 8);
-    k_mn_tilesum<<<gt, 256, 0, s>>>(n, k0, k1, tiles, E, tsum);
+    const int gt = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 16);
+    k_mn_tilesum<<<gt, kMnThreads, 0, s>>>(n, k0, k1, tiles, E, tsum);
     k_mn_tileprefix<<<1, 1024, 0, s>>>(tsum, tiles, P);
     const int64_t s1 = s_begin + s_count;
     const int64_t tb = s_begin / kMnTile, te = (s1 + kMnTile - 1) / kMnTile;
-    const unsigned gs = (unsigned)((te - tb + 1 + 255) / 256);
-    const int gm = (int)std::min<int64_t>(te - tb, (int64_t)num_sms() * 8);
+    const int gm = (int)std::min<int64_t>(te - tb, (int64_t)num_sms() * 16);
     static const bool carve = [] {
       cudaFuncSetAttribute(k_mn_merge<double>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
@@ -1190,14 +1209,17 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
       return true;
     }();
     (void)carve;
+    // more tiles than CTAs: the bounds first, all searches at once
+    int64_t* lo = te - tb > gm ? reinterpret_cast<int64_t*>(P + ((tiles + 1 + 31) / 32) * 32) : nullptr;
+    const unsigned gs = (unsigned)((te - tb + 1 + 255) / 256);
     if (dtype == PFR_F64) {
-      k_mn_search<double><<<gs, 256, 0, s>>>((const double*)W, n, ws.f0, P, tsum, tiles, tb, te, lo);
-      k_mn_merge<double><<<gm, 256, 0, s>>>((const double*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a);
+      if (lo) k_mn_search<double><<<gs, 256, 0, s>>>((const double*)W, n, E, P, tsum, tiles, tb, te, lo);
+      k_mn_merge<double><<<gm, kMnThreads, 0, s>>>((const double*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a);
     } else {
-      k_mn_search<float><<<gs, 256, 0, s>>>((const float*)W, n, ws.f0, P, tsum, tiles, tb, te, lo);
-      k_mn_merge<float><<<gm, 256, 0, s>>>((const float*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a);
+      if (lo) k_mn_search<float><<<gs, 256, 0, s>>>((const float*)W, n, E, P, tsum, tiles, tb, te, lo);
+      k_mn_merge<float><<<gm, kMnThreads, 0, s>>>((const float*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a);
     }
-    note_launch(4);
+    note_launch(lo ? 4 : 3);
     note_launch();
   }
   return cudaGetLastError();
