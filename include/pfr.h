@@ -192,6 +192,21 @@ int pfr_deliver_offspring_logw(const void* lw, int64_t n, int dtype, int accum, 
 int pfr_deliver_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng, int32_t* c,
                            int32_t* max_steps, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
 
+/* Fused rejection delivery (own PHILOX stream): permute_parallel(
+ * rejection_ancestors(w, sup_w)) (resamplers.py:237-310, ancestry.py:
+ * 125-174); a slot claims its ancestor when it accepts, so the ancestry is
+ * never re-read for claiming.  Identical to pfr_rejection followed by
+ * pfr_permute (max_rounds as there). */
+int pfr_deliver_rejection(const void* w, int64_t n, int dtype, double bound, const pfr_rng* rng, int64_t max_rounds,
+                          int32_t* c, int32_t* max_steps, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
+/* Fused multinomial delivery (own PHILOX stream): permute_parallel(
+ * multinomial_ancestors(w)) (resamplers.py:56-74, ancestry.py:125-174); the
+ * merge claims each slot's ancestor as it writes it.  Identical to
+ * pfr_multinomial followed by pfr_permute. */
+int pfr_deliver_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng, int32_t* c,
+                            int32_t* max_steps, uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
 /* multinomial_ancestors (resamplers.py:56-74).
  *   rng mode ARRAYS: `uniforms` are the pre-scaled draws in [0, W[N-1]);
  *   rng mode NUMPY : u = random(N) * W[N-1] replayed from the stream; out a is unsorted;

@@ -106,6 +106,8 @@ _SIGNATURES = {
     "pfr_weight_stats": ([_P, _I64, _INT, _P, _INT, _P, _P, _SZ, _P], _INT),
     "pfr_probe_gather": ([_P, _I64, _INT, _I64, _P, _P], _INT),
     "pfr_deliver_metropolis": ([_P, _I64, _INT, _I64, _RNGP, _P, _P, _P, _P, _SZ, _P], _INT),
+    "pfr_deliver_rejection": ([_P, _I64, _INT, ctypes.c_double, _RNGP, _I64, _P, _P, _P, _P, _SZ, _P], _INT),
+    "pfr_deliver_multinomial": ([_P, _I64, _INT, _INT, _RNGP, _P, _P, _P, _P, _SZ, _P], _INT),
 }
 
 _lib = None

@@ -298,6 +298,40 @@ int pfr_deliver_metropolis(const void* w, int64_t n, int dtype, int64_t steps, c
   return PFR_OK;
 }
 
+int pfr_deliver_rejection(const void* w, int64_t n, int dtype, double bound, const pfr_rng* rng, int64_t max_rounds,
+                          int32_t* c, int32_t* max_steps, uint32_t* status, void* ws_ptr, size_t ws_bytes,
+                          void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && c && status, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(rng && rng->mode == PFR_RNG_PHILOX, "the fused rejection delivery uses the PHILOX stream");
+  if (!(bound > 0) || !std::isfinite(bound)) return fail(PFR_E_ARG, "weight bound must be finite and positive");
+  PFR_WS(PFR_OP_DELIVER);
+  cudaStream_t s = (cudaStream_t)stream;
+  // claims reset, slots + claims (a in the workspace's sorted-ancestry
+  // scratch), then the permute's walk
+  PFR_CHECK_LAUNCH(launch_claims_reset(n, max_steps, ws, s), "pfr_deliver_rejection");
+  PFR_CHECK_LAUNCH(launch_rejection(w, n, dtype, bound, 0.0, rng, max_rounds, ws.a, nullptr, nullptr, status, ws, s, 0,
+                                    n, ws.d),
+                   "pfr_deliver_rejection");
+  PFR_CHECK_LAUNCH(launch_walk(ws.a, n, c, max_steps, status, ws, s), "pfr_deliver_rejection");
+  return PFR_OK;
+}
+
+int pfr_deliver_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng, int32_t* c,
+                            int32_t* max_steps, uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
+  PFR_REQUIRE(valid_n(n) && w && c && status, "bad arguments");
+  PFR_REQUIRE(is_float(dtype), "weights must be float32 or float64");
+  PFR_REQUIRE(rng && rng->mode == PFR_RNG_PHILOX, "the fused multinomial delivery uses the PHILOX stream");
+  PFR_REQUIRE(accum >= 0 && accum <= PFR_ACC_SERIAL, "unknown accumulation mode");
+  PFR_WS(PFR_OP_DELIVER);
+  cudaStream_t s = (cudaStream_t)stream;
+  PFR_CHECK_LAUNCH(launch_claims_reset(n, max_steps, ws, s), "pfr_deliver_multinomial");
+  PFR_CHECK_LAUNCH(launch_multinomial(w, n, dtype, accum, rng, nullptr, 0, ws.a, status, ws, s, 0, n, ws.d),
+                   "pfr_deliver_multinomial");
+  PFR_CHECK_LAUNCH(launch_walk(ws.a, n, c, max_steps, status, ws, s), "pfr_deliver_multinomial");
+  return PFR_OK;
+}
+
 int pfr_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng, const double* uniforms,
                     int sorted_serial, int32_t* a, uint32_t* status, void* ws_ptr, size_t ws_bytes, void* stream) {
   PFR_REQUIRE(valid_n(n) && w && a, "bad arguments");

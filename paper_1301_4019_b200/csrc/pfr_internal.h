@@ -102,14 +102,15 @@ cudaError_t launch_lower_bound(const void* W, int64_t n, int dtype, const double
                                cudaStream_t s);
 cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng,
                                const double* uniforms, int sorted_serial, int32_t* a, uint32_t* status,
-                               const Workspace& ws, cudaStream_t s, int64_t s_begin = 0, int64_t s_count = -1);
+                               const Workspace& ws, cudaStream_t s, int64_t s_begin = 0, int64_t s_count = -1,
+                               int32_t* claim = nullptr);
 cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr_rng* rng,
                               const double* u_draws, const void* j_draws, int idx_dtype, int32_t* a,
                               uint32_t* status, cudaStream_t s, int64_t c_begin = 0, int64_t c_count = -1, int32_t* claim = nullptr);
 cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
                              int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
                              const Workspace& ws, cudaStream_t s, int64_t s_begin = 0,
-                             int64_t s_count = -1);
+                             int64_t s_count = -1, int32_t* claim = nullptr);
 
 // launcher (pfr_rejreplay.cu): rejection on the reference's numpy stream (parity mode)
 cudaError_t launch_rejection_replay(const void* w, int64_t n, int dtype, double bound, double cap,

@@ -227,6 +227,7 @@ struct RejArgs {
   T* out_w;
   unsigned long long* next_chunk;
   uint32_t* status;
+  int32_t* claim;  // fused delivery: the permute's claims (atomicMin of the slot at its ancestor)
 };
 
 constexpr int kRejChunk = 256;
@@ -467,6 +468,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
 
   auto finish = [&](uint32_t jd, T wd, uint32_t ntrips) {
     A.a[slot] = (int32_t)jd;
+    if (A.claim) atomicMin(A.claim + jd, (int32_t)(A.s0 + slot));
     if (A.trips) A.trips[slot] = (int32_t)ntrips;
     if (kCapped) {
       const T vd = wd < capv ? wd : capv;
@@ -477,6 +479,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
   auto no_progress = [&]() {
     flags |= PFR_ST_NOPROGRESS;
     A.a[slot] = (int32_t)(A.s0 + slot);
+    if (A.claim) atomicMin(A.claim + A.s0 + slot, (int32_t)(A.s0 + slot));
     if (A.trips) A.trips[slot] = (int32_t)A.max_trips;
     if (kCapped) A.out_w[slot] = T(1);
     slot = -1;
@@ -819,7 +822,7 @@ template <typename T>
 __global__ void __launch_bounds__(kMnThreads) k_mn_merge(const T* __restrict__ W, int64_t n, const double* __restrict__ E,
                                                   const double* __restrict__ P, const double* __restrict__ tsum,
                                                   const int64_t* __restrict__ lo_t, int64_t tiles, int64_t s0,
-                                                  int64_t s1, int32_t* __restrict__ out) {
+                                                  int64_t s1, int32_t* __restrict__ out, int32_t* __restrict__ claim) {
   __shared__ double s_warp[kMnWarps + 1];
   __shared__ T sw[kMnStage];
   __shared__ int64_t s_lohi[2];
@@ -915,7 +918,11 @@ __global__ void __launch_bounds__(kMnThreads) k_mn_merge(const T* __restrict__ W
         }
         const int64_t k = k0i + i;
         const int64_t pos = lo + a;
-        if (k >= s0 && k < s1) out[k - s0] = (int32_t)(pos < n ? pos : n - 1);
+        if (k >= s0 && k < s1) {
+          const int32_t v = (int32_t)(pos < n ? pos : n - 1);
+          out[k - s0] = v;
+          if (claim) atomicMin(claim + v, (int32_t)k);
+        }
       }
       __syncthreads();
       continue;
@@ -926,7 +933,11 @@ __global__ void __launch_bounds__(kMnThreads) k_mn_merge(const T* __restrict__ W
       const int64_t k = k0i + i;
       if (k >= n) break;
       while (pos < hi && (double)ldg(W + pos) < u[i]) ++pos;
-      if (k >= s0 && k < s1) out[k - s0] = (int32_t)(pos < n ? pos : n - 1);
+      if (k >= s0 && k < s1) {
+        const int32_t v = (int32_t)(pos < n ? pos : n - 1);
+        out[k - s0] = v;
+        if (claim) atomicMin(claim + v, (int32_t)k);
+      }
     }
     __syncthreads();
   }
@@ -1034,7 +1045,7 @@ cudaError_t launch_metropolis(const void* w, int64_t n, int dtype, int64_t steps
 
 cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
                              int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
-                             const Workspace& ws, cudaStream_t s, int64_t s_begin, int64_t s_count) {
+                             const Workspace& ws, cudaStream_t s, int64_t s_begin, int64_t s_count, int32_t* claim) {
   if (s_count < 0) s_count = n - s_begin;
   if (rng && rng->mode == PFR_RNG_NUMPY && s_begin == 0 && s_count == n)
     return launch_rejection_replay(w, n, dtype, bound, cap, rng, max_rounds, a, trips, out_w, status, ws, s);
@@ -1124,14 +1135,14 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
   } while (0)
   if (dtype == PFR_F64) {
     RejArgs<double> A{(const double*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
-                      s_begin, s_count, a, trips, (double*)out_w, next, status};
+                      s_begin, s_count, a, trips, (double*)out_w, next, status, claim};
     if (cap > 0)
       PFR_REJ_DISPATCH(double, true);
     else
       PFR_REJ_DISPATCH(double, false);
   } else {
     RejArgs<float> A{(const float*)w, n, cap > 0 ? cap : bound, cap, k0, k1, lemire_threshold(n), max_trips,
-                     s_begin, s_count, a, trips, (float*)out_w, next, status};
+                     s_begin, s_count, a, trips, (float*)out_w, next, status, claim};
     if (cap > 0)
       PFR_REJ_DISPATCH(float, true);
     else
@@ -1145,7 +1156,8 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
 
 cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, const pfr_rng* rng,
                                const double* uniforms, int sorted_serial, int32_t* a, uint32_t* status,
-                               const Workspace& ws, cudaStream_t s, int64_t s_begin, int64_t s_count) {
+                               const Workspace& ws, cudaStream_t s, int64_t s_begin, int64_t s_count,
+                               int32_t* claim) {
   if (s_count < 0) s_count = n - s_begin;
   const bool full = s_begin == 0 && s_count == n;
   if (sorted_serial && !full) return cudaErrorNotSupported;
@@ -1214,10 +1226,10 @@ cudaError_t launch_multinomial(const void* w, int64_t n, int dtype, int accum, c
     const unsigned gs = (unsigned)((te - tb + 1 + 255) / 256);
     if (dtype == PFR_F64) {
       if (lo) k_mn_search<double><<<gs, 256, 0, s>>>((const double*)W, n, E, P, tsum, tiles, tb, te, lo);
-      k_mn_merge<double><<<gm, kMnThreads, 0, s>>>((const double*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a);
+      k_mn_merge<double><<<gm, kMnThreads, 0, s>>>((const double*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a, claim);
     } else {
       if (lo) k_mn_search<float><<<gs, 256, 0, s>>>((const float*)W, n, E, P, tsum, tiles, tb, te, lo);
-      k_mn_merge<float><<<gm, kMnThreads, 0, s>>>((const float*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a);
+      k_mn_merge<float><<<gm, kMnThreads, 0, s>>>((const float*)W, n, E, P, tsum, lo, tiles, s_begin, s1, a, claim);
     }
     note_launch(lo ? 4 : 3);
     note_launch();

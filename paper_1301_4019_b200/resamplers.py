@@ -411,6 +411,36 @@ def deliver(w, config: ResamplerConfig, rng, *, rng_mode=None, accum=None, index
         _raise(st, require_positive_total=True)  # resample_ancestors' check_weights (resamplers.py:372)
         c = L.to_index_dtype(c, index_dtype) if out is None else c
         return (c, int(steps.item())) if return_max_steps else c
+    if alg in ("rejection", "multinomial") and (rng_mode or L.config.rng_mode) == "philox":
+        # fused: the resampler makes the permute's claims as it writes each slot
+        if alg == "rejection":
+            w, st = _weights_checked(w, require_positive_total=False)
+        else:
+            w = L.as_weights(w)
+            st = L.new_status()  # the weight scan reports check_weights' flags
+        n = w.numel()
+        c = out if out is not None else torch.empty(n, dtype=torch.int32, device=w.device)
+        steps = torch.zeros(1, dtype=torch.int32, device=w.device) if return_max_steps else None
+        ws, wsb = L.workspace(n)
+        r = _rng(rng, rng_mode)
+        extra = None
+        if alg == "rejection":
+            bound = float(config.sup_w) if config.sup_w is not None else float(w.max())
+            if not math.isfinite(bound) or bound <= 0:
+                raise ValueError(f"weight bound must be finite and positive, got {bound}")
+            L.call("pfr_deliver_rejection", w.data_ptr(), n, L.dtype_code(w), bound, r, int(MAX_REJECTION_ROUNDS),
+                   c.data_ptr(), L.ptr(steps), st.data_ptr(), ws, wsb, L.stream_handle())
+
+            def extra(bits):
+                if bits & L.ST_NOPROGRESS:
+                    raise RuntimeError(f"rejection resampling made no progress after {MAX_REJECTION_ROUNDS} "
+                                       f"rounds; weight bound {bound} is far above every weight")
+        else:
+            L.call("pfr_deliver_multinomial", w.data_ptr(), n, L.dtype_code(w), L.accum_code(accum), r,
+                   c.data_ptr(), L.ptr(steps), st.data_ptr(), ws, wsb, L.stream_handle())
+        _raise(st, require_positive_total=True, extra=extra)  # resample_ancestors' check_weights
+        c = L.to_index_dtype(c, index_dtype) if out is None else c
+        return (c, int(steps.item())) if return_max_steps else c
     kw = {"rng_mode": rng_mode}
     if alg.startswith("multinomial"):
         kw["accum"] = accum

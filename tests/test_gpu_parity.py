@@ -762,3 +762,33 @@ def test_rejection_table_on_off_identical(tmp_path):
     assert set(res[0].files) == set(res[1].files) and len(res[0].files) == 40
     for k in res[0].files:
         np.testing.assert_array_equal(res[0][k], res[1][k], err_msg=k)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("alg", ["rejection", "multinomial"])
+@pytest.mark.parametrize("n", [1, 1000, 4097, (1 << 20) + 5])
+def test_fused_rejection_multinomial_delivery_equals_two_calls(dtype, alg, n):
+    """deliver(rejection / multinomial) in the own stream makes the permute's
+    claims inside the resampler: element for element (and max steps) the
+    same as permute_parallel(resample_ancestors(...))."""
+    g = np.random.default_rng(n + 3)
+    wn = np.exp(g.normal(0, 1.0, n))
+    wn[g.random(n) < 0.1] = 0.0
+    wn[0] = 1.0
+    w = torch.from_numpy(wn.astype(dtype)).cuda()
+    cfg = pf.ResamplerConfig(alg, sup_w=float(w.max()) if alg == "rejection" else None)
+    c, s = pf.deliver(w, cfg, pf.RngStream(4, (n,)), return_max_steps=True, index_dtype=torch.int32)
+    a = pf.resample_ancestors(w, cfg, pf.RngStream(4, (n,)), index_dtype=torch.int32).ancestors
+    c2, s2 = pf.permute_parallel(a, return_max_steps=True, index_dtype=torch.int32)
+    np.testing.assert_array_equal(np_(c), np_(c2))
+    assert s == s2
+    assert O.satisfies_predicate(np_(c))
+
+
+@pytest.mark.parametrize("alg", ["rejection", "multinomial"])
+def test_fused_delivery_validates(alg):
+    with pytest.raises(ValueError, match="non-negative"):
+        pf.deliver(np.array([1.0, -1.0, 2.0, 3.0]), pf.ResamplerConfig(alg, sup_w=3.0 if alg == "rejection" else None),
+                   pf.RngStream(0))
+    with pytest.raises(ValueError, match="positive"):
+        pf.deliver(np.zeros(8), pf.ResamplerConfig(alg, sup_w=1.0 if alg == "rejection" else None), pf.RngStream(0))
