@@ -635,7 +635,9 @@ def main():
                             "and short deliveries, the long ones (rejection, Metropolis) computed in sequence on "
                             "one stream and the short ones on another, each result downloaded on its own stream "
                             "as soon as its delivery is done; link_only_ms = the same copies with no compute "
-                            "(the host-link floor)"},
+                            "(the host-link floor); results are int32 indices (the C ABI's output; the "
+                            "reference's numpy arrays are int64 -- index_dtype=torch.int64 converts on the device "
+                            "at twice the download bytes)"},
             "gpu_launches": launches,
             "clocks": clocks,
             "per_delivery_ms": {k: sum(v) / len(v) for k, v in per_delivery.items()},
