@@ -418,8 +418,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
   // certain-reject table (kTab): trip q needs its gather only when beta *
   // bound <= thr or the proposal's group holds a capped weight above thr
   extern __shared__ uint32_t rej_tab[];
-  uint32_t ubig = 0;   // 2^(31-k) with a table
-  uint32_t notab = 1;  // 1: no table chosen (every trip gathers)
+  uint32_t ulim = 0xFFFFFFFFu;  // 2^(31-k) - 1 with a table; no table: every trip gathers
   if constexpr (kTab) {
     __shared__ int s_k;
     if (threadIdx.x == 0) {
@@ -440,8 +439,7 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
       const uint4* src = reinterpret_cast<const uint4*>(tb.bits + (int64_t)k * tb.words);
       uint4* dst = reinterpret_cast<uint4*>(rej_tab);
       for (int64_t i = threadIdx.x; i < tb.words / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
-      ubig = 1u << (31 - k);
-      notab = 0;
+      ulim = (1u << (31 - k)) - 1u;
     }
     __syncthreads();
   }
@@ -456,8 +454,8 @@ __global__ void __launch_bounds__(kTab ? kRejTabThreads : 256, 1) k_rejection_ph
         const uint32_t gq = d.j[q] >> tb.lg;
         const uint32_t bit = rej_tab[gq >> 5] >> (gq & 31);
         // u = (2m+1) 2^-24 (f32, m = x >> 9) or (2x+1) 2^-33 (f64) exceeds
-        // 2^-(k+1) exactly when x >= 2^(31-k) (ubig)
-        nd = (d.x[q] < ubig) | (bit & 1u) | notab;
+        // 2^-(k+1) exactly when x > 2^(31-k) - 1 (ulim; all ones: no table)
+        nd = (d.x[q] <= ulim) | (bit & 1u);
       }
       need[q] = nd;
       wj[q] = T(0);
