@@ -485,8 +485,8 @@ def main():
     # first) and 1.80 ms round-robin over two streams; stream priorities did
     # not help.
     names = [f"{jobs[k][1]}/{jobs[k][3]}" for k in range(len(jobs))]
-    seq = ["rejection/f32", "rejection/f64", "systematic/f64", "metropolis/f32", "stratified/f32",
-           "metropolis/f64", "multinomial/f32", "stratified/f64", "multinomial/f64", "systematic/f32"]
+    seq = os.environ.get("PFR_E2E_SEQ", "systematic/f32,rejection/f32,rejection/f64,stratified/f32,metropolis/f32,"
+                         "metropolis/f64,multinomial/f32,stratified/f64,multinomial/f64,systematic/f64").split(",")
     order = [names.index(x) for x in seq]
     e2e_streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
     stream_of = {k: e2e_streams[0 if jobs[k][1] in ("rejection", "metropolis") else 1] for k in order}

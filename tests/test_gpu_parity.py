@@ -792,3 +792,37 @@ def test_fused_delivery_validates(alg):
                    pf.RngStream(0))
     with pytest.raises(ValueError, match="positive"):
         pf.deliver(np.zeros(8), pf.ResamplerConfig(alg, sup_w=1.0 if alg == "rejection" else None), pf.RngStream(0))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("kind", ["two_spikes", "mostly_zero", "ramp"])
+def test_own_stream_multinomial_long_weight_runs(dtype, kind):
+    """The own-stream multinomial merge when a uniform tile's W run does not
+    fit shared memory (flat stretches of zero weights: the global-memory
+    path): the ancestry is sorted, selects only positive weights, and its
+    counts follow N w / W."""
+    n = (1 << 18) + 77
+    g = np.random.default_rng(len(kind))
+    if kind == "two_spikes":
+        w = np.zeros(n)
+        w[0], w[-1] = 1.0, 1.0
+    elif kind == "mostly_zero":
+        w = np.zeros(n)
+        idx = g.choice(n, 300, replace=False)
+        w[idx] = g.random(300) + 0.5
+    else:
+        w = np.linspace(0.0, 1.0, n) ** 8
+    w = w.astype(dtype)
+    for fused in (False, True):
+        if fused:
+            c = np_(pf.deliver(w, pf.ResamplerConfig("multinomial"), pf.RngStream(6), index_dtype=torch.int64))
+            assert O.satisfies_predicate(c)
+            a = np.sort(c)
+        else:
+            a = np_(pf.multinomial_ancestors(w, pf.RngStream(6), index_dtype=torch.int64))
+            assert np.all(np.diff(a) >= 0)
+        assert np.all(w[a] > 0)
+        cnt = np.bincount(a, minlength=n).astype(np.float64)
+        expect = n * w.astype(np.float64) / w.astype(np.float64).sum()
+        sd = np.sqrt(np.maximum(expect, 1.0))
+        assert np.all(np.abs(cnt - expect) < 7 * sd + 1)
