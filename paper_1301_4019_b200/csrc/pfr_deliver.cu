@@ -734,7 +734,7 @@ struct ResolveQ {
 // (local hole, global slot); words are indexed by global slot and exist for
 // [wlo, whi) only (a shard's halo: a chain leaving it sets the overflow flag
 // and the host falls back).
-template <bool kShard = false>
+template <bool kShard = false, bool kTrack = true>
 __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const uint32_t* __restrict__ words,
                                          int32_t* __restrict__ c, int64_t wlo, int64_t whi, int64_t gbase,
                                          int& longest, bool& overflow) {
@@ -749,7 +749,7 @@ __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const 
       const int e = b + 32 * i + lane;
       if (e < qlen) {
         xz[i] = Q.xz[e];
-        st[i] = Q.st[e] + 1;
+        if constexpr (kTrack) st[i] = Q.st[e] + 1;
         const int64_t z = xz[i].y;
         w[i] = (!kShard || (z >= wlo && z < whi)) ? __ldcg(words + z) : 0xFFFFFFFFu;
       }
@@ -766,8 +766,8 @@ __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const 
           overflow = true;  // outside the shard's halo (or an unwritten word): the host falls back
         } else if (!(w[i] & kFirst)) {
           c[xz[i].x] = (int32_t)par;
-          longest = max(longest, st[i]);
-        } else if (st[i] >= kBackBound || (kShard && (int64_t)par >= whi)) {
+          if constexpr (kTrack) longest = max(longest, st[i]);
+        } else if ((kTrack && st[i] >= kBackBound) || (kShard && (int64_t)par >= whi)) {
           overflow = true;  // abandoned: the rare-path kernel resolves every chain
         } else {
           keep = true;
@@ -777,7 +777,7 @@ __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const 
       if (keep) {
         const int pos = out + __popc(m & ((1u << lane) - 1));
         Q.xz[pos] = make_uint2(xz[i].x, w[i] & kParentMask);
-        Q.st[pos] = (uint8_t)st[i];
+        if constexpr (kTrack) Q.st[pos] = (uint8_t)st[i];
       }
       out += __popc(m);
     }
@@ -795,7 +795,10 @@ __device__ __forceinline__ int lean_pass(ResolveQ& Q, int lane, int qlen, const 
 // pass, a pass running once enough chains wait -- so a pass costs one L2
 // round trip for several subtiles' chains, overlapped with the next
 // subtile's prefetched loads.
-template <typename T, typename A, int UM, bool kShard = false>
+// kTrack (max_steps requested): per-chain step counts for max_steps and the
+// per-chain bound; otherwise the drain is bounded by its pass count (a chain
+// left then is resolved by the rare path, as an abandoned one)
+template <typename A, bool kShard = false, bool kTrack = true>
 __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
   extern __shared__ __align__(16) unsigned char fused_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -811,7 +814,9 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
   // wlo] covers [wlo, whi): the single-GPU call has gbase = wlo = 0, whi = n
   const int64_t gbase = kShard ? p.gbase : 0, wlo = kShard ? p.wlo : 0, whi = kShard ? p.whi : p.n;
   const uint32_t* __restrict__ wds = p.words - wlo;  // indexed by global slot (only inside [wlo, whi))
-  auto pass = [&]() { return lean_pass<kShard>(Q, lane, qlen, wds, p.c, wlo, whi, gbase, longest, overflow); };
+  auto pass = [&]() {
+    return lean_pass<kShard, kTrack>(Q, lane, qlen, wds, p.c, wlo, whi, gbase, longest, overflow);
+  };
   const bool vec_ok = !kShard || ((gbase - wlo) & 3) == 0;  // 16-byte word loads need a 4-aligned offset
   const uint4* __restrict__ words4 = reinterpret_cast<const uint4*>(p.words + (gbase - wlo));
   int4* __restrict__ c4 = reinterpret_cast<int4*>(p.c);
@@ -888,7 +893,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
       for (int t = 0; t < 4; ++t) {
         if ((pend >> (4 * q + t)) & 1u) {
           Q.xz[pos] = make_uint2(xb + 128 * q + 4 * lane + t, e[t] & kParentMask);  // (local hole, global slot)
-          Q.st[pos] = 0;
+          if constexpr (kTrack) Q.st[pos] = 0;
           ++pos;
         }
       }
@@ -897,12 +902,18 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) k_dv_resolve(DvArgs<A> p) {
     __syncwarp();
     if (qlen >= kRThresh) qlen = pass();
   }
-  while (qlen) qlen = pass();
+  for (int drain = 0; qlen; ++drain) {
+    if (!kTrack && drain > kBackBound) {
+      overflow = true;  // the rare path resolves every chain
+      break;
+    }
+    qlen = pass();
+  }
   if (overflow) {
     atomicOr(&p.state->flags, kOverflow);
     status_or(p.status, PFR_ST_OVERFLOW);
   }
-  if (p.max_steps) {
+  if (kTrack && p.max_steps) {
     longest = __reduce_max_sync(0xffffffffu, longest);
     if (lane == 0 && longest) atomicMax(p.max_steps, longest);
   }
@@ -1119,10 +1130,12 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
     if (occ2 < 0) {
       e = cudaFuncSetAttribute(k_dv_produce<T, A, UM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(k_dv_resolve<T, A, UM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+      e = cudaFuncSetAttribute(k_dv_resolve<A, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(k_dv_resolve<A, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
       if (e != cudaSuccess) return e;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_dv_produce<T, A, UM>, kFWarps * 32, smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_dv_resolve<T, A, UM>, kFWarps * 32, smem3);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_dv_resolve<A, false, true>, kFWarps * 32, smem3);
       occ2 = max(occ2, 1);
       occ3 = max(occ3, 1);
     }
@@ -1131,7 +1144,11 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
     const int64_t g3 = max((int64_t)1, min((int64_t)num_sms() * occ3, (subs + kFWarps - 1) / kFWarps));
     e = launch_pdl_smem(k_dv_produce<T, A, UM>, dim3((unsigned)g2), dim3(kFWarps * 32), (size_t)smem, s, false, p);
     if (e != cudaSuccess || stages < 3) return e;
-    e = launch_pdl_smem(k_dv_resolve<T, A, UM>, dim3((unsigned)g3), dim3(kFWarps * 32), (size_t)smem3, s, false, p);
+    e = p.max_steps
+            ? launch_pdl_smem(k_dv_resolve<A, false, true>, dim3((unsigned)g3), dim3(kFWarps * 32), (size_t)smem3, s,
+                              false, p)
+            : launch_pdl_smem(k_dv_resolve<A, false, false>, dim3((unsigned)g3), dim3(kFWarps * 32), (size_t)smem3,
+                              s, false, p);
     if (e != cudaSuccess || stages < 4) return e;
     return launch_pdl(k_dv_rare<T, A, UM>, dim3(num_sms()), dim3(kTileThreads), s, true, p);
   }
@@ -1283,15 +1300,15 @@ cudaError_t shard_resolve_t(DvArgs<double> p, cudaStream_t s) {
   const int smem = (int)(sizeof(ResolveQ) * kFWarps);
   static int occ = -1;
   if (occ < 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_dv_resolve<T, double, kUSys, true>,
+    cudaError_t e = cudaFuncSetAttribute(k_dv_resolve<double, true, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dv_resolve<T, double, kUSys, true>, kFWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dv_resolve<double, true, true>, kFWarps * 32, smem);
     occ = max(occ, 1);
   }
   const int64_t subs = (p.n + kSub - 1) / kSub;
   const int64_t g = max((int64_t)1, min((int64_t)num_sms() * occ, (subs + kFWarps - 1) / kFWarps));
-  k_dv_resolve<T, double, kUSys, true><<<(unsigned)g, kFWarps * 32, smem, s>>>(p);
+  k_dv_resolve<double, true, true><<<(unsigned)g, kFWarps * 32, smem, s>>>(p);
   note_launch();
   return cudaGetLastError();
 }
