@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 3) k_dv_produce(DvArgs<A> p) {
 
 // K3w's chain queue: one per warp, in shared memory.
 constexpr int kRQ = 1024;     // entries (>= kRThresh + the 512 chains one subtile can add)
-constexpr int kRThresh = 384; // a pass runs once this many chains wait (~1 pass per subtile)
+constexpr int kRThresh = 256; // a pass runs once this many chains wait (160-384 measure alike)
 struct ResolveQ {
   uint2 xz[kRQ];  // (hole, next slot)
   uint8_t st[kRQ];
