@@ -826,3 +826,23 @@ def test_own_stream_multinomial_long_weight_runs(dtype, kind):
         expect = n * w.astype(np.float64) / w.astype(np.float64).sum()
         sd = np.sqrt(np.maximum(expect, 1.0))
         assert np.all(np.abs(cnt - expect) < 7 * sd + 1)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [4096, 70000])
+def test_delivery_long_chain_goes_to_the_rare_path(dtype, n):
+    """w = (2, 1, ..., 1, 0): O = (2, 3, ..., N, N), one loser chain of
+    length N-2 -- past the resolve kernel's bounds (per-chain steps when
+    max_steps is requested, the drain's pass count otherwise), so the rare
+    path resolves it: both calls equal the oracle's delivery."""
+    w = np.ones(n)
+    w[0], w[-1] = 2.0, 0.0
+    w = w.astype(dtype)
+    # O does not depend on the offset here: floor(j + 2 + u) = j + 2 for any u
+    want = O.permute(O.expand_cumulative(O.systematic(w.astype(np.float64), 0.5)))
+    cfg = pf.ResamplerConfig("systematic")
+    c_track, steps = pf.deliver(w, cfg, pf.RngStream(0), return_max_steps=True, index_dtype=torch.int64)
+    c_plain = pf.deliver(w, cfg, pf.RngStream(0), index_dtype=torch.int64)
+    np.testing.assert_array_equal(np_(c_track), want)
+    np.testing.assert_array_equal(np_(c_plain), want)
+    assert steps >= n - 2
