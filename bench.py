@@ -374,6 +374,14 @@ def main():
         cfg = rej_cfg[dt] if alg == "rejection" else cfgs[alg]
         return pf.deliver(w, cfg, rs, index_dtype=torch.int32, out=out)
 
+    # submission order of the concurrent step: the longest deliveries first
+    # (rejection, Metropolis), so the short ones fill the SMs around them
+    # (1.00 ms/step vs 1.07 ms in table order; PFR_CONC_ORDER=table for A/B)
+    conc_order = list(range(len(jobs)))
+    if os.environ.get("PFR_CONC_ORDER") != "table":
+        rank_alg = {"rejection": 0, "metropolis": 1, "multinomial": 2, "stratified": 3, "systematic": 4}
+        conc_order.sort(key=lambda k: (rank_alg[jobs[k][1]], jobs[k][3]))
+
     def concurrent_step(step):
         flush.zero_()
         torch.cuda._sleep(STEP_PREROLL_CYCLES)
@@ -381,7 +389,8 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         done = []
-        for k, (i, alg, j, dt) in enumerate(jobs):
+        for k in conc_order:
+            i, alg, j, dt = jobs[k]
             sk = conc_streams[k]
             sk.wait_event(e0)
             with torch.cuda.stream(sk):

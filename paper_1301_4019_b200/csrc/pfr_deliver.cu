@@ -1096,6 +1096,22 @@ cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t s, bool coo
   return launch_pdl_smem(kernel, grid, block, 0, s, cooperative, args...);
 }
 
+// The rare-path kernel is launched after every delivery and exits at once
+// unless a flag is set; it is cooperative (grid syncs), and a cooperative
+// launch needs all its CTAs resident together -- with a full-machine grid it
+// waits for concurrent work on other streams to drain (measured: 4x slower
+// concurrent steps when it queued behind the persistent rejection kernels).
+// A 16-CTA grid co-resides with anything; the rare work itself (repair,
+// pointer jumping) is grid-strided and only slower on adversarial inputs.
+// PFR_RARE_GRID overrides (A/B aid).
+inline int rare_grid() {
+  static const int g = [] {
+    const char* v = getenv("PFR_RARE_GRID");
+    return v ? std::max(1, atoi(v)) : 16;
+  }();
+  return g;
+}
+
 template <typename T, typename A, int UM>
 cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   // PFR_DV_STAGES (profiling aid): launch only the first k kernels
@@ -1150,7 +1166,7 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
             : launch_pdl_smem(k_dv_resolve<A, false, false>, dim3((unsigned)g3), dim3(kFWarps * 32), (size_t)smem3,
                               s, false, p);
     if (e != cudaSuccess || stages < 4) return e;
-    return launch_pdl(k_dv_rare<T, A, UM>, dim3(num_sms()), dim3(kTileThreads), s, true, p);
+    return launch_pdl(k_dv_rare<T, A, UM>, dim3(rare_grid()), dim3(kTileThreads), s, true, p);
   }
   e = launch_pdl(k_dv_expand<T, A, UM>, dim3(tiles), dim3(kTileThreads), s, false, p);
   if (e != cudaSuccess || stages < 3) return e;
@@ -1181,7 +1197,7 @@ cudaError_t deliver_typed(DvArgs<A> p, cudaStream_t s) {
   // one CTA per SM: the grid only has to be co-resident (grid.sync), and in
   // the common case every CTA returns at once, so a small grid launches fastest
   (void)occ;
-  return launch_pdl(k_dv_rare<T, A, UM>, dim3(num_sms()), dim3(kTileThreads), s, true, p);
+  return launch_pdl(k_dv_rare<T, A, UM>, dim3(rare_grid()), dim3(kTileThreads), s, true, p);
 }
 
 template <typename T, typename A>
