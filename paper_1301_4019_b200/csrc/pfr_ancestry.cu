@@ -468,7 +468,10 @@ cudaError_t launch_fallback(const FallbackArgs& args, cudaStream_t s) {
   }
   FallbackArgs a = args;
   void* params[] = {&a};
-  dim3 grid(num_sms() * blocks_per_sm), block(256);
+  // launched every time and exits unless a walker overflowed: a small
+  // cooperative grid co-resides with concurrent work (a full-machine grid
+  // waits for other streams' kernels to drain; see rare_grid in pfr_deliver.cu)
+  dim3 grid((unsigned)std::min(num_sms() * blocks_per_sm, 16)), block(256);
   note_launch();
   return cudaLaunchCooperativeKernel((const void*)k_fallback<kSorted>, grid, block, params, 0, s);
 }

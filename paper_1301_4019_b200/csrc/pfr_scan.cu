@@ -418,7 +418,9 @@ cudaError_t scan_typed(const void* in, void* out, int64_t n, int exclusive, int 
     if (repair) {
       // tile maxima scratch: the sum-tree region past the aggregates and group totals
       U* tmax = reinterpret_cast<U*>(agg + tiles + 8 + (tiles + kGroupTiles - 1) / kGroupTiles + 8);
-      e = launch_ex(k_sc_repair<U>, dim3((unsigned)num_sms()), dim3(kTileThreads), s, true, true, (U*)out, n, tiles,
+      // cooperative, launched every time (exits unless flagged): a small grid
+      // co-resides with concurrent work (see rare_grid in pfr_deliver.cu)
+      e = launch_ex(k_sc_repair<U>, dim3(16u), dim3(kTileThreads), s, true, true, (U*)out, n, tiles,
                     ws.dv, tmax, exclusive, total, status);
     }
   }
