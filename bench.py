@@ -500,6 +500,8 @@ def main():
     e2e_streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
     stream_of = {k: e2e_streams[0 if jobs[k][1] in ("rejection", "metropolis") else 1] for k in order}
     stream_of[order[-1]] = e2e_streams[2]  # the last upload (the smallest job) never queues behind another
+    if os.environ.get("PFR_E2E_STREAMS") == "each":  # A/B: every delivery on its own stream
+        stream_of = {k: torch.cuda.Stream(device=dev) for k in order}
 
     for s in range(args.warmup + args.steps):
         flush.zero_()
