@@ -326,9 +326,11 @@ __device__ __forceinline__ T rej_thr(double bound, int k) {
   return (T)bound * (T)ldexp(1.0, -(k + 1));
 }
 
+// (also check_weights' flags, diagnostics.py:38-51: the table reads every
+// weight once, so the rejection needs no separate validation pass)
 template <typename T, bool kCapped>
 __global__ void __launch_bounds__(256) k_rej_table(const T* __restrict__ w, int64_t n, double bound, double cap,
-                                                   RejTab tb) {
+                                                   RejTab tb, uint32_t* status) {
   constexpr int kW = 4;  // words per warp and pass: four independent loads in flight per lane
   const int lane = threadIdx.x & 31;
   const T capv = (T)cap;
@@ -337,6 +339,7 @@ __global__ void __launch_bounds__(256) k_rej_table(const T* __restrict__ w, int6
   for (int k = 0; k < kRejTabK; ++k) thr[k] = rej_thr<T>(cap > 0 ? cap : bound, k);
   const int64_t g = (int64_t)1 << tb.lg;
   uint32_t cnt = 0;  // lane k < kRejTabK: set bits of threshold k
+  FlagAcc<T> facc;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t w0 = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * kW; w0 < tb.words;
        w0 += warps * kW) {
@@ -348,6 +351,7 @@ __global__ void __launch_bounds__(256) k_rej_table(const T* __restrict__ w, int6
       for (int q = 0; q < kW; ++q) {
         const int64_t e = (w0 + q) * 32 + lane;
         vmax[q] = e < n ? ldg(w + e) : T(0);
+        if (e < n) facc.add(vmax[q]);
       }
 #pragma unroll
       for (int q = 0; q < kW; ++q) {
@@ -363,6 +367,7 @@ __global__ void __launch_bounds__(256) k_rej_table(const T* __restrict__ w, int6
         const int64_t e0 = grp * g, e1 = min(e0 + g, n);
         for (int64_t e = e0; e < e1; ++e) {
           const T wj = ldg(w + e);
+          facc.add(wj);
           const T v = kCapped ? (wj < capv ? wj : capv) : wj;
           if (v > vmax[q]) vmax[q] = v;
         }
@@ -383,6 +388,7 @@ __global__ void __launch_bounds__(256) k_rej_table(const T* __restrict__ w, int6
     }
   }
   if (lane < kRejTabK && cnt) atomicAdd(tb.counts + lane, cnt);
+  status_or_warp(status, facc.flags());
 }
 
 // Steady state: every lane owns a slot; the gathers of batch k are issued,
@@ -1045,8 +1051,11 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
                              int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status,
                              const Workspace& ws, cudaStream_t s, int64_t s_begin, int64_t s_count, int32_t* claim) {
   if (s_count < 0) s_count = n - s_begin;
-  if (rng && rng->mode == PFR_RNG_NUMPY && s_begin == 0 && s_count == n)
+  if (rng && rng->mode == PFR_RNG_NUMPY && s_begin == 0 && s_count == n) {
+    cudaError_t e = launch_check_weights(w, n, dtype, status, s);  // check_weights' flags
+    if (e != cudaSuccess) return e;
     return launch_rejection_replay(w, n, dtype, bound, cap, rng, max_rounds, a, trips, out_w, status, ws, s);
+  }
   if (!rng || rng->mode != PFR_RNG_PHILOX) return cudaErrorNotSupported;
   unsigned long long* next = reinterpret_cast<unsigned long long*>(&ws.hdr->cell[2]);
   cudaError_t e = cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
@@ -1090,17 +1099,22 @@ cudaError_t launch_rejection(const void* w, int64_t n, int dtype, double bound, 
     const double cb = cap > 0 ? cap : bound;
     if (dtype == PFR_F64) {
       if (cap > 0)
-        k_rej_table<double, true><<<tblocks, 256, 0, s>>>((const double*)w, n, cb, cap, tb);
+        k_rej_table<double, true><<<tblocks, 256, 0, s>>>((const double*)w, n, cb, cap, tb, status);
       else
-        k_rej_table<double, false><<<tblocks, 256, 0, s>>>((const double*)w, n, cb, cap, tb);
+        k_rej_table<double, false><<<tblocks, 256, 0, s>>>((const double*)w, n, cb, cap, tb, status);
     } else {
       if (cap > 0)
-        k_rej_table<float, true><<<tblocks, 256, 0, s>>>((const float*)w, n, cb, cap, tb);
+        k_rej_table<float, true><<<tblocks, 256, 0, s>>>((const float*)w, n, cb, cap, tb, status);
       else
-        k_rej_table<float, false><<<tblocks, 256, 0, s>>>((const float*)w, n, cb, cap, tb);
+        k_rej_table<float, false><<<tblocks, 256, 0, s>>>((const float*)w, n, cb, cap, tb, status);
     }
     note_launch();
     use_tab = true;
+  }
+  if (!use_tab) {
+    // check_weights' flags (the table kernel reports them when it runs)
+    e = launch_check_weights(w, n, dtype, status, s);
+    if (e != cudaSuccess) return e;
   }
   const size_t tab_smem = use_tab ? (size_t)tb.words * 4 : 0;
   // measured (N=2^20, sigma=1, sup = max w): table kernel 8 trips per lane

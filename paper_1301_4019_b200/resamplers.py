@@ -267,7 +267,8 @@ def _rejection(w, bound, cap, rng, rng_mode, max_rounds, return_trips, index_dty
     bound = float(bound)
     if not math.isfinite(bound) or bound <= 0:
         raise ValueError(f"weight bound must be finite and positive, got {bound}")
-    w, st = _weights_checked(w, require_positive_total=False)
+    w = L.as_weights(w)
+    st = L.new_status()  # pfr_rejection reports check_weights' flags (the certain-reject table pass)
     n = w.numel()
     a = torch.empty(n, dtype=torch.int32, device=w.device)
     trips = torch.empty(n, dtype=torch.int32, device=w.device) if return_trips else None
@@ -413,11 +414,10 @@ def deliver(w, config: ResamplerConfig, rng, *, rng_mode=None, accum=None, index
         return (c, int(steps.item())) if return_max_steps else c
     if alg in ("rejection", "multinomial") and (rng_mode or L.config.rng_mode) == "philox":
         # fused: the resampler makes the permute's claims as it writes each slot
-        if alg == "rejection":
-            w, st = _weights_checked(w, require_positive_total=False)
-        else:
-            w = L.as_weights(w)
-            st = L.new_status()  # the weight scan reports check_weights' flags
+        # the resamplers report check_weights' flags themselves (the rejection
+        # table pass, the multinomial weight scan)
+        w = L.as_weights(w)
+        st = L.new_status()
         n = w.numel()
         c = out if out is not None else torch.empty(n, dtype=torch.int32, device=w.device)
         steps = torch.zeros(1, dtype=torch.int32, device=w.device) if return_max_steps else None
