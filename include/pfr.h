@@ -227,7 +227,9 @@ int pfr_metropolis(const void* w, int64_t n, int dtype, int64_t steps, const pfr
  * with cap > 0, rejection_ancestors_capped (258-279): v = min(w, cap),
  * bound = cap, out_w[i] = w[a[i]] / v[a[i]] (1 where v[a[i]] == 0).
  * trips (nullable) gets per-slot proposal counts; max_rounds bounds them
- * (the reference raises after 100000 rounds: NOPROGRESS). */
+ * (the reference raises after 100000 rounds: NOPROGRESS).  check_weights'
+ * flags (diagnostics.py:38-51) go to status: from the certain-reject table
+ * pass (4096 <= N <= 2^22, workspace with the O region) or a check pass. */
 int pfr_rejection(const void* w, int64_t n, int dtype, double bound, double cap, const pfr_rng* rng,
                   int64_t max_rounds, int32_t* a, int32_t* trips, void* out_w, uint32_t* status, void* ws,
                   size_t ws_bytes, void* stream);
